@@ -1,0 +1,190 @@
+"""ctypes binding of the C oracle -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2306_16688_b200``) never does; it shares no code with it.
+
+``ppo_step`` composes the C functions in the order of one trainer step
+(SURVEY.md §3.3): GAE per shard -> batch-wide normalisation over the union of the shards
+-> loss and gradient per shard (scale 1/N_global, summed in rank order, C-5) -> Adam.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with plain gcc (no fast-math: IEEE double semantics)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-Wall",
+                               "-o", _SO, _SRC, "-lm"])
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        d, i64, i32, u8 = C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_uint8)
+        f = C.POINTER(C.c_float)
+        ip = C.POINTER(C.c_int)
+        _lib.oracle_gae.argtypes = [C.c_int, C.c_int, C.c_int, f, f, u8, C.c_double, C.c_double, d, d]
+        _lib.oracle_moments.argtypes = [d, i64, d, d]
+        _lib.oracle_adv_norm.argtypes = [d, i64, C.c_double, C.c_int, d, d, d]
+        _lib.oracle_param_count.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip]
+        _lib.oracle_param_count.restype = i64
+        _lib.oracle_forward.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, d]
+        _lib.oracle_loss_and_grad.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, i32,
+                                              d, d, d, C.c_double, C.c_double, C.c_double,
+                                              C.c_double, d, d, d]
+        _lib.oracle_adam.argtypes = [i64, d, d, d, d, i64, C.c_double, C.c_double, C.c_double,
+                                     C.c_double]
+    return _lib
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def _ints(xs):
+    arr = (C.c_int * max(1, len(xs)))(*xs)
+    return arr
+
+
+# ------------------------------------------------------------------ C-1
+def gae(rewards, values, dones, gamma, lam):
+    """rewards/dones [T][ld], values [T+1][ld] -> (adv, ret) float64 [T][B=ld]."""
+    r = np.ascontiguousarray(rewards, dtype=np.float32)
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    dd = np.ascontiguousarray(dones, dtype=np.uint8)
+    T, ld = r.shape
+    assert v.shape == (T + 1, ld) and dd.shape == (T, ld)
+    adv = np.empty((T, ld), np.float64)
+    ret = np.empty((T, ld), np.float64)
+    lib().oracle_gae(T, ld, ld, _p(r, C.c_float), _p(v, C.c_float), _p(dd, C.c_uint8),
+                     gamma, lam, _p(adv, C.c_double), _p(ret, C.c_double))
+    return adv, ret
+
+
+# ------------------------------------------------------------------ C-2
+def moments(a):
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    mu, m2 = C.c_double(), C.c_double()
+    lib().oracle_moments(_p(a, C.c_double), a.size, C.byref(mu), C.byref(m2))
+    return mu.value, m2.value
+
+
+def adv_norm(a, eps=1e-8, unbiased=False):
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    out = np.empty_like(a)
+    mu, sd = C.c_double(), C.c_double()
+    lib().oracle_adv_norm(_p(a, C.c_double), a.size, eps, int(unbiased), _p(out, C.c_double),
+                          C.byref(mu), C.byref(sd))
+    return out, mu.value, sd.value
+
+
+# ------------------------------------------------------------------ C-3 / C-4
+def param_count(obs_dim, hidden, heads):
+    return lib().oracle_param_count(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads))
+
+
+def forward(obs_dim, hidden, heads, params, obs):
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    x = np.ascontiguousarray(obs, dtype=np.float64)[:, :obs_dim].copy()
+    n = x.shape[0]
+    out = np.empty((n, sum(heads) + 1), np.float64)
+    lib().oracle_forward(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads),
+                         _p(p, C.c_double), n, _p(x, C.c_double), _p(out, C.c_double))
+    return out
+
+
+def loss_and_grad(obs_dim, hidden, heads, params, obs, actions, logp_old, adv_hat, ret,
+                  clip_eps=0.2, value_coef=0.5, entropy_coef=0.01, grad_scale=None,
+                  grad=None, sums=None, want_per_sample=False):
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    x = np.ascontiguousarray(np.asarray(obs, dtype=np.float64)[:, :obs_dim])
+    n = x.shape[0]
+    act = np.ascontiguousarray(actions, dtype=np.int32).reshape(n, len(heads))
+    lo = np.ascontiguousarray(logp_old, dtype=np.float64).reshape(-1)
+    ah = np.ascontiguousarray(adv_hat, dtype=np.float64).reshape(-1)
+    rt = np.ascontiguousarray(ret, dtype=np.float64).reshape(-1)
+    if grad is None:
+        grad = np.zeros(p.size, np.float64)
+    if sums is None:
+        sums = np.zeros(5, np.float64)
+    if grad_scale is None:
+        grad_scale = 1.0 / n
+    ps = np.empty(n, np.float64) if want_per_sample else None
+    lib().oracle_loss_and_grad(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads),
+                               _p(p, C.c_double), n, _p(x, C.c_double), _p(act, C.c_int32),
+                               _p(lo, C.c_double), _p(ah, C.c_double), _p(rt, C.c_double),
+                               clip_eps, value_coef, entropy_coef, grad_scale,
+                               _p(grad, C.c_double), _p(sums, C.c_double),
+                               _p(ps, C.c_double) if ps is not None else None)
+    return grad, sums, ps
+
+
+# ------------------------------------------------------------------ C-6
+def adam(p, m, v, g, t, lr=3e-4, b1=0.9, b2=0.999, eps=1e-8):
+    """In place on float64 contiguous arrays."""
+    for a in (p, m, v):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    lib().oracle_adam(p.size, _p(p, C.c_double), _p(m, C.c_double), _p(v, C.c_double),
+                      _p(g, C.c_double), int(t), lr, b1, b2, eps)
+
+
+# ------------------------------------------------------------------ one trainer step
+def log_pi(cfg, params, obs, actions):
+    """log pi_theta(a|s) summed over heads, by the oracle forward (test-fixture helper)."""
+    z = forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, obs)
+    out = np.zeros(z.shape[0])
+    s = 0
+    for h, a in enumerate(cfg.heads):
+        zz = z[:, s:s + a]
+        mx = zz.max(axis=1, keepdims=True)
+        lsm = zz - (mx + np.log(np.exp(zz - mx).sum(axis=1, keepdims=True)))
+        out += lsm[np.arange(z.shape[0]), actions[:, h]]
+        s += a
+    return out
+
+
+def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, t=1,
+             apply=True):
+    """One trainer step of the oracle over K shards (list of dicts from synth.make_batch
+    with a ``logp_old`` entry).  Returns a dict with adv/ret per shard, mean/std, grad,
+    loss sums and (if apply) the updated params/m/v."""
+    advs, rets = [], []
+    for sh in shards:
+        a, r = gae(sh["rewards"], sh["values"], sh["dones"], cfg.gamma, cfg.lam)
+        advs.append(a.reshape(-1))
+        rets.append(r.reshape(-1))
+    allA = np.concatenate(advs)
+    N = allA.size
+    _, mu, sd = adv_norm(allA, eps=eps, unbiased=unbiased)
+    p64 = np.asarray(params, dtype=np.float64).copy()
+    grad = np.zeros(p64.size)
+    sums = np.zeros(5)
+    for sh, a, r in zip(shards, advs, rets):                 # rank order (C-5)
+        ahat = (a - mu) / (sd + eps)
+        loss_and_grad(cfg.obs_dim, cfg.hidden, cfg.heads, p64, sh["obs"], sh["actions"],
+                      sh["logp_old"], ahat, r, cfg.clip_eps, cfg.value_coef, cfg.entropy_coef,
+                      grad_scale=1.0 / N, grad=grad, sums=sums)
+    out = dict(adv=advs, ret=rets, mean=mu, std=sd, grad=grad, sums=sums, N=N)
+    if apply:
+        if adam_state is None:
+            adam_state = (np.zeros_like(p64), np.zeros_like(p64))
+        m, v = adam_state
+        adam(p64, m, v, grad, t, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps)
+        out.update(params=p64, m=m, v=v)
+    return out

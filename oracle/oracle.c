@@ -1,0 +1,225 @@
+/* oracle.c -- TEST INFRASTRUCTURE ONLY.  See oracle.h for the contract and citations.
+ *
+ * Plain C99 in double.  Every function is a direct transcription of a definition in
+ * DESIGN.md §3; there is no blocking, fusion or reordering beyond the
+ * definition, so it can be checked against the formulas by eye.  Pins: tests/test_oracle_*.py.
+ * Parity status per function: all pinned except the conventions listed
+ * there as "parity unpinned" (hyper-parameter defaults, sigma convention, head sizes, init).
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- C-1 GAE */
+void oracle_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
+                double gamma, double lambda, double* adv, double* ret) {
+  for (int b = 0; b < B; ++b) {
+    double A_next = 0.0;                         /* A_T = 0 */
+    for (int t = T - 1; t >= 0; --t) {
+      double m = 1.0 - (double)(d[(int64_t)t * ld + b] != 0);       /* m_t = 1 - d_t */
+      double r_t = r[(int64_t)t * ld + b];
+      double v_t = v[(int64_t)t * ld + b];
+      double v_n = v[(int64_t)(t + 1) * ld + b];
+      double delta = r_t + gamma * v_n * m - v_t;                  /* delta_t */
+      double A = delta + gamma * lambda * m * A_next;              /* A_t */
+      adv[(int64_t)t * B + b] = A;
+      ret[(int64_t)t * B + b] = A + v_t;                           /* R_t = A_t + v_t */
+      A_next = A;
+    }
+  }
+}
+
+/* ---------------------------------------------------------------- C-2 normalisation */
+void oracle_moments(const double* a, int64_t n, double* mean, double* m2) {
+  long double s = 0.0L;
+  for (int64_t i = 0; i < n; ++i) s += a[i];
+  long double mu = n > 0 ? s / (long double)n : 0.0L;
+  long double q = 0.0L;
+  for (int64_t i = 0; i < n; ++i) {
+    long double e = (long double)a[i] - mu;
+    q += e * e;
+  }
+  *mean = (double)mu;
+  *m2 = (double)q;
+}
+
+void oracle_adv_norm(const double* a, int64_t n, double eps, int unbiased,
+                     double* out, double* mean_out, double* std_out) {
+  double mu, m2;
+  oracle_moments(a, n, &mu, &m2);
+  double denom = unbiased ? (double)(n - 1) : (double)n;
+  double sigma = denom > 0 ? sqrt(m2 / denom) : 0.0;
+  for (int64_t i = 0; i < n; ++i) out[i] = (a[i] - mu) / (sigma + eps);
+  if (mean_out) *mean_out = mu;
+  if (std_out) *std_out = sigma;
+}
+
+/* ---------------------------------------------------------------- network helpers */
+static int n_actions(int H, const int* heads) {
+  int A = 0;
+  for (int h = 0; h < H; ++h) A += heads[h];
+  return A;
+}
+
+/* d[0] = obs_dim, d[1..L] = hidden, d[L+1] = A + 1 */
+static void layer_dims(int obs_dim, int L, const int* hidden, int H, const int* heads, int* d) {
+  d[0] = obs_dim;
+  for (int l = 0; l < L; ++l) d[l + 1] = hidden[l];
+  d[L + 1] = n_actions(H, heads) + 1;
+}
+
+int64_t oracle_param_count(int obs_dim, int L, const int* hidden, int H, const int* heads) {
+  int d[64];
+  layer_dims(obs_dim, L, hidden, H, heads, d);
+  int64_t P = 0;
+  for (int l = 0; l <= L; ++l) P += (int64_t)d[l + 1] * d[l] + d[l + 1];
+  return P;
+}
+
+/* y[l] for l = 0..L (y[0] = obs row), z = head output.  ys: (L+1) x maxw, z: A+1 */
+static void forward_one(int L, const int* d, const double* params, const double* x,
+                        double* ys, int maxw, double* z) {
+  memcpy(ys, x, sizeof(double) * d[0]);
+  int64_t off = 0;
+  for (int l = 0; l <= L; ++l) {
+    const double* W = params + off;                       /* W_l[out][in] */
+    const double* bias = W + (int64_t)d[l + 1] * d[l];    /* b_l[out] */
+    const double* in = ys + (int64_t)l * maxw;
+    double* outp = (l < L) ? ys + (int64_t)(l + 1) * maxw : z;
+    for (int o = 0; o < d[l + 1]; ++o) {
+      double acc = bias[o];
+      for (int i = 0; i < d[l]; ++i) acc += W[(int64_t)o * d[l] + i] * in[i];
+      outp[o] = (l < L) ? tanh(acc) : acc;                 /* tanh trunk, linear head */
+    }
+    off += (int64_t)d[l + 1] * d[l] + d[l + 1];
+  }
+}
+
+/* ---------------------------------------------------------------- C-3 forward */
+void oracle_forward(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                    const double* params, int64_t n, const double* obs, double* out) {
+  int d[64];
+  layer_dims(obs_dim, L, hidden, H, heads, d);
+  int maxw = 0;
+  for (int l = 0; l <= L + 1; ++l) maxw = d[l] > maxw ? d[l] : maxw;
+  double* ys = (double*)malloc(sizeof(double) * (size_t)(L + 1) * maxw);
+  for (int64_t i = 0; i < n; ++i)
+    forward_one(L, d, params, obs + i * obs_dim, ys, maxw, out + i * d[L + 1]);
+  free(ys);
+}
+
+/* ---------------------------------------------------------------- C-4 loss and gradient */
+void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                          const double* params, int64_t n, const double* obs,
+                          const int32_t* actions, const double* logp_old,
+                          const double* adv_hat, const double* ret,
+                          double clip_eps, double value_coef, double entropy_coef,
+                          double grad_scale, double* grad, double* sums, double* per_sample) {
+  int d[64];
+  layer_dims(obs_dim, L, hidden, H, heads, d);
+  const int A = d[L + 1] - 1;
+  int maxw = 0;
+  for (int l = 0; l <= L + 1; ++l) maxw = d[l] > maxw ? d[l] : maxw;
+  int64_t offs[64];
+  offs[0] = 0;
+  for (int l = 0; l <= L; ++l) offs[l + 1] = offs[l] + (int64_t)d[l + 1] * d[l] + d[l + 1];
+
+  double* ys = (double*)malloc(sizeof(double) * (size_t)(L + 1) * maxw);
+  double* z = (double*)malloc(sizeof(double) * (size_t)(A + 1));
+  double* lsm = (double*)malloc(sizeof(double) * (size_t)(A + 1));   /* log-softmax */
+  double* p = (double*)malloc(sizeof(double) * (size_t)(A + 1));
+  double* Hh = (double*)malloc(sizeof(double) * (size_t)(H > 0 ? H : 1));
+  double* delta = (double*)malloc(sizeof(double) * (size_t)maxw);
+  double* dy = (double*)malloc(sizeof(double) * (size_t)maxw);
+
+  for (int64_t i = 0; i < n; ++i) {
+    forward_one(L, d, params, obs + i * obs_dim, ys, maxw, z);
+
+    /* per-head log-softmax (max-subtracted), probabilities, log-prob, entropy */
+    double logpi = 0.0, ent = 0.0;
+    int s = 0;
+    for (int h = 0; h < H; ++h) {
+      double mx = z[s];
+      for (int j = 1; j < heads[h]; ++j) mx = z[s + j] > mx ? z[s + j] : mx;
+      double se = 0.0;
+      for (int j = 0; j < heads[h]; ++j) se += exp(z[s + j] - mx);
+      double lse = mx + log(se);
+      double hh = 0.0;
+      for (int j = 0; j < heads[h]; ++j) {
+        lsm[s + j] = z[s + j] - lse;
+        p[s + j] = exp(lsm[s + j]);
+        hh -= p[s + j] * lsm[s + j];
+      }
+      Hh[h] = hh;
+      ent += hh;
+      logpi += lsm[s + actions[i * H + h]];
+      s += heads[h];
+    }
+    const double Ah = adv_hat[i];
+    const double rho = exp(logpi - logp_old[i]);
+    const double rho_c = rho < 1.0 - clip_eps ? 1.0 - clip_eps
+                       : (rho > 1.0 + clip_eps ? 1.0 + clip_eps : rho);
+    const double s1 = rho * Ah, s2 = rho_c * Ah;
+    const double l_pg = -(s1 < s2 ? s1 : s2);
+    const double V = z[A];
+    const double l_v = (V - ret[i]) * (V - ret[i]);
+    const double loss_i = l_pg + value_coef * l_v - entropy_coef * ent;
+    if (per_sample) per_sample[i] = loss_i;
+    sums[0] += l_pg;
+    sums[1] += l_v;
+    sums[2] += ent;
+    sums[3] += fabs(rho - 1.0) > clip_eps ? 1.0 : 0.0;
+    sums[4] += logp_old[i] - logpi;
+
+    /* per-sample logit gradient (closed form, see header), times grad_scale = 1/N */
+    const double mask = (Ah >= 0.0) ? (rho <= 1.0 + clip_eps ? 1.0 : 0.0)
+                                    : (rho >= 1.0 - clip_eps ? 1.0 : 0.0);
+    s = 0;
+    for (int h = 0; h < H; ++h) {
+      for (int j = 0; j < heads[h]; ++j) {
+        double onehot = (j == actions[i * H + h]) ? 1.0 : 0.0;
+        double g = -mask * Ah * rho * (onehot - p[s + j])
+                   + entropy_coef * p[s + j] * (lsm[s + j] + Hh[h]);
+        delta[s + j] = grad_scale * g;
+      }
+      s += heads[h];
+    }
+    delta[A] = grad_scale * 2.0 * value_coef * (V - ret[i]);
+
+    /* backprop through the layers, l = L (head) down to 0 */
+    for (int l = L; l >= 0; --l) {
+      const double* W = params + offs[l];
+      double* gW = grad + offs[l];
+      double* gb = gW + (int64_t)d[l + 1] * d[l];
+      const double* in = ys + (int64_t)l * maxw;                /* y_l, input of layer l */
+      for (int o = 0; o < d[l + 1]; ++o) {
+        for (int k = 0; k < d[l]; ++k) gW[(int64_t)o * d[l] + k] += delta[o] * in[k];
+        gb[o] += delta[o];
+      }
+      if (l == 0) break;
+      for (int k = 0; k < d[l]; ++k) {
+        double acc = 0.0;
+        for (int o = 0; o < d[l + 1]; ++o) acc += delta[o] * W[(int64_t)o * d[l] + k];
+        dy[k] = acc;
+      }
+      for (int k = 0; k < d[l]; ++k) delta[k] = dy[k] * (1.0 - in[k] * in[k]);  /* tanh' */
+    }
+  }
+  free(ys); free(z); free(lsm); free(p); free(Hh); free(delta); free(dy);
+}
+
+/* ---------------------------------------------------------------- C-6 Adam */
+void oracle_adam(int64_t P, double* p, double* m, double* v, const double* g, int64_t t,
+                 double lr, double b1, double b2, double eps) {
+  const double bc1 = 1.0 - pow(b1, (double)t);
+  const double bc2 = 1.0 - pow(b2, (double)t);
+  for (int64_t i = 0; i < P; ++i) {
+    m[i] = b1 * m[i] + (1.0 - b1) * g[i];
+    v[i] = b2 * v[i] + (1.0 - b2) * g[i] * g[i];
+    double mhat = m[i] / bc1;
+    double vhat = v[i] / bc2;
+    p[i] -= lr * mhat / (sqrt(vhat) + eps);
+  }
+}

@@ -1,0 +1,77 @@
+/* oracle.h -- TEST INFRASTRUCTURE ONLY (not part of the product path).
+ *
+ * Plain, slow, obviously-correct CPU reference of SRL's trainer hot path
+ * (arXiv 2306.16688; §3.2.2 trainer workers, L885 §5 "we employ PPO").
+ * PAPER.md names PPO but states none of its equations; each function below follows the
+ * reading written in DESIGN.md §3, which takes the
+ * formulas from SPEC.md's `learning` module and the standard PPO/GAE algorithm.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load liboracle.so.  It shares no code, header, table or helper with the CUDA library.
+ * All arithmetic is double (long double for the batch moments); inputs arrive in the
+ * exact values the GPU path receives (fp32 arrays, fp16 observations widened exactly).
+ *
+ * Network (C-A9, C-A10): obs -> L tanh layers -> head of A+1 outputs (A = sum of the
+ * categorical head sizes, value last).  Flat parameter layout: for each layer l = 1..L+1,
+ * W_l[out][in] row-major, then b_l[out]; head rows ordered head 0 .. head H-1, value last.
+ */
+#ifndef SRL_ORACLE_H
+#define SRL_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* C-1  GAE by the backward recursion (BASELINE.json north_star):
+ *   m_t = 1 - d_t;  delta_t = r_t + gamma * v_{t+1} * m_t - v_t;
+ *   A_t = delta_t + gamma * lambda * m_t * A_{t+1},  A_T = 0;   R_t = A_t + v_t  (C-A1, C-A3).
+ * r, d: [T][ld], v: [T+1][ld] (row T = bootstrap value).  adv, ret: dense [T][B]. */
+void oracle_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
+                double gamma, double lambda, double* adv, double* ret);
+
+/* C-2  batch moments, two-pass in long double: mean, and M2 = sum (a - mean)^2. */
+void oracle_moments(const double* a, int64_t n, double* mean, double* m2);
+
+/* C-2  advantage normalisation (C-A4): sigma = sqrt(M2 / n) (population,
+ * unbiased=0) or sqrt(M2 / (n-1)) (unbiased=1);  out_i = (a_i - mean) / (sigma + eps). */
+void oracle_adv_norm(const double* a, int64_t n, double eps, int unbiased,
+                     double* out, double* mean_out, double* std_out);
+
+/* number of parameters of the network */
+int64_t oracle_param_count(int obs_dim, int L, const int* hidden, int H, const int* heads);
+
+/* C-3  forward: per sample, naive dense layers in double.
+ * obs: [n][obs_dim] (dense).  out: [n][A+1] = (logits..., value). */
+void oracle_forward(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                    const double* params, int64_t n, const double* obs, double* out);
+
+/* C-4  PPO loss and its exact gradient (C-A5..C-A7):
+ *   per head h: l^h = logsoftmax(z^h) (max-subtracted), p^h = exp(l^h);
+ *   logpi = sum_h l^h[a_h];  H = sum_h -sum_j p^h_j l^h_j;  rho = exp(logpi - logp_old);
+ *   loss_i = -min(rho*A, clip(rho, 1-eps, 1+eps)*A) + c_v (V - R)^2 - c_e H.
+ * The mean loss of the batch is sum_i loss_i / N with N = the GLOBAL sample count; the
+ * gradient of that mean w.r.t. every parameter, restricted to these n samples, is ADDED to
+ * grad[P] with grad_scale = 1/N (so K shards summed in rank order give the K=1 gradient).
+ * Per-sample logit gradient (derivative of loss_i):
+ *   d/dz^h_j = -mask*A*rho*(1[j=a_h] - p^h_j) + c_e p^h_j (l^h_j + H^h),
+ *   mask = (A >= 0 ? rho <= 1+eps : rho >= 1-eps) (inclusive, C-A6);  d/dV = 2 c_v (V - R).
+ * sums[5] += { sum loss_pg, sum (V-R)^2, sum H, sum 1[|rho-1| > eps], sum (logp_old - logpi) }.
+ * adv_hat: advantages already normalised.  per_sample (nullable): [n] loss_i. */
+void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                          const double* params, int64_t n, const double* obs,
+                          const int32_t* actions, const double* logp_old,
+                          const double* adv_hat, const double* ret,
+                          double clip_eps, double value_coef, double entropy_coef,
+                          double grad_scale, double* grad, double* sums, double* per_sample);
+
+/* C-6  Adam (C-A13), PyTorch semantics, step t >= 1:
+ *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
+ *   p -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps). */
+void oracle_adam(int64_t P, double* p, double* m, double* v, const double* g, int64_t t,
+                 double lr, double b1, double b2, double eps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
