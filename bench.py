@@ -1,0 +1,386 @@
+#!/usr/bin/env python3
+"""Benchmark: PPO trainer samples/sec for the whole hot path (GAE -> normalisation ->
+forward -> loss -> backward -> allreduce -> Adam) on synthetic Atari-shaped batches.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config atari] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Scaling is weak: every rank trains its own full config-shaped shard (T x B columns); the
+ranks' shards are disjoint column blocks of one global batch, normalised globally and
+reduced by one NCCL allreduce of the gradient bucket per step.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "PPO trainer samples/sec (GAE+update, device-timed) at 1/2/4/8 B200"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="atari")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps (capped at 100)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_ids):
+        self.ids = ",".join(str(i) for i in gpu_ids)
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", self.ids, "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.monotonic(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self, t0, t1):
+        win = [s for t, s in self.samples if t0 - 0.06 <= t <= t1 + 0.06]
+        note = "timed-region samples"
+        if not win:
+            win = [s for _, s in self.samples]
+            note = "no sample inside the timed region; samples from the whole run"
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "note": "nvidia-smi unavailable"}
+        sm = [float(s[1]) for s in win if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in win if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in win for k in range(4) if s[4 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(win), "note": note}
+
+
+# ------------------------------------------------------------------ CPU oracle
+def time_oracle(cfg, budget_s, params=None):
+    """The oracle (as it stands, 1 thread) on a bounded sample of the workload: T x B' columns
+    with B' chosen so the run takes about budget_s.  Returns (samples/s, n, B', seconds)."""
+    import oracle
+    import synth
+    if params is None:
+        params = synth.make_params(cfg, 0)
+
+    def run(Bp):
+        c = cfg.with_(B=Bp * cfg.agents)
+        b = synth.make_batch(c, seed=0)
+        b["logp_old"] = synth.logp_old_uniform_policy(c, b["xi"])
+        t = time.perf_counter()
+        oracle.ppo_step(c, params, [b], apply=True)
+        return time.perf_counter() - t, b["n"]
+
+    t1, n1 = run(1)
+    Bp = int(max(1, min(cfg.B // cfg.agents, round(budget_s / max(t1, 1e-6)))))
+    if Bp == 1:
+        return n1 / t1, n1, 1, t1
+    t, n = run(Bp)
+    return n / t, n, Bp, t
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the oracle as it stands, on this box's host cores, same metric/unit."""
+    import synth
+    cfg = synth.get_config(args.config)
+    if rank != 0:
+        return
+    per_step = max(0.2, 150.0 / max(1, args.steps + args.warmup))
+    import oracle
+    params = synth.make_params(cfg, 0)
+    # calibrate one column, then size the per-step sample
+    _, _, _, t1 = time_oracle(cfg, 0.0, params)
+    Bp = int(max(1, min(cfg.B // cfg.agents, per_step / max(t1, 1e-6))))
+    c = cfg.with_(B=Bp * cfg.agents)
+    b = synth.make_batch(c, seed=0)
+    b["logp_old"] = synth.logp_old_uniform_policy(c, b["xi"])
+    st = None
+    for _ in range(args.warmup):
+        oracle.ppo_step(c, params, [b], apply=True)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        oracle.ppo_step(c, params, [b], apply=True, t=k + 1)
+    dt = time.perf_counter() - t0
+    value = b["n"] * args.steps / dt
+    sample = (f"{cfg.name}-shaped T={cfg.T}, B'={Bp * cfg.agents} columns ({b['n']} samples) per "
+              f"step, full network, GAE+norm+loss/grad+Adam, C double, 1 thread")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": cfg.name, "T": cfg.T, "B_per_step": Bp * cfg.agents},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main_ours(args, world, rank, local):
+    import torch
+    import synth
+    import paper_2306_16688_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+
+    cfg = synth.get_config(args.config)
+    gcfg = cfg.with_(B=cfg.B * world)          # weak scaling: one config-sized shard per rank
+    b = synth.make_batch(gcfg, seed=0, world=world, rank=rank)
+    b["logp_old"] = synth.logp_old_uniform_policy(cfg, b["xi"])
+    n = b["n"]
+    N = n * world
+    params = torch.from_numpy(synth.make_params(cfg, 0)).to(dev)
+    keys = ("rewards", "values", "dones", "obs", "actions", "logp_old")
+    host = {k: torch.from_numpy(np.ascontiguousarray(b[k])).pin_memory() for k in keys}
+    d = {k: host[k].to(dev) for k in keys}
+    h2d_bytes = sum(host[k].numel() * host[k].element_size() for k in keys)
+
+    nccl_id = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    ctx = P.PPOContext(P.NetSpec.from_config(cfg), max_local_n=n, rank=rank, world=world,
+                       nccl_id=nccl_id, device=local)
+    ctx.load_params(params)
+    T, Bk = b["rewards"].shape
+    adv = torch.empty(T, Bk, dtype=torch.float32, device=dev)
+    ret = torch.empty_like(adv)
+    gst = torch.empty(3, dtype=torch.float64, device=dev)
+    ms = torch.empty(2, dtype=torch.float64, device=dev)
+    stats = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8, device=dev)
+    stats_host = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8).pin_memory()
+    stream = torch.cuda.current_stream()
+    gae_ev = []
+
+    def step(src, timed_gae=False):
+        if timed_gae:
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+        P.gae(src["rewards"], src["values"], src["dones"], cfg.gamma, cfg.lam, adv=adv, ret=ret, stats=gst)
+        if timed_gae:
+            e1.record()
+        P.adv_norm(adv.view(-1), local_stats=gst, ctx=ctx, mean_std=ms)
+        if timed_gae:
+            e2.record()
+            gae_ev.append((e0, e1, e2))
+        ctx.step(N, src["obs"], src["actions"], src["logp_old"], adv.view(-1), ret.view(-1), ms,
+                 apply=True, stats=stats)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        step(d)
+    barrier()
+    sampler = ClockSampler(range(world)) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    # ---------------- timed region: device-resident inputs (working set > L2: see config)
+    K = args.steps
+    ctx.prof_reset()
+    ctx.profile(True)
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    wall0 = time.monotonic()
+    e_start.record()
+    for _ in range(K):
+        step(d, timed_gae=True)
+    e_end.record()
+    barrier()
+    wall1 = time.monotonic()
+    ctx.profile(False)
+    ms_total = max_over_ranks(e_start.elapsed_time(e_end))
+    recs = ctx.prof_records()
+    gae_ms = [a.elapsed_time(b_) for a, b_, _ in gae_ev]
+    norm_ms = [b_.elapsed_time(c) for _, b_, c in gae_ev]
+    stats_dev = P.decode_stats(stats)
+
+    # ---------------- end to end: host (pinned) inputs copied in, stats copied out, per step
+    Ke = args.e2e_steps or min(K, 100)
+    for _ in range(2):
+        dd = {k: host[k].to(dev, non_blocking=True) for k in keys}
+        step(dd)
+        stats_host.copy_(stats, non_blocking=True)
+    barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record()
+    for _ in range(Ke):
+        dd = {k: host[k].to(dev, non_blocking=True) for k in keys}
+        step(dd)
+        stats_host.copy_(stats, non_blocking=True)
+    x1.record()
+    barrier()
+    e2e_ms = max_over_ranks(x0.elapsed_time(x1))
+    if sampler:
+        time.sleep(0.1)
+        sampler.stop()
+
+    if dist:
+        dist.barrier()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- per-kernel table and the dominant kernel's roofline
+    import math
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    tf_sus = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    peak_src = "measured" if peaks else "fallback"
+    agg = {}
+    for name, t, fl, by in recs:
+        a = agg.setdefault(name, [0.0, 0, 0.0, 0.0])
+        a[0] += t; a[1] += 1; a[2] += fl; a[3] += by
+    agg["gae_scan"] = [sum(gae_ms), len(gae_ms), 0.0, 17.0 * n * len(gae_ms)]
+    agg["adv_norm"] = [sum(norm_ms), len(norm_ms), 0.0, 0.0]
+    step_ms = ms_total / K
+    kernels = []
+    for name, (t, cnt, fl, by) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+        avg = t / max(cnt, 1)
+        row = {"name": name, "ms_per_step": t / K, "share": (t / K) / step_ms, "launches_per_step": cnt / K}
+        if fl > 0:
+            row.update(tflops=fl / cnt / (avg * 1e-3) / 1e12, frac_tensor=fl / cnt / (avg * 1e-3) / 1e12 / tf_sus)
+        if by > 0:
+            row.update(gbs=by / cnt / (avg * 1e-3) / 1e9, frac_hbm=by / cnt / (avg * 1e-3) / 1e9 / hbm)
+        kernels.append(row)
+    dom = max(((k, v) for k, v in agg.items() if v[2] > 0), key=lambda kv: kv[1][0])
+    dname, (dt, dcnt, dfl, dby) = dom
+    davg_s = dt / dcnt * 1e-3
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(args.config, {}).get(dname)
+    except Exception:
+        pass
+    achieved = dfl / dcnt / davg_s / 1e12
+    roofline = {"bound": "tensor", "kernel": dname, "achieved": achieved, "peak": tf_sus,
+                "unit": "TFLOP/s", "frac": achieved / tf_sus, "traffic": traffic,
+                "peak_source": f"{peak_src} bf16_tflops_sustained (fp16 dense = bf16 dense, nominal ratio 1)",
+                "flops_per_launch": dfl / dcnt, "ms_per_launch": davg_s * 1e3}
+    # our kernels per step: gae_kernel + merge (srl_gae), merge (srl_adv_norm), the ppo step's
+    # 3L+2 GEMMs, finalize_w + finalize_b + extras, adam, stats (NCCL's kernels not counted)
+    L = len(cfg.hidden)
+    per_step = 2 + 1 + (L + 1 + (L + 1) + L) + 3 + 1 + 1
+    cpu = None
+    if not args.no_cpu_baseline:
+        v, cn, Bp, secs = time_oracle(cfg, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{cfg.name}-shaped T={cfg.T}, B'={Bp * cfg.agents} columns ({cn} samples; "
+                         f"{secs:.1f} s), full network, GAE+norm+loss/grad+Adam, C double, 1 thread"}
+    clocks = sampler.summary(wall0, wall1) if sampler else None
+    out = {
+        "metric": METRIC, "value": N * K / (ms_total * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "T": cfg.T, "B_per_rank": cfg.B, "obs_dim": cfg.obs_dim,
+                   "hidden": list(cfg.hidden), "heads": list(cfg.heads), "samples_per_step": N,
+                   "frames_per_step": N * cfg.frame_skip, "parallelism": f"dp{world}",
+                   "l2": "no flush: per-step working set > L2 (obs %.0f MB + activations %.0f MB + "
+                         "dZ %.0f MB per rank vs 126 MB L2)" % (
+                             n * cfg.ld_obs * 2 / 1e6, n * sum(cfg.hidden) * 2 / 1e6,
+                             n * max(cfg.hidden) * 4 / 1e6)},
+        "frames_per_s": N * cfg.frame_skip * K / (ms_total * 1e-3),
+        "e2e": {"value": N * Ke / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes * world,
+                "d2h_bytes_per_step": P.srl.STATS_BYTES * world, "steps": Ke},
+        "gpu_launches": per_step * K,
+        "roofline": roofline,
+        "kernels": kernels,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "last_stats": {k: stats_dev[k] for k in ("loss", "policy_loss", "value_loss", "entropy",
+                                                 "clip_fraction", "nonfinite", "step")},
+    }
+    if any(math.isnan(x) for x in (out["value"],)):
+        raise SystemExit("nan throughput")
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+        return
+    if args.gpus > 1 and world == 1:
+        raise SystemExit("--gpus N > 1: launch with torchrun --nproc-per-node N (one rank per GPU)")
+    main_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/* srl.h -- C ABI of the B200-native SRL trainer hot path (libsrl.so, sm_100a).
+ *
+ * The method: one PPO update of SRL's trainer worker on a batch of trajectories
+ * (arXiv 2306.16688, §3.2.2 "Trainer workers": aggregate a batch, load it
+ * to the GPU, compute a gradient step; multi-trainer SPMD with gradient synchronisation at
+ * the end of every iteration; L885 §5: the algorithm is PPO).  PAPER.md does not write the
+ * PPO/GAE equations; the readings used here are DESIGN.md §3 (from SPEC.md S:L593-611 and
+ * BASELINE.json north_star).  The calls follow SPEC.md's statement of the problem:
+ *   gae -> srl_gae;  advantage normalisation -> srl_adv_norm;
+ *   backward/ppo_step -> srl_ppo_step;  reduce_gradients ->
+ *   srl_allreduce_grads.  srl_ppo_step mirrors Algorithm.step(sample) -> {'loss': ...}
+ *   plus inc_version() of PAPER.md Code 1 (L649-654).
+ *
+ * Conventions (all entry points):
+ *  - Pointers named *_dev / documented "device" are CUDA device pointers on the context's
+ *    device (or the current device for ctx-less calls).  All work is enqueued on `stream`
+ *    (stream-ordered, no host synchronisation); the caller keeps every buffer alive until
+ *    that work completes.  The caller owns every batch buffer and the stream; a context owns
+ *    its parameters, optimiser state, gradient bucket, workspace and communicator.
+ *  - Argument validation (null pointers, shapes, strides, alignment, capacity) is done on
+ *    the host before any launch; failure returns SRL_EINVAL and nothing is enqueued.
+ *    srl_last_error() returns a thread-local message for the last non-OK status.
+ *  - There is no CPU fallback: without a CUDA device every compute call returns SRL_ECUDA.
+ *  - A context is single-owner: no concurrent calls on one context.
+ */
+#ifndef SRL_H
+#define SRL_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* srl_stream_t;     /* == cudaStream_t; NULL = legacy default stream */
+typedef struct srl_ctx srl_ctx;
+
+typedef enum srl_status {
+  SRL_OK = 0,
+  SRL_EINVAL = 1,        /* bad argument: null pointer, shape, stride, alignment, n > max_local_n */
+  SRL_ECUDA = 2,         /* CUDA runtime / launch failure, or no device */
+  SRL_ENCCL = 3,         /* NCCL failure */
+  SRL_ENOMEM = 4,        /* device allocation failed */
+  SRL_EUNSUPPORTED = 5,  /* valid request this build does not implement */
+  SRL_ESTATE = 6         /* call not valid in the context's state */
+} srl_status;
+
+const char* srl_last_error(void);
+int srl_abi_version(void);                    /* 1 */
+
+/* ---------------------------------------------------------------- a1: GAE
+ * Generalised advantage estimation over time-major columns (SPEC.md S:L593-601,
+ * BASELINE.json north_star, readings C-A1/C-A3).  For each column b and
+ * t = T-1 .. 0, with m_t = 1 - d_t:
+ *     delta_t = r_t + gamma * v_{t+1} * m_t - v_t,   A_t = delta_t + gamma*lambda*m_t*A_{t+1},
+ *     A_T = 0,   R_t = A_t + v_t.
+ * d_t = 1 means the episode ended AT transition t: it cuts v_{t+1} and A_{t+1}.
+ *   rewards  device f32 [T][ld]          values device f32 [T+1][ld] (row T = bootstrap)
+ *   dones    device u8  [T][ld] (0/1)    adv_out device f32 [T][ld]   ret_out f32 [T][ld] or NULL
+ *   stats_out device f64 [3] or NULL: {n, mean, M2} of adv over the T*B entries (M2 = sum of
+ *             squared deviations), the input srl_adv_norm takes as local_stats.
+ * Layout: element (t, b) at t*ld + b; ld >= B.  With ld == B the outputs are the dense
+ * sample-major vectors srl_ppo_step consumes (sample i = t*B + b).  T >= 1, B >= 1.
+ * Columns are independent: a rank passes its own block of columns. */
+srl_status srl_gae(int T, int B, int ld, const float* rewards, const float* values,
+                   const uint8_t* dones, float gamma, float lambda,
+                   float* adv_out, float* ret_out, double* stats_out, srl_stream_t stream);
+
+/* ---------------------------------------------------------------- a2: normalisation
+ * Batch-wide advantage normalisation (C-A4):
+ *     mu, sigma over ALL samples of ALL ranks of ctx (ctx == NULL: this buffer only);
+ *     sigma = sqrt(M2 / N) (unbiased = 0, default) or sqrt(M2 / (N-1)) (unbiased = 1);
+ *     A_hat_i = (A_i - mu) / (sigma + eps).
+ *   adv         device f32 [n]; normalised in place iff apply != 0.
+ *   local_stats device f64 [3] {n, mean, M2} of this rank's adv (from srl_gae), or NULL to
+ *               compute them here (warp-shuffle + block reduction over adv).
+ *   mean_std_out device f64 [2] {mu, sigma} or NULL.
+ * With ctx != NULL and world > 1 the ranks' {n, mean, M2} are all-gathered (NCCL) and merged
+ * in rank order (Chan et al.), so mu and sigma are bit-identical on all ranks. */
+srl_status srl_adv_norm(srl_ctx* ctx, float* adv, int64_t n, const double* local_stats,
+                        float eps, int unbiased, int apply, double* mean_std_out,
+                        srl_stream_t stream);
+
+/* ---------------------------------------------------------------- a3-a7: model context */
+typedef enum srl_precision {
+  SRL_PREC_F16_SCALED = 0   /* fp16 GEMM operands, fp32 accumulate (TMEM), per-sample dZ */
+} srl_precision;
+
+typedef struct srl_ppo_config {
+  int obs_dim;              /* observation width (>= 1) */
+  int ld_obs;               /* fp16 row stride of obs, >= obs_dim, % 8 == 0 (16-B rows) */
+  int n_hidden;             /* L >= 1 tanh layers */
+  const int* hidden;        /* [L] widths, each a multiple of 64 in [64, 1024] */
+  int n_heads;              /* H >= 1 categorical heads (C-A8) */
+  const int* head_sizes;    /* [H]; sum + 1 (value column) <= 64 */
+  float clip_eps, value_coef, entropy_coef;   /* 0.2, 0.5, 0.01 (C-A5) */
+  float lr, beta1, beta2, adam_eps;           /* 3e-4, 0.9, 0.999, 1e-8 (C-A13) */
+  float adv_eps;            /* 1e-8: A_hat = (A - mu) / (sigma + adv_eps) inside the loss */
+  int64_t max_local_n;      /* workspace sizing: largest n_local passed to srl_ppo_step */
+  int precision;            /* srl_precision */
+} srl_ppo_config;
+
+/* Device-resident statistics written by srl_ppo_step (global means over n_global). */
+typedef struct srl_ppo_stats {
+  double policy_loss;       /* mean -min(rho A, clip(rho) A) */
+  double value_loss;        /* mean (V - R)^2 (before value_coef) */
+  double entropy;           /* mean sum-over-heads entropy */
+  double clip_fraction;     /* mean 1[|rho - 1| > eps] */
+  double approx_kl;         /* mean (logp_old - logpi) */
+  double loss;              /* policy_loss + value_coef*value_loss - entropy_coef*entropy */
+  double adv_mean, adv_std; /* the normalisation used */
+  int64_t n_global;
+  int64_t nonfinite;        /* non-finite per-sample losses + gradient entries (all ranks) */
+  int64_t fp16_saturated;   /* fp16 stores clamped to +-65504 (all ranks) */
+  int64_t step;             /* Adam step t after this call = policy version (Code 1 inc_version) */
+} srl_ppo_stats;
+
+/* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller. */
+srl_status srl_nccl_unique_id(uint8_t out[128]);
+
+/* Create a context on CUDA device `device` for rank `rank` of `world`.  nccl_id must be the
+ * same 128 bytes on every rank (NULL iff world == 1).  Parameters are zero until
+ * srl_ppo_load_params.  Layout of the flat parameter vector (C-A10): for
+ * l = 1..L+1, W_l[out][in] row-major then b_l[out]; head rows head 0 .. head H-1, value last. */
+srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int world,
+                          const uint8_t* nccl_id, int device, srl_ctx** out);
+srl_status srl_ppo_destroy(srl_ctx* ctx);
+
+/* Context-owned device buffers: params f32 [P] (fp32 master), grads f32 [P + 8] (the
+ * gradient bucket: P gradient entries then 8 reduced statistics), Adam m and v f32 [P].
+ * layout_digest = FNV-1a-64 over the int32 dims and head sizes. */
+srl_status srl_ppo_params(srl_ctx* ctx, float** params_dev, float** grads_dev, int64_t* P,
+                          uint64_t* layout_digest);
+srl_status srl_ppo_adam_state(srl_ctx* ctx, float** m_dev, float** v_dev, int64_t* step);
+
+/* Copy P f32 parameters (device pointer) into the context, reset Adam (m = v = 0, t = 0)
+ * and refresh the fp16 weight shadows the GEMMs read. */
+srl_status srl_ppo_load_params(srl_ctx* ctx, const float* params_dev, srl_stream_t stream);
+
+/* One PPO update on this rank's samples (rows a3 -> a4 -> a5 -> a6 -> a7 of DESIGN.md §2):
+ * forward, clipped-surrogate + value + entropy loss, backward,
+ * gradient allreduce over the ctx's ranks, Adam.  Mean loss over n_global samples.
+ *   obs       device f16 bits [n_local][ld_obs]      actions device i32 [n_local][H]
+ *   logp_old  device f32 [n_local]                     adv device f32 [n_local] (raw A)
+ *   ret       device f32 [n_local] (R = A + v)
+ *   adv_mean_std device f64 [2] {mu, sigma} from srl_adv_norm (advantages normalised inside
+ *             the loss kernel), or NULL if adv is already normalised.
+ *   apply     1: full update.  0: stop after the backward pass: grads_dev holds this rank's
+ *             gradient of (sum of its per-sample losses) / n_global, no communication, no
+ *             Adam (SPEC backward).
+ *   stats_out device srl_ppo_stats* or NULL.
+ * n_local <= max_local_n, n_local >= 1, n_global >= n_local. */
+srl_status srl_ppo_step(srl_ctx* ctx, int64_t n_local, int64_t n_global,
+                        const uint16_t* obs, const int32_t* actions, const float* logp_old,
+                        const float* adv, const float* ret, const double* adv_mean_std,
+                        int apply, srl_ppo_stats* stats_out, srl_stream_t stream);
+
+/* a6: in-place allreduce over the ctx's ranks of a device f32 buffer (SPEC reduce_gradients
+ * S:L505-513): op 0 = sum, op 1 = mean.  world == 1: identity (op 1 leaves values as is). */
+srl_status srl_allreduce_grads(srl_ctx* ctx, float* buf, int64_t count, int op,
+                               srl_stream_t stream);
+
+/* ---------------------------------------------------------------- profiling
+ * With profiling on, srl_ppo_step records a CUDA event pair on its stream around every
+ * kernel (or collective) it launches, with that launch's algorithmic FLOPs and HBM bytes
+ * (DESIGN.md §5).  srl_prof_read(i) waits for record i and returns its name (static string),
+ * duration in ms and the two algorithmic counts.  srl_prof_reset drops all records. */
+srl_status srl_prof_enable(srl_ctx* ctx, int on);
+srl_status srl_prof_reset(srl_ctx* ctx);
+int srl_prof_count(srl_ctx* ctx);
+srl_status srl_prof_read(srl_ctx* ctx, int i, const char** name, float* ms, double* flops,
+                         double* bytes);
+
+/* ---------------------------------------------------------------- test hook
+ * D[M][N] (device f32, dense) = sum_k A(m,k) * B(n,k) through the tcgen05 GEMM core with
+ * its split-K epilogue (the dW path of a5).  A: a_mn == 0 -> fp16 [M][lda] (K contiguous),
+ * a_mn == 1 -> fp16 [K][lda] (M contiguous); B likewise with N.  lda, ldb % 8 == 0.
+ * bn in {64, 128, 256} is the N tile; splits >= 1 the K split count.  Used by tests only. */
+srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int a_mn, int lda,
+                          const uint16_t* B, int b_mn, int ldb, int bn, int splits, float* D,
+                          srl_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

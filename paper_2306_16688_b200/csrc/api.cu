@@ -1,0 +1,665 @@
+// api.cu -- the C ABI of include/srl.h: validation, the model context, the step schedule
+// and the NCCL plumbing (a6).  Every compute step runs in this library's kernels.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "srl.h"
+
+namespace srl {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+}  // namespace srl
+
+using namespace srl;
+
+#define FAIL(code, msg)            \
+  do {                             \
+    set_error(msg);                \
+    return code;                   \
+  } while (0)
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess)                                                          \
+      FAIL(SRL_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));              \
+  } while (0)
+#define CKN(x)                                                                      \
+  do {                                                                              \
+    ncclResult_t r_ = (x);                                                          \
+    if (r_ != ncclSuccess) FAIL(SRL_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+static srl_status require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    FAIL(SRL_ECUDA, "no CUDA device (libsrl has no CPU fallback)");
+  return SRL_OK;
+}
+
+extern "C" const char* srl_last_error(void) { return g_err.c_str(); }
+extern "C" int srl_abi_version(void) { return 1; }
+
+// ------------------------------------------------------------------ a1
+extern "C" srl_status srl_gae(int T, int B, int ld, const float* rewards, const float* values,
+                              const uint8_t* dones, float gamma, float lambda, float* adv_out,
+                              float* ret_out, double* stats_out, srl_stream_t stream) {
+  if (T < 1 || B < 1 || ld < B) FAIL(SRL_EINVAL, "srl_gae: need T >= 1, B >= 1, ld >= B");
+  if (!rewards || !values || !dones || !adv_out) FAIL(SRL_EINVAL, "srl_gae: null pointer");
+  if (srl_status st = require_device()) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  double* part = nullptr;
+  const int nb = gae_num_blocks(B);
+  if (stats_out) CK(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * 3 * nb, s));
+  CK(launch_gae(T, B, ld, rewards, values, dones, gamma, lambda, adv_out, ret_out, part, s));
+  if (stats_out) {
+    CK(launch_merge_moments(part, nb, stats_out, nullptr, 0, s));
+    CK(cudaFreeAsync(part, s));
+  }
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ context
+struct Lay {
+  int in, out;             // out = A+1 for the head
+  int64_t w_off, b_off;    // flat offsets
+  __half* w16;
+  int w16_ld, w16_rows;
+  int bn_fwd;              // N tile of the GEMM producing this layer's output (fwd)
+  int bn_dx;               // N tile of the dX GEMM that produces dZ of this layer's INPUT
+  int bn_dw, dw_n_tiles, dw_m_tiles, splits_max;
+  float* part;             // dW partials [splits][out or in][ld_part]
+  int64_t part_rows, ld_part;
+  float* colsum;           // db partials of this layer: [sms][4][out] (hidden) / [sms][4][64] (head)
+  int colsum_ld;
+};
+
+struct srl_ctx {
+  int device = 0, rank = 0, world = 1, sms = 148;
+  srl_ppo_config cfg{};
+  std::vector<int> hidden, heads, dims;
+  int L = 0, A = 0;
+  int64_t P = 0, max_n = 0;
+  uint64_t digest = 0;
+  std::vector<Lay> lay;
+  float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr;
+  int64_t* t_dev = nullptr;
+  std::vector<__half*> Y;
+  __half* G16 = nullptr;
+  __half* dZ[2] = {nullptr, nullptr};
+  double* stats_part = nullptr;
+  unsigned long long* counters = nullptr;
+  double* norm_scratch = nullptr;   // [world*3] gathered + [3] merged
+  ncclComm_t comm = nullptr;
+  std::vector<void*> allocs;
+  // profiling (srl_prof_*): an event pair around every kernel srl_ppo_step launches
+  struct ProfRec { const char* name; cudaEvent_t a, b; double flops, bytes; };
+  bool prof = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+};
+
+static cudaEvent_t prof_event(srl_ctx* c) {
+  if (c->pool_used == c->pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->pool.push_back(e);
+  }
+  return c->pool[c->pool_used++];
+}
+
+struct ProfScope {
+  srl_ctx* c; cudaStream_t s; const char* name; double flops, bytes; cudaEvent_t a = nullptr;
+  ProfScope(srl_ctx* c_, cudaStream_t s_, const char* n, double f, double b)
+      : c(c_), s(s_), name(n), flops(f), bytes(b) {
+    if (c->prof) { a = prof_event(c); cudaEventRecord(a, s); }
+  }
+  ~ProfScope() {
+    if (c->prof) {
+      cudaEvent_t b2 = prof_event(c);
+      cudaEventRecord(b2, s);
+      c->recs.push_back({name, a, b2, flops, bytes});
+    }
+  }
+};
+
+static int pick_bn(int n) {
+  if (n % 256 == 0) return 256;
+  if (n <= 64) return 64;
+  if (n % 128 == 0 || n <= 128) return 128;
+  return 128;
+}
+
+static uint64_t fnv1a(const std::vector<int>& xs) {
+  uint64_t h = 1469598103934665603ull;
+  for (int x : xs) {
+    int32_t v = x;
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(&v);
+    for (int i = 0; i < 4; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+  }
+  return h;
+}
+
+template <class T>
+static srl_status dalloc(srl_ctx* c, T** p, size_t bytes) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+  if (e != cudaSuccess) FAIL(SRL_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  cudaMemset(q, 0, bytes ? bytes : 16);
+  c->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return SRL_OK;
+}
+
+static void free_ctx(srl_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+}
+
+extern "C" srl_status srl_nccl_unique_id(uint8_t out[128]) {
+  if (!out) FAIL(SRL_EINVAL, "srl_nccl_unique_id: null");
+  ncclUniqueId id;
+  CKN(ncclGetUniqueId(&id));
+  std::memcpy(out, id.internal, 128);
+  return SRL_OK;
+}
+
+static SegTable make_segs(srl_ctx* c, const std::vector<int>& splits,
+                          const std::vector<int>& colsum_parts) {
+  SegTable t{};
+  t.n = 0;
+  for (int l = 0; l <= c->L; ++l) {
+    const Lay& y = c->lay[l];
+    Segment w{};
+    w.off = y.w_off;
+    w.rows = y.out;
+    w.cols = y.in;
+    w.is_bias = 0;
+    w.part = y.part;
+    w.splits = splits.empty() ? 0 : splits[l];
+    w.ld_part = y.ld_part;
+    w.split_stride = y.part_rows * y.ld_part;
+    w.transposed = (l == c->L);
+    w.w16 = y.w16;
+    w.w16_ld = y.w16_ld;
+    t.s[t.n++] = w;
+    Segment b{};
+    b.off = y.b_off;
+    b.rows = 1;
+    b.cols = y.out;
+    b.is_bias = 1;
+    b.colsum = y.colsum;
+    b.nparts = colsum_parts.empty() ? 0 : colsum_parts[l];
+    b.colsum_ld = y.colsum_ld;
+    t.s[t.n++] = b;
+  }
+  return t;
+}
+
+extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int world,
+                                     const uint8_t* nccl_id, int device, srl_ctx** out) {
+  if (!cfg || !out) FAIL(SRL_EINVAL, "srl_ppo_create: null");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) FAIL(SRL_EINVAL, "srl_ppo_create: bad rank/world");
+  if (world > 1 && !nccl_id) FAIL(SRL_EINVAL, "srl_ppo_create: world > 1 needs nccl_id");
+  if (cfg->obs_dim < 1 || cfg->ld_obs < cfg->obs_dim || cfg->ld_obs % 8)
+    FAIL(SRL_EINVAL, "srl_ppo_create: need 1 <= obs_dim <= ld_obs, ld_obs % 8 == 0");
+  if (cfg->n_hidden < 1 || cfg->n_hidden > 8 || !cfg->hidden)
+    FAIL(SRL_EINVAL, "srl_ppo_create: need 1 <= n_hidden <= 8");
+  for (int l = 0; l < cfg->n_hidden; ++l)
+    if (cfg->hidden[l] < 64 || cfg->hidden[l] % 64 || cfg->hidden[l] > 1024)
+      FAIL(SRL_EINVAL, "srl_ppo_create: hidden widths must be multiples of 64 in [64, 1024]");
+  if (cfg->n_heads < 1 || cfg->n_heads > kMaxHeads || !cfg->head_sizes)
+    FAIL(SRL_EINVAL, "srl_ppo_create: need 1 <= n_heads <= 8");
+  int A = 0;
+  for (int h = 0; h < cfg->n_heads; ++h) {
+    if (cfg->head_sizes[h] < 1) FAIL(SRL_EINVAL, "srl_ppo_create: head size < 1");
+    A += cfg->head_sizes[h];
+  }
+  if (A + 1 > kHeadCols) FAIL(SRL_EINVAL, "srl_ppo_create: sum(head_sizes) + 1 must be <= 64");
+  if (cfg->max_local_n < 1 || cfg->max_local_n > (int64_t)1 << 31)
+    FAIL(SRL_EINVAL, "srl_ppo_create: need 1 <= max_local_n <= 2^31");
+  if (cfg->precision != SRL_PREC_F16_SCALED) FAIL(SRL_EUNSUPPORTED, "srl_ppo_create: precision");
+  if (srl_status st = require_device()) return st;
+  CK(cudaSetDevice(device));
+  if (!tmap_init()) FAIL(SRL_ECUDA, "cuTensorMapEncodeTiled unavailable");
+
+  srl_ctx* c = new srl_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  c->cfg = *cfg;
+  c->hidden.assign(cfg->hidden, cfg->hidden + cfg->n_hidden);
+  c->heads.assign(cfg->head_sizes, cfg->head_sizes + cfg->n_heads);
+  c->cfg.hidden = c->hidden.data();
+  c->cfg.head_sizes = c->heads.data();
+  c->L = cfg->n_hidden;
+  c->A = A;
+  c->max_n = cfg->max_local_n;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  c->dims.push_back(cfg->obs_dim);
+  for (int h : c->hidden) c->dims.push_back(h);
+  c->dims.push_back(A + 1);
+  std::vector<int> dig(c->dims);
+  dig.insert(dig.end(), c->heads.begin(), c->heads.end());
+  c->digest = fnv1a(dig);
+
+  auto bail = [&](srl_status st) { free_ctx(c); return st; };
+  int64_t off = 0;
+  int max_h = 0;
+  c->lay.resize(c->L + 1);
+  for (int l = 0; l <= c->L; ++l) {
+    Lay& y = c->lay[l];
+    y.in = c->dims[l];
+    y.out = c->dims[l + 1];
+    y.w_off = off;
+    y.b_off = off + (int64_t)y.out * y.in;
+    off = y.b_off + y.out;
+    y.w16_ld = (l == 0) ? (y.in + 7) / 8 * 8 : y.in;
+    y.w16_rows = (l == c->L) ? kHeadCols : y.out;
+    if (l < c->L) max_h = std::max(max_h, y.out);
+  }
+  c->P = off;
+  srl_status st;
+  if ((st = dalloc(c, &c->params, sizeof(float) * c->P))) return bail(st);
+  if ((st = dalloc(c, &c->grads, sizeof(float) * (c->P + 8)))) return bail(st);
+  if ((st = dalloc(c, &c->m, sizeof(float) * c->P))) return bail(st);
+  if ((st = dalloc(c, &c->v, sizeof(float) * c->P))) return bail(st);
+  if ((st = dalloc(c, &c->t_dev, sizeof(int64_t)))) return bail(st);
+  if ((st = dalloc(c, &c->counters, sizeof(unsigned long long) * 4))) return bail(st);
+  if ((st = dalloc(c, &c->stats_part, sizeof(double) * 8 * c->sms))) return bail(st);
+  if ((st = dalloc(c, &c->norm_scratch, sizeof(double) * (3 * kMomentBlocks + 3 * world + 8)))) return bail(st);
+  const int64_t n = c->max_n;
+  for (int l = 0; l <= c->L; ++l) {
+    Lay& y = c->lay[l];
+    if ((st = dalloc(c, &y.w16, sizeof(__half) * (size_t)y.w16_rows * y.w16_ld))) return bail(st);
+    y.bn_fwd = (l == c->L) ? kHeadCols : pick_bn(y.out);
+    y.bn_dx = pick_bn(y.in);
+    // dW: hidden layer: D[out][in] = dZ^T X; head: D^T[in][64] = Y^T g
+    const int dM = (l == c->L) ? y.in : y.out;
+    const int dN = (l == c->L) ? kHeadCols : y.in;
+    y.bn_dw = (l == c->L) ? kHeadCols : pick_bn(dN);
+    y.dw_m_tiles = (dM + 127) / 128;
+    y.dw_n_tiles = (dN + y.bn_dw - 1) / y.bn_dw;
+    y.splits_max = std::max(1, c->sms / (y.dw_m_tiles * y.dw_n_tiles));
+    y.part_rows = dM;
+    y.ld_part = (int64_t)y.dw_n_tiles * y.bn_dw;
+    if ((st = dalloc(c, &y.part, sizeof(float) * y.splits_max * y.part_rows * y.ld_part))) return bail(st);
+    y.colsum_ld = (l == c->L) ? kHeadCols : y.out;
+    if ((st = dalloc(c, &y.colsum, sizeof(float) * c->sms * y.colsum_ld))) return bail(st);
+  }
+  c->Y.resize(c->L);
+  for (int l = 0; l < c->L; ++l)
+    if ((st = dalloc(c, &c->Y[l], sizeof(__half) * (size_t)n * c->dims[l + 1]))) return bail(st);
+  if ((st = dalloc(c, &c->G16, sizeof(__half) * (size_t)n * kHeadCols))) return bail(st);
+  for (int k = 0; k < 2; ++k)
+    if ((st = dalloc(c, &c->dZ[k], sizeof(__half) * (size_t)n * max_h))) return bail(st);
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(id.internal, nccl_id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      c->comm = nullptr;
+      free_ctx(c);
+      return SRL_ENCCL;
+    }
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    set_error(std::string("srl_ppo_create: ") + cudaGetErrorString(e));
+    free_ctx(c);
+    return SRL_ECUDA;
+  }
+  *out = c;
+  return SRL_OK;
+}
+
+extern "C" srl_status srl_ppo_destroy(srl_ctx* ctx) {
+  free_ctx(ctx);
+  return SRL_OK;
+}
+
+extern "C" srl_status srl_ppo_params(srl_ctx* c, float** params_dev, float** grads_dev,
+                                     int64_t* P, uint64_t* digest) {
+  if (!c) FAIL(SRL_EINVAL, "srl_ppo_params: null ctx");
+  if (params_dev) *params_dev = c->params;
+  if (grads_dev) *grads_dev = c->grads;
+  if (P) *P = c->P;
+  if (digest) *digest = c->digest;
+  return SRL_OK;
+}
+
+extern "C" srl_status srl_ppo_adam_state(srl_ctx* c, float** m_dev, float** v_dev,
+                                         int64_t* step) {
+  if (!c) FAIL(SRL_EINVAL, "srl_ppo_adam_state: null ctx");
+  CK(cudaSetDevice(c->device));
+  if (m_dev) *m_dev = c->m;
+  if (v_dev) *v_dev = c->v;
+  if (step) CK(cudaMemcpy(step, c->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return SRL_OK;
+}
+
+extern "C" srl_status srl_ppo_load_params(srl_ctx* c, const float* params_dev,
+                                          srl_stream_t stream) {
+  if (!c || !params_dev) FAIL(SRL_EINVAL, "srl_ppo_load_params: null");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaMemcpyAsync(c->params, params_dev, sizeof(float) * c->P, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemsetAsync(c->m, 0, sizeof(float) * c->P, s));
+  CK(cudaMemsetAsync(c->v, 0, sizeof(float) * c->P, s));
+  CK(cudaMemsetAsync(c->t_dev, 0, sizeof(int64_t), s));
+  SegTable t = make_segs(c, {}, {});
+  CK(launch_shadow(t, c->params, s));
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ a2
+extern "C" srl_status srl_adv_norm(srl_ctx* ctx, float* adv, int64_t n, const double* local_stats,
+                                   float eps, int unbiased, int apply, double* mean_std_out,
+                                   srl_stream_t stream) {
+  if (n < 1) FAIL(SRL_EINVAL, "srl_adv_norm: n < 1");
+  if (!adv && (!local_stats || apply)) FAIL(SRL_EINVAL, "srl_adv_norm: null adv");
+  if (srl_status st = require_device()) return st;
+  if (ctx) CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  double* scratch = nullptr;   // [kMomentBlocks*3] partials, [3] local, [world*3] gathered, [2] ms
+  const int world = ctx ? ctx->world : 1;
+  const size_t cnt = 3 * kMomentBlocks + 3 + 3 * world + 2;
+  if (ctx) scratch = ctx->norm_scratch;   // context-owned: no allocation on the hot path
+  else CK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * cnt, s));
+  double* local = scratch + 3 * kMomentBlocks;
+  double* gathered = local + 3;
+  double* ms = gathered + 3 * world;
+  if (!local_stats) {
+    CK(launch_moments(adv, n, scratch, s));
+    CK(launch_merge_moments(scratch, kMomentBlocks, local, nullptr, 0, s));
+    local_stats = local;
+  }
+  if (world > 1) {
+    CKN(ncclAllGather(local_stats, gathered, 3, ncclDouble, ctx->comm, s));
+    CK(launch_merge_moments(gathered, world, nullptr, ms, unbiased, s));
+  } else {
+    CK(launch_merge_moments(local_stats, 1, nullptr, ms, unbiased, s));
+  }
+  if (apply) CK(launch_normalize(adv, n, ms, eps, s));
+  if (mean_std_out)
+    CK(cudaMemcpyAsync(mean_std_out, ms, sizeof(double) * 2, cudaMemcpyDeviceToDevice, s));
+  if (!ctx) CK(cudaFreeAsync(scratch, s));
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ a6
+extern "C" srl_status srl_allreduce_grads(srl_ctx* c, float* buf, int64_t count, int op,
+                                          srl_stream_t stream) {
+  if (!c || !buf || count < 0 || (op != 0 && op != 1)) FAIL(SRL_EINVAL, "srl_allreduce_grads: bad args");
+  if (c->world == 1 || count == 0) return SRL_OK;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CKN(ncclAllReduce(buf, buf, (size_t)count, ncclFloat, op == 1 ? ncclAvg : ncclSum, c->comm, s));
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ a3..a7
+static srl_status gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
+                       const CUtensorMap& tb, GemmArgs& g, int sms, cudaStream_t s,
+                       int* grid_out = nullptr) {
+  const int units = g.m_tiles * g.n_tiles * g.k_splits;
+  const int grid = std::min(units, sms);
+  if (grid_out) *grid_out = grid;
+  cudaError_t e = launch_gemm(bn, a_mn, b_mn, epi, ta, tb, g, grid, s);
+  if (e != cudaSuccess) FAIL(SRL_ECUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
+  return SRL_OK;
+}
+
+#define TM(map, ...)                                                             \
+  do {                                                                           \
+    if (!make_tmap_2d(&(map), __VA_ARGS__)) FAIL(SRL_ECUDA, "tensor map encode failed"); \
+  } while (0)
+
+extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global,
+                                   const uint16_t* obs, const int32_t* actions,
+                                   const float* logp_old, const float* adv, const float* ret,
+                                   const double* adv_mean_std, int apply,
+                                   srl_ppo_stats* stats_out, srl_stream_t stream) {
+  if (!c) FAIL(SRL_EINVAL, "srl_ppo_step: null ctx");
+  if (n_local < 1 || n_local > c->max_n || n_global < n_local)
+    FAIL(SRL_EINVAL, "srl_ppo_step: need 1 <= n_local <= max_local_n, n_global >= n_local");
+  if (!obs || !actions || !logp_old || !adv || !ret) FAIL(SRL_EINVAL, "srl_ppo_step: null input");
+  if ((reinterpret_cast<uintptr_t>(obs) & 15) != 0) FAIL(SRL_EINVAL, "srl_ppo_step: obs must be 16-byte aligned");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int n = (int)n_local;
+  const int L = c->L;
+  const int sms = c->sms;
+  const float inv_n = (float)(1.0 / (double)n_global);
+  const __half* X0 = reinterpret_cast<const __half*>(obs);
+  const int ld_obs = c->cfg.ld_obs;
+  CK(cudaMemsetAsync(c->counters, 0, sizeof(unsigned long long) * 4, s));
+
+  // ---------------- a3: forward hidden layers Y_l = tanh(Y_{l-1} W_l^T + b_l)
+  for (int l = 0; l < L; ++l) {
+    const Lay& y = c->lay[l];
+    CUtensorMap ta, tb;
+    const __half* X = l == 0 ? X0 : c->Y[l - 1];
+    const int ldx = l == 0 ? ld_obs : y.in;
+    TM(ta, X, y.in, n, (uint64_t)ldx * 2, 64, 128);
+    TM(tb, y.w16, y.in, y.out, (uint64_t)y.w16_ld * 2, 64, y.bn_fwd);
+    GemmArgs g{};
+    g.M = n; g.N = y.out;
+    g.m_tiles = (n + 127) / 128; g.n_tiles = y.out / y.bn_fwd; g.k_splits = 1;
+    g.kb_total = (y.in + 63) / 64; g.kb_per_split = g.kb_total;
+    g.out = c->Y[l]; g.ld_out = y.out;
+    g.bias = c->params + y.b_off;
+    ProfScope ps(c, s, l == 0 ? "fwd_l1" : "fwd_hidden", 2.0 * n * y.in * y.out,
+                 2.0 * n * (y.in + y.out) + 2.0 * y.in * y.out + 4.0 * y.out);
+    if (srl_status st = gemm(y.bn_fwd, false, false, EPI_TANH, ta, tb, g, sms, s)) return st;
+  }
+  // ---------------- a4: head GEMM + fused PPO loss -> per-sample dlogits G16
+  const Lay& hd = c->lay[L];
+  int grid_loss = 0;
+  {
+    CUtensorMap ta, tb;
+    TM(ta, c->Y[L - 1], hd.in, n, (uint64_t)hd.in * 2, 64, 128);
+    TM(tb, hd.w16, hd.in, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
+    GemmArgs g{};
+    g.M = n; g.N = kHeadCols;
+    g.m_tiles = (n + 127) / 128; g.n_tiles = 1; g.k_splits = 1;
+    g.kb_total = (hd.in + 63) / 64; g.kb_per_split = g.kb_total;
+    g.out = c->G16; g.ld_out = kHeadCols;
+    g.bias = c->params + hd.b_off;
+    g.colsum = hd.colsum; g.colsum_ld = kHeadCols;
+    g.counters = c->counters;
+    g.actions = actions; g.logp_old = logp_old; g.adv = adv; g.ret = ret;
+    g.mean_std = adv_mean_std; g.stats = c->stats_part;
+    g.n_heads = (int)c->heads.size(); g.A = c->A;
+    for (int h = 0; h < g.n_heads; ++h) g.head_size[h] = c->heads[h];
+    g.clip_eps = c->cfg.clip_eps; g.value_coef = c->cfg.value_coef;
+    g.entropy_coef = c->cfg.entropy_coef; g.adv_eps = c->cfg.adv_eps;
+    ProfScope ps(c, s, "head_loss", 2.0 * n * hd.in * hd.out,
+                 2.0 * n * hd.in + 2.0 * n * kHeadCols + (16.0 + 4.0 * g.n_heads) * n);
+    if (srl_status st = gemm(64, false, false, EPI_LOSS, ta, tb, g, sms, s, &grid_loss)) return st;
+  }
+  // ---------------- a5: backward.  dW via split-K partials, dX with fused dtanh + db sums
+  std::vector<int> splits(L + 1, 1), colsum_parts(L + 1, 0);
+  colsum_parts[L] = grid_loss;
+  auto dW = [&](int l, const __half* Amat, int lda, const __half* Bmat, int ldb) -> srl_status {
+    const Lay& y = c->lay[l];
+    const int dM = (l == L) ? y.in : y.out;
+    const int dN = (l == L) ? kHeadCols : y.in;
+    CUtensorMap ta, tb;
+    TM(ta, Amat, dM, n, (uint64_t)lda * 2, 64, 64);
+    TM(tb, Bmat, dN, n, (uint64_t)ldb * 2, 64, 64);
+    GemmArgs g{};
+    g.M = dM; g.N = dN;
+    g.m_tiles = y.dw_m_tiles; g.n_tiles = y.dw_n_tiles;
+    g.kb_total = (n + 63) / 64;
+    int S = std::min(y.splits_max, g.kb_total);
+    g.kb_per_split = (g.kb_total + S - 1) / S;
+    S = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+    g.k_splits = S;
+    g.part = y.part; g.ld_part = y.ld_part; g.part_split_stride = y.part_rows * y.ld_part;
+    splits[l] = S;
+    const int realN = (l == L) ? y.out : dN;
+    ProfScope ps(c, s, l == L ? "dW_head" : (l == 0 ? "dW_l1" : "dW_hidden"),
+                 2.0 * n * dM * realN, 2.0 * n * (dM + dN) + 4.0 * S * dM * y.ld_part);
+    return gemm(y.bn_dw, true, true, EPI_PART, ta, tb, g, sms, s);
+  };
+  auto dX = [&](int l, const __half* dz_in, int k_width, __half* dz_out) -> srl_status {
+    // dZ_{in of layer l} = (dZ_out_l W_l) * (1 - Y_{l-1}^2), colsum -> db of layer l-1
+    const Lay& y = c->lay[l];
+    const Lay& yp = c->lay[l - 1];
+    CUtensorMap ta, tb;
+    TM(ta, dz_in, k_width, n, (uint64_t)k_width * 2, 64, 128);
+    TM(tb, y.w16, y.in, y.w16_rows, (uint64_t)y.w16_ld * 2, 64, 64);
+    GemmArgs g{};
+    g.M = n; g.N = y.in;
+    g.m_tiles = (n + 127) / 128; g.n_tiles = y.in / y.bn_dx; g.k_splits = 1;
+    g.kb_total = (k_width + 63) / 64; g.kb_per_split = g.kb_total;
+    g.out = dz_out; g.ld_out = y.in;
+    g.y_prev = c->Y[l - 1]; g.ld_y = y.in;
+    g.colsum = yp.colsum; g.colsum_ld = yp.colsum_ld;
+    g.counters = c->counters;
+    int grid = 0;
+    const int realK = (l == L) ? y.out : k_width;
+    ProfScope ps(c, s, l == L ? "dX_head" : "dX_hidden", 2.0 * n * realK * y.in,
+                 2.0 * n * (k_width + 2.0 * y.in) + 2.0 * y.in * k_width);
+    srl_status st = gemm(y.bn_dx, false, true, EPI_DTANH, ta, tb, g, sms, s, &grid);
+    colsum_parts[l - 1] = grid;
+    return st;
+  };
+  if (srl_status st = dW(L, c->Y[L - 1], hd.in, c->G16, kHeadCols)) return st;
+  int cur = 0;
+  if (srl_status st = dX(L, c->G16, kHeadCols, c->dZ[cur])) return st;
+  for (int l = L - 1; l >= 0; --l) {
+    const Lay& y = c->lay[l];
+    const __half* Xl = l == 0 ? X0 : c->Y[l - 1];
+    const int ldx = l == 0 ? ld_obs : y.in;
+    if (srl_status st = dW(l, c->dZ[cur], y.out, Xl, ldx)) return st;
+    if (l > 0) {
+      if (srl_status st = dX(l, c->dZ[cur], y.out, c->dZ[cur ^ 1])) return st;
+      cur ^= 1;
+    }
+  }
+  SegTable segs = make_segs(c, splits, colsum_parts);
+  {
+    double rd = 0;
+    for (int l = 0; l <= L; ++l) rd += 4.0 * splits[l] * c->lay[l].out * c->lay[l].in +
+                                       4.0 * colsum_parts[l] * c->lay[l].colsum_ld;
+    ProfScope ps(c, s, "grad_finalize", 0.0, rd + 4.0 * c->P);
+    CK(launch_finalize_grads(segs, c->P, inv_n, c->grads, c->counters, s));
+    CK(launch_extras(c->P, inv_n, c->stats_part, grid_loss, c->counters, c->grads, s));
+  }
+  if (apply) {
+    // ---------------- a6: gradient allreduce (bucket already scaled by 1/N_global)
+    if (c->world > 1) {
+      ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8));
+      CKN(ncclAllReduce(c->grads, c->grads, (size_t)(c->P + 8), ncclFloat, ncclSum, c->comm, s));
+    }
+    // ---------------- a7: Adam + fp16 shadow refresh
+    ProfScope ps(c, s, "adam", 0.0, 30.0 * c->P);
+    CK(launch_adam(segs, c->P, c->params, c->m, c->v, c->grads, c->t_dev, c->cfg.lr,
+                   c->cfg.beta1, c->cfg.beta2, c->cfg.adam_eps, s));
+  }
+  CK(launch_stats(c->grads, c->P, adv_mean_std, n_global, c->cfg.value_coef, c->cfg.entropy_coef,
+                  c->t_dev, apply, stats_out, s));
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ profiling
+extern "C" srl_status srl_prof_enable(srl_ctx* c, int on) {
+  if (!c) FAIL(SRL_EINVAL, "srl_prof_enable: null ctx");
+  c->prof = on != 0;
+  return SRL_OK;
+}
+
+extern "C" srl_status srl_prof_reset(srl_ctx* c) {
+  if (!c) FAIL(SRL_EINVAL, "srl_prof_reset: null ctx");
+  c->recs.clear();
+  c->pool_used = 0;
+  return SRL_OK;
+}
+
+extern "C" int srl_prof_count(srl_ctx* c) { return c ? (int)c->recs.size() : 0; }
+
+extern "C" srl_status srl_prof_read(srl_ctx* c, int i, const char** name, float* ms,
+                                    double* flops, double* bytes) {
+  if (!c || i < 0 || i >= (int)c->recs.size()) FAIL(SRL_EINVAL, "srl_prof_read: index");
+  const auto& r = c->recs[i];
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventSynchronize(r.b));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, r.a, r.b));
+  if (name) *name = r.name;
+  if (ms) *ms = t;
+  if (flops) *flops = r.flops;
+  if (bytes) *bytes = r.bytes;
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ test hook
+__global__ void sum_parts_kernel(const float* part, int S, int64_t split_stride, int M, int N,
+                                 int64_t ld_part, float* D) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)M * N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / N), cc = (int)(i % N);
+    float acc = 0.f;
+    for (int k = 0; k < S; ++k) acc += part[k * split_stride + r * ld_part + cc];
+    D[i] = acc;
+  }
+}
+
+extern "C" srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int a_mn, int lda,
+                                     const uint16_t* B, int b_mn, int ldb, int bn, int splits,
+                                     float* D, srl_stream_t stream) {
+  if (M < 1 || N < 1 || K < 1 || !A || !B || !D || lda % 8 || ldb % 8 || splits < 1)
+    FAIL(SRL_EINVAL, "srl_debug_gemm: bad args");
+  if (bn != 64 && bn != 128 && bn != 256) FAIL(SRL_EINVAL, "srl_debug_gemm: bn");
+  if (srl_status st = require_device()) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CUtensorMap ta, tb;
+  if (!a_mn) TM(ta, A, K, M, (uint64_t)lda * 2, 64, 128);
+  else TM(ta, A, M, K, (uint64_t)lda * 2, 64, 64);
+  if (!b_mn) TM(tb, B, K, N, (uint64_t)ldb * 2, 64, bn);
+  else TM(tb, B, N, K, (uint64_t)ldb * 2, 64, 64);
+  GemmArgs g{};
+  g.M = M; g.N = N;
+  g.m_tiles = (M + 127) / 128; g.n_tiles = (N + bn - 1) / bn;
+  g.kb_total = (K + 63) / 64;
+  int S = std::min(splits, g.kb_total);
+  g.kb_per_split = (g.kb_total + S - 1) / S;
+  S = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  g.k_splits = S;
+  g.ld_part = (int64_t)g.n_tiles * bn;
+  g.part_split_stride = (int64_t)M * g.ld_part;
+  float* part = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * S * g.part_split_stride, s));
+  g.part = part;
+  if (srl_status st = gemm(bn, a_mn != 0, b_mn != 0, EPI_PART, ta, tb, g, num_sms(), s)) return st;
+  sum_parts_kernel<<<256, 256, 0, s>>>(part, S, g.part_split_stride, M, N, g.ld_part, D);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(part, s));
+  return SRL_OK;
+}

@@ -1,0 +1,246 @@
+// gae.cu -- a1 (GAE reverse scan) and a2 (batch moments, merge, normalisation) kernels.
+//
+// GAE (BASELINE.json north_star):
+//   m_t = 1 - d_t;  delta_t = r_t + gamma v_{t+1} m_t - v_t;  A_t = delta_t + gamma lambda m_t A_{t+1}
+// is an affine recurrence A_t = delta_t + c_t A_{t+1}.  One thread per env column (coalesced
+// time-major rows) is too little parallelism for B ~ 1k columns, so each block owns 32
+// columns and splits T into W chunks of TC rows, one warp per chunk:
+//   pass 1: every warp scans its chunk from A_end = 0 and publishes (a_first, prod c);
+//   combine: A entering chunk w = fold of the later chunks' (a, P) summaries;
+//   pass 2: every warp re-runs the exact recurrence from the true A_end (values are
+//   register-resident), writes adv/ret and accumulates moments.
+// Integer inputs with gamma = lambda = 1 stay exact, so the result is bit-identical to the
+// sequential recursion (C-B1).  Moments per block are {n, mean, M2} in double, merged in a
+// fixed order (deterministic), shifted sums inside a thread.
+#include <math.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace srl {
+
+__device__ __forceinline__ void chan_merge(double& n, double& mean, double& m2, double nb,
+                                           double mb, double m2b) {
+  if (nb == 0.0) return;
+  if (n == 0.0) { n = nb; mean = mb; m2 = m2b; return; }
+  const double tot = n + nb;
+  const double delta = mb - mean;
+  mean = mean + delta * (nb / tot);
+  m2 = m2 + m2b + delta * delta * (n * nb / tot);
+  n = tot;
+}
+
+// warp merge (fixed butterfly order), result valid in every lane
+__device__ __forceinline__ void warp_merge(double& n, double& mean, double& m2) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double nb = __shfl_xor_sync(0xffffffffu, n, o);
+    double mb = __shfl_xor_sync(0xffffffffu, mean, o);
+    double qb = __shfl_xor_sync(0xffffffffu, m2, o);
+    // lower lane index first so both partners compute the same combination
+    if (threadIdx.x & o) {
+      double n0 = nb, m0 = mb, q0 = qb;
+      chan_merge(n0, m0, q0, n, mean, m2);
+      n = n0; mean = m0; m2 = q0;
+    } else {
+      chan_merge(n, mean, m2, nb, mb, qb);
+    }
+  }
+}
+
+template <int TC>
+__global__ void __launch_bounds__(TC <= 8 ? 1024 : 512)
+gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __restrict__ v,
+           const uint8_t* __restrict__ d, float gamma, float gl, float* __restrict__ adv,
+           float* __restrict__ ret, double* __restrict__ part) {
+  __shared__ float s_a[32][33];
+  __shared__ float s_p[32][33];
+  __shared__ float s_carry[32];
+  __shared__ double s_mom[32][3];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int b = blockIdx.x * 32 + lane;
+  const bool col_ok = b < B;
+  const int SC = W * TC;
+  const int nsc = (T + SC - 1) / SC;
+  float carry = 0.f;                       // A at the first row after this super-chunk
+  double sh = 0.0, s1 = 0.0, s2 = 0.0;     // shifted sums of my adv values
+  int cnt_all = 0;
+  bool have_shift = false;
+
+  for (int sc = nsc - 1; sc >= 0; --sc) {
+    const int t0 = sc * SC + w * TC;
+    float delta[TC], c[TC], vt[TC];
+#pragma unroll
+    for (int i = 0; i < TC; ++i) {
+      const int t = t0 + i;
+      if (col_ok && t < T) {
+        const float rr = __ldg(r + (int64_t)t * ld + b);
+        const float v0 = __ldg(v + (int64_t)t * ld + b);
+        const float v1 = __ldg(v + (int64_t)(t + 1) * ld + b);
+        const float m = __ldg(d + (int64_t)t * ld + b) ? 0.f : 1.f;
+        delta[i] = rr + gamma * v1 * m - v0;
+        c[i] = gl * m;
+        vt[i] = v0;
+      } else {
+        delta[i] = 0.f;   // rows past T: identity step
+        c[i] = 1.f;
+        vt[i] = 0.f;
+      }
+    }
+    // pass 1: chunk summary with A_end = 0
+    float a = 0.f, P = 1.f;
+#pragma unroll
+    for (int i = TC - 1; i >= 0; --i) {
+      a = delta[i] + c[i] * a;
+      P *= c[i];
+    }
+    s_a[w][lane] = a;
+    s_p[w][lane] = P;
+    __syncthreads();
+    float Ain = carry;
+    for (int w2 = W - 1; w2 > w; --w2) Ain = s_a[w2][lane] + s_p[w2][lane] * Ain;
+    // pass 2: exact recurrence from the true A_end
+    a = Ain;
+#pragma unroll
+    for (int i = TC - 1; i >= 0; --i) {
+      a = delta[i] + c[i] * a;
+      const int t = t0 + i;
+      if (col_ok && t < T) {
+        adv[(int64_t)t * ld + b] = a;
+        if (ret) ret[(int64_t)t * ld + b] = a + vt[i];
+        if (!have_shift) { sh = a; have_shift = true; }
+        const double e = (double)a - sh;
+        s1 += e;
+        s2 += e * e;
+        ++cnt_all;
+      }
+    }
+    if (w == 0) s_carry[lane] = a;         // A at row sc*SC
+    __syncthreads();
+    carry = s_carry[lane];
+  }
+  if (!part) return;
+  // thread moments -> warp -> block (fixed order)
+  double n = (double)cnt_all;
+  double mean = n > 0 ? sh + s1 / n : 0.0;
+  double m2 = n > 0 ? fmax(s2 - s1 * s1 / n, 0.0) : 0.0;
+  warp_merge(n, mean, m2);
+  if (lane == 0) { s_mom[w][0] = n; s_mom[w][1] = mean; s_mom[w][2] = m2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double N = 0, M = 0, Q = 0;
+    for (int k = 0; k < W; ++k) chan_merge(N, M, Q, s_mom[k][0], s_mom[k][1], s_mom[k][2]);
+    part[blockIdx.x * 3 + 0] = N;
+    part[blockIdx.x * 3 + 1] = M;
+    part[blockIdx.x * 3 + 2] = Q;
+  }
+}
+
+int gae_num_blocks(int B) { return (B + 31) / 32; }
+
+cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
+                       float gamma, float lambda, float* adv, float* ret, double* part,
+                       cudaStream_t s) {
+  const int blocks = gae_num_blocks(B);
+  const float gl = gamma * lambda;
+  if (T <= 32 * 8) {            // <= 32 warps of 8 rows, one pass
+    const int W = (T + 7) / 8;
+    gae_kernel<8><<<blocks, 32 * W, 0, s>>>(T, B, ld, r, v, d, gamma, gl, adv, ret, part);
+  } else {                       // <= 16 warps of 16 rows per super-chunk of 256 rows
+    const int W = std::min(16, (T + 15) / 16);
+    gae_kernel<16><<<blocks, 32 * W, 0, s>>>(T, B, ld, r, v, d, gamma, gl, adv, ret, part);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- a2: moments of a vector
+__global__ void __launch_bounds__(256) moments_kernel(const float* __restrict__ x, int64_t n,
+                                                      double* __restrict__ part) {
+  __shared__ double s_mom[8][3];
+  // block k owns the contiguous range [k*n/G, (k+1)*n/G); threads stride inside it
+  const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+  double sh = 0.0, s1 = 0.0, s2 = 0.0;
+  int64_t cnt = 0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double a = (double)__ldg(x + i);
+    if (cnt == 0) sh = a;
+    const double e = a - sh;
+    s1 += e;
+    s2 += e * e;
+    ++cnt;
+  }
+  double N = (double)cnt;
+  double mean = cnt ? sh + s1 / N : 0.0;
+  double m2 = cnt ? fmax(s2 - s1 * s1 / N, 0.0) : 0.0;
+  warp_merge(N, mean, m2);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { s_mom[w][0] = N; s_mom[w][1] = mean; s_mom[w][2] = m2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0, c = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) chan_merge(a, b, c, s_mom[k][0], s_mom[k][1], s_mom[k][2]);
+    part[blockIdx.x * 3 + 0] = a;
+    part[blockIdx.x * 3 + 1] = b;
+    part[blockIdx.x * 3 + 2] = c;
+  }
+}
+
+cudaError_t launch_moments(const float* x, int64_t n, double* part, cudaStream_t s) {
+  moments_kernel<<<kMomentBlocks, 256, 0, s>>>(x, n, part);
+  return cudaGetLastError();
+}
+
+// merge partial triples in index order (contiguous ranges per thread, then a fixed tree)
+__global__ void __launch_bounds__(256) merge_moments_kernel(const double* __restrict__ part,
+                                                            int count, double* out,
+                                                            double* mean_std, int unbiased) {
+  __shared__ double sn[256], sm[256], sq[256];
+  const int t = threadIdx.x;
+  const int lo = (int)((int64_t)count * t / 256), hi = (int)((int64_t)count * (t + 1) / 256);
+  double n = 0, mean = 0, m2 = 0;
+  for (int k = lo; k < hi; ++k) chan_merge(n, mean, m2, part[3 * k], part[3 * k + 1], part[3 * k + 2]);
+  sn[t] = n; sm[t] = mean; sq[t] = m2;
+  __syncthreads();
+  for (int o = 128; o >= 1; o >>= 1) {
+    if (t < o) {
+      double a = sn[t], b = sm[t], c = sq[t];
+      chan_merge(a, b, c, sn[t + o], sm[t + o], sq[t + o]);
+      sn[t] = a; sm[t] = b; sq[t] = c;
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    if (out) { out[0] = sn[0]; out[1] = sm[0]; out[2] = sq[0]; }
+    if (mean_std) {
+      const double denom = unbiased ? sn[0] - 1.0 : sn[0];
+      mean_std[0] = sm[0];
+      mean_std[1] = denom > 0 ? sqrt(sq[0] / denom) : 0.0;
+    }
+  }
+}
+
+cudaError_t launch_merge_moments(const double* part, int count, double* out, double* mean_std,
+                                 int unbiased, cudaStream_t s) {
+  merge_moments_kernel<<<1, 256, 0, s>>>(part, count, out, mean_std, unbiased);
+  return cudaGetLastError();
+}
+
+__global__ void normalize_kernel(float* __restrict__ x, int64_t n, const double* __restrict__ ms,
+                                 float eps) {
+  const double mu = ms[0], sd = ms[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = (float)(((double)x[i] - mu) / (sd + (double)eps));
+}
+
+cudaError_t launch_normalize(float* x, int64_t n, const double* mean_std, float eps,
+                             cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 4 * 148) blocks = 4 * 148;
+  if (blocks < 1) blocks = 1;
+  normalize_kernel<<<(int)blocks, 256, 0, s>>>(x, n, mean_std, eps);
+  return cudaGetLastError();
+}
+
+}  // namespace srl

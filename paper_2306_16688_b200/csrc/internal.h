@@ -1,0 +1,78 @@
+// internal.h -- declarations shared by the libsrl translation units (not part of the ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "gemm_tc.cuh"
+
+namespace srl {
+
+// ---- error plumbing (thread-local message behind srl_last_error)
+void set_error(const std::string& msg);
+
+// ---- device info
+int num_sms();
+
+// ---- a1 / a2 kernels (gae.cu)
+// Moments triple {n, mean, M2} as 3 doubles.
+cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
+                       float gamma, float lambda, float* adv, float* ret,
+                       double* part /* [gae_num_blocks(B)][3] or null */, cudaStream_t s);
+int gae_num_blocks(int B);
+constexpr int kMomentBlocks = 256;
+cudaError_t launch_moments(const float* x, int64_t n, double* part /*[kMomentBlocks][3]*/,
+                           cudaStream_t s);
+// merge `count` partial triples in index order -> out[3]; if mean_std != null also writes
+// {mean, sigma} with sigma = sqrt(M2 / (unbiased ? n-1 : n)).
+cudaError_t launch_merge_moments(const double* part, int count, double* out, double* mean_std,
+                                 int unbiased, cudaStream_t s);
+cudaError_t launch_normalize(float* x, int64_t n, const double* mean_std, float eps,
+                             cudaStream_t s);
+
+// ---- GEMM (mlp.cu)
+bool tmap_init();
+bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                  uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+// D = A * B^T over the given shape; picks the instantiation (bn, a_mn, b_mn, epi).
+cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
+                        const CUtensorMap& tb, const GemmArgs& args, int grid, cudaStream_t s);
+size_t gemm_smem_bytes(int bn, int colsum_ld);
+
+// ---- parameter segments (misc.cu): one weight matrix or bias vector of the flat layout
+struct Segment {
+  int64_t off;          // offset in the flat parameter / gradient vector
+  int rows, cols;       // weight: [rows=out][cols=in]; bias: rows = 1, cols = out
+  int is_bias;
+  // gradient source
+  const float* part;    // weight: dW partials [splits][part_rows][ld_part] (transposed if head)
+  int splits;
+  int64_t ld_part, split_stride;
+  int transposed;       // head: partial holds dW^T ([in][G])
+  const float* colsum;  // bias: [nparts][colsum_ld]
+  int nparts, colsum_ld;
+  // fp16 shadow (weights only)
+  __half* w16;
+  int w16_ld;
+};
+constexpr int kMaxSegs = 20;
+struct SegTable {
+  int n;
+  Segment s[kMaxSegs];
+};
+cudaError_t launch_finalize_grads(const SegTable& t, int64_t P, float inv_n, float* bucket,
+                                  unsigned long long* counters, cudaStream_t s);
+cudaError_t launch_extras(int64_t P, float inv_n, const double* stats_part, int nstats,
+                          const unsigned long long* counters, float* bucket, cudaStream_t s);
+cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float* v,
+                        const float* bucket, const int64_t* t_dev, float lr, float b1,
+                        float b2, float eps, cudaStream_t s);
+cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s);
+cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,
+                         int64_t n_global, float value_coef, float entropy_coef,
+                         int64_t* t_dev, int apply, void* stats_out, cudaStream_t s);
+
+}  // namespace srl

@@ -1,0 +1,97 @@
+// mlp.cu -- TMA descriptor encoding and the GEMM instantiations used by the trainer step.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "internal.h"
+
+namespace srl {
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool tmap_init() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// fp16 row-major matrix with `outer` rows of `inner` elements, row pitch row_bytes;
+// box {box_inner, box_outer}, 128-byte swizzle, out-of-bounds elements read as zero.
+bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                  uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  if (!tmap_init()) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+size_t gemm_smem_bytes(int bn, int colsum_ld) {
+  switch (bn) {
+    case 64: return GemmCfg<64>::smem_bytes(colsum_ld);
+    case 128: return GemmCfg<128>::smem_bytes(colsum_ld);
+    default: return GemmCfg<256>::smem_bytes(colsum_ld);
+  }
+}
+
+template <int BN, bool AM, bool BM, int EPI>
+static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                              int grid, cudaStream_t s) {
+  auto kern = gemm_tc_kernel<BN, AM, BM, EPI>;
+  const size_t smem = GemmCfg<BN>::smem_bytes(a.colsum_ld);
+  static size_t configured = 0;
+  if (smem > configured) {
+    // attribute is set for the largest size ever requested (epilogue colsum area varies)
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(GemmCfg<BN>::smem_bytes(1024)));
+    if (e != cudaSuccess) return e;
+    configured = GemmCfg<BN>::smem_bytes(1024);
+  }
+  kern<<<grid, GemmCfg<BN>::THREADS, smem, s>>>(ta, tb, a);
+  return cudaGetLastError();
+}
+
+#define SRL_DISPATCH_BN(AM, BM, EPI)                                         \
+  switch (bn) {                                                              \
+    case 64: return launch_one<64, AM, BM, EPI>(ta, tb, args, grid, s);      \
+    case 128: return launch_one<128, AM, BM, EPI>(ta, tb, args, grid, s);    \
+    case 256: return launch_one<256, AM, BM, EPI>(ta, tb, args, grid, s);    \
+    default: return cudaErrorInvalidValue;                                   \
+  }
+
+cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
+                        const CUtensorMap& tb, const GemmArgs& args, int grid, cudaStream_t s) {
+  if (grid < 1) grid = 1;
+  switch (epi) {
+    case EPI_TANH:
+      if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_TANH) }
+      break;
+    case EPI_DTANH:
+      if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_DTANH) }
+      break;
+    case EPI_LOSS:
+      if (!a_mn && !b_mn && bn == 64) return launch_one<64, false, false, EPI_LOSS>(ta, tb, args, grid, s);
+      break;
+    case EPI_PART:
+      if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_PART) }
+      if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_PART) }
+      if (a_mn && !b_mn) { SRL_DISPATCH_BN(true, false, EPI_PART) }
+      if (a_mn && b_mn) { SRL_DISPATCH_BN(true, true, EPI_PART) }
+      break;
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace srl

@@ -1,0 +1,286 @@
+"""Thin ctypes binding of libsrl.so (include/srl.h).  Argument marshalling only: every step
+of the hot path runs in the library's CUDA kernels.  torch supplies device memory, streams
+and process groups.  There is no CPU fallback: a missing or unloadable library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libsrl.so")
+
+SRL_OK, SRL_EINVAL, SRL_ECUDA, SRL_ENCCL, SRL_ENOMEM, SRL_EUNSUPPORTED, SRL_ESTATE = range(7)
+
+# every symbol include/srl.h declares (checked by tests/test_abi.py)
+EXPORTS = ("srl_last_error", "srl_abi_version", "srl_gae", "srl_adv_norm", "srl_nccl_unique_id",
+           "srl_ppo_create", "srl_ppo_destroy", "srl_ppo_params", "srl_ppo_adam_state",
+           "srl_ppo_load_params", "srl_ppo_step", "srl_allreduce_grads", "srl_prof_enable",
+           "srl_prof_reset", "srl_prof_count", "srl_prof_read", "srl_debug_gemm")
+
+
+class SrlError(RuntimeError):
+    pass
+
+
+class PPOConfigC(C.Structure):
+    _fields_ = [("obs_dim", C.c_int), ("ld_obs", C.c_int), ("n_hidden", C.c_int),
+                ("hidden", C.POINTER(C.c_int)), ("n_heads", C.c_int),
+                ("head_sizes", C.POINTER(C.c_int)),
+                ("clip_eps", C.c_float), ("value_coef", C.c_float), ("entropy_coef", C.c_float),
+                ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("adam_eps", C.c_float), ("adv_eps", C.c_float),
+                ("max_local_n", C.c_int64), ("precision", C.c_int)]
+
+
+class PPOStatsC(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("policy_loss", "value_loss", "entropy", "clip_fraction",
+                                          "approx_kl", "loss", "adv_mean", "adv_std")] + \
+               [(k, C.c_int64) for k in ("n_global", "nonfinite", "fp16_saturated", "step")]
+
+
+STATS_BYTES = C.sizeof(PPOStatsC)
+STATS_FIELDS = [f for f, _ in PPOStatsC._fields_]
+
+_lib = None
+
+
+def lib():
+    """Load libsrl.so (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(SO):
+        raise SrlError(f"{SO} is missing: run `python -m paper_2306_16688_b200.build` "
+                       "(there is no CPU fallback)")
+    L = C.CDLL(SO)
+    vp, i64, st = C.c_void_p, C.c_int64, C.c_int
+    L.srl_last_error.restype = C.c_char_p
+    L.srl_abi_version.restype = C.c_int
+    L.srl_gae.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_float, C.c_float, vp, vp, vp, vp]
+    L.srl_adv_norm.argtypes = [vp, vp, i64, vp, C.c_float, C.c_int, C.c_int, vp, vp]
+    L.srl_nccl_unique_id.argtypes = [C.c_char_p]
+    L.srl_ppo_create.argtypes = [C.POINTER(PPOConfigC), C.c_int, C.c_int, C.c_char_p, C.c_int,
+                                 C.POINTER(vp)]
+    L.srl_ppo_destroy.argtypes = [vp]
+    L.srl_ppo_params.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64), C.POINTER(C.c_uint64)]
+    L.srl_ppo_adam_state.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64)]
+    L.srl_ppo_load_params.argtypes = [vp, vp, vp]
+    L.srl_ppo_step.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
+    L.srl_allreduce_grads.argtypes = [vp, vp, i64, C.c_int, vp]
+    L.srl_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
+                                 C.c_int, C.c_int, C.c_int, vp, vp]
+    L.srl_prof_enable.argtypes = [vp, C.c_int]
+    L.srl_prof_reset.argtypes = [vp]
+    L.srl_prof_count.argtypes = [vp]
+    L.srl_prof_read.argtypes = [vp, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_float),
+                                C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    for name in EXPORTS[2:]:
+        getattr(L, name).restype = st
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != SRL_OK:
+        raise SrlError(f"libsrl status {rc}: {lib().srl_last_error().decode()}")
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _cuda(t, dtype, name):
+    if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise SrlError(f"{name}: need a contiguous CUDA {dtype} tensor, got {t.dtype} on {t.device}")
+    return t
+
+
+# ------------------------------------------------------------------ a1
+def gae(rewards, values, dones, gamma, lam, adv=None, ret=None, stats=None, ld=None, stream=None):
+    """srl_gae on [T][ld] tensors; returns (adv, ret, stats{n, mean, M2} f64[3])."""
+    _cuda(rewards, torch.float32, "rewards")
+    _cuda(values, torch.float32, "values")
+    _cuda(dones, torch.uint8, "dones")
+    T, ldr = rewards.shape
+    B = ldr if ld is None else ld
+    if adv is None:
+        adv = torch.empty_like(rewards)
+    if ret is None:
+        ret = torch.empty_like(rewards)
+    if stats is None:
+        stats = torch.empty(3, dtype=torch.float64, device=rewards.device)
+    _check(lib().srl_gae(T, B, ldr, _ptr(rewards), _ptr(values), _ptr(dones), gamma, lam,
+                         _ptr(adv), _ptr(ret), _ptr(stats), _stream(stream)))
+    return adv, ret, stats
+
+
+# ------------------------------------------------------------------ a2
+def adv_norm(adv, local_stats=None, eps=1e-8, unbiased=False, apply=False, ctx=None,
+             mean_std=None, stream=None):
+    _cuda(adv, torch.float32, "adv")
+    if mean_std is None:
+        mean_std = torch.empty(2, dtype=torch.float64, device=adv.device)
+    h = ctx.handle if ctx is not None else None
+    _check(lib().srl_adv_norm(h, _ptr(adv), adv.numel(), _ptr(local_stats), eps, int(unbiased),
+                              int(apply), _ptr(mean_std), _stream(stream)))
+    return mean_std
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().srl_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _cudart():
+    lib()
+    return C.CDLL("libcudart.so.12")
+
+
+def copy_from_device_ptr(dst: torch.Tensor, src_ptr: int, nbytes: int, stream=None):
+    """cudaMemcpyAsync(dst <- raw device pointer), stream-ordered."""
+    rt = _cudart()
+    rt.cudaMemcpyAsync.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]
+    rc = rt.cudaMemcpyAsync(C.c_void_p(dst.data_ptr()), C.c_void_p(src_ptr), nbytes, 3,
+                            _stream(stream))
+    if rc != 0:
+        raise SrlError(f"cudaMemcpyAsync failed: {rc}")
+    return dst
+
+
+@dataclass
+class NetSpec:
+    obs_dim: int
+    hidden: tuple
+    heads: tuple
+    ld_obs: int = 0
+    clip_eps: float = 0.2
+    value_coef: float = 0.5
+    entropy_coef: float = 0.01
+    lr: float = 3e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    adv_eps: float = 1e-8
+
+    @classmethod
+    def from_config(cls, cfg):
+        return cls(cfg.obs_dim, tuple(cfg.hidden), tuple(cfg.heads), cfg.ld_obs, cfg.clip_eps,
+                   cfg.value_coef, cfg.entropy_coef, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps)
+
+
+class PPOContext:
+    """Owns an srl_ctx: params (f32 master + f16 shadows), Adam state, gradient bucket,
+    workspace and (world > 1) the NCCL communicator."""
+
+    def __init__(self, spec: NetSpec, max_local_n: int, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None, device: int | None = None):
+        self.spec = spec
+        self.device = torch.cuda.current_device() if device is None else device
+        self._hid = (C.c_int * len(spec.hidden))(*spec.hidden)
+        self._heads = (C.c_int * len(spec.heads))(*spec.heads)
+        ld = spec.ld_obs or (spec.obs_dim + 7) // 8 * 8
+        self.cfg = PPOConfigC(spec.obs_dim, ld, len(spec.hidden), self._hid, len(spec.heads),
+                              self._heads, spec.clip_eps, spec.value_coef, spec.entropy_coef,
+                              spec.lr, spec.beta1, spec.beta2, spec.adam_eps, spec.adv_eps,
+                              int(max_local_n), 0)
+        h = C.c_void_p()
+        _check(lib().srl_ppo_create(C.byref(self.cfg), rank, world, nccl_id, self.device,
+                                    C.byref(h)))
+        self.handle = h
+        self.rank, self.world = rank, world
+        p, g, P, dg = C.c_void_p(), C.c_void_p(), C.c_int64(), C.c_uint64()
+        _check(lib().srl_ppo_params(h, C.byref(p), C.byref(g), C.byref(P), C.byref(dg)))
+        self.params_ptr, self.grads_ptr, self.P, self.layout_digest = p.value, g.value, P.value, dg.value
+        m, v, t = C.c_void_p(), C.c_void_p(), C.c_int64()
+        _check(lib().srl_ppo_adam_state(h, C.byref(m), C.byref(v), C.byref(t)))
+        self.m_ptr, self.v_ptr = m.value, v.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().srl_ppo_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load_params(self, params: torch.Tensor, stream=None):
+        _cuda(params, torch.float32, "params")
+        assert params.numel() == self.P
+        _check(lib().srl_ppo_load_params(self.handle, _ptr(params), _stream(stream)))
+
+    def _read(self, ptr, n, stream=None):
+        out = torch.empty(n, dtype=torch.float32, device=f"cuda:{self.device}")
+        return copy_from_device_ptr(out, ptr, 4 * n, stream)
+
+    def params(self, stream=None):
+        return self._read(self.params_ptr, self.P, stream)
+
+    def grads(self, stream=None):
+        """The gradient bucket [P + 8] (gradients, then the 8 reduced statistics)."""
+        return self._read(self.grads_ptr, self.P + 8, stream)
+
+    def adam_state(self, stream=None):
+        return self._read(self.m_ptr, self.P, stream), self._read(self.v_ptr, self.P, stream)
+
+    def step(self, n_global, obs, actions, logp_old, adv, ret, adv_mean_std=None, apply=True,
+             stats=None, stream=None):
+        """srl_ppo_step; returns the device stats buffer (uint8 [sizeof srl_ppo_stats])."""
+        _cuda(obs, torch.float16, "obs")
+        _cuda(actions, torch.int32, "actions")
+        for t, nm in ((logp_old, "logp_old"), (adv, "adv"), (ret, "ret")):
+            _cuda(t, torch.float32, nm)
+        n_local = logp_old.numel()
+        if stats is None:
+            stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
+        _check(lib().srl_ppo_step(self.handle, n_local, int(n_global), _ptr(obs), _ptr(actions),
+                                  _ptr(logp_old), _ptr(adv), _ptr(ret), _ptr(adv_mean_std),
+                                  int(apply), _ptr(stats), _stream(stream)))
+        return stats
+
+    def profile(self, on: bool = True):
+        _check(lib().srl_prof_enable(self.handle, int(on)))
+
+    def prof_reset(self):
+        _check(lib().srl_prof_reset(self.handle))
+
+    def prof_records(self):
+        """[(name, ms, flops, bytes)] for every launch recorded since the last reset."""
+        out = []
+        nm, ms, fl, by = C.c_char_p(), C.c_float(), C.c_double(), C.c_double()
+        for i in range(lib().srl_prof_count(self.handle)):
+            _check(lib().srl_prof_read(self.handle, i, C.byref(nm), C.byref(ms), C.byref(fl),
+                                       C.byref(by)))
+            out.append((nm.value.decode(), ms.value, fl.value, by.value))
+        return out
+
+    def allreduce_grads(self, buf: torch.Tensor, op: int = 0, stream=None):
+        _cuda(buf, torch.float32, "buf")
+        _check(lib().srl_allreduce_grads(self.handle, _ptr(buf), buf.numel(), op, _stream(stream)))
+        return buf
+
+
+def decode_stats(stats_u8: torch.Tensor) -> dict:
+    raw = bytes(stats_u8.cpu().numpy().tobytes())
+    s = PPOStatsC.from_buffer_copy(raw)
+    return {k: getattr(s, k) for k in STATS_FIELDS}
+
+
+def debug_gemm(A, a_mn, B, b_mn, M, N, K, bn=128, splits=1, stream=None):
+    """Test hook: D[M][N] = sum_k A(m,k) B(n,k) through the tcgen05 GEMM (EPI_PART path)."""
+    D = torch.empty(M, N, dtype=torch.float32, device=A.device)
+    _check(lib().srl_debug_gemm(M, N, K, _ptr(A), int(a_mn), A.shape[1], _ptr(B), int(b_mn),
+                                B.shape[1], bn, splits, _ptr(D), _stream(stream)))
+    return D

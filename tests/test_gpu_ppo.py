@@ -1,0 +1,132 @@
+"""a3-a7 parity: the full trainer step through the C ABI vs the oracle (C-T3..C-T6).
+
+Sizes: every BASELINE.json config at its true T, widths and heads, with B reduced so the
+oracle finishes in seconds while still spanning several 128-row tiles and a ragged tail.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from ppo_harness import gpu_step, grad_errors, make_inputs, oracle_term_scales
+
+pytestmark = pytest.mark.gpu
+
+REDUCED = {"tiny": 4, "atari": 16, "gfootball": 16, "smac": 20, "hns": 4}
+TOL = 2e-3
+
+
+def _check_grads(cfg, g, gref):
+    errs = grad_errors(cfg, g, gref)
+    bad = {k: v for k, v in errs.items() if v[0] > TOL or v[1] > TOL}
+    assert not bad, bad
+
+
+def _check_stats(cfg, st, o, sc):
+    N = o["N"]
+    ref = o["sums"] / N
+    assert abs(st["policy_loss"] - ref[0]) <= TOL * sc["pg"]
+    assert abs(st["value_loss"] - ref[1]) <= TOL * sc["v"]
+    assert abs(st["entropy"] - ref[2]) <= TOL * sc["ent"]
+    assert abs(st["clip_fraction"] - ref[3]) <= sc["clip_near"] + 1.0 / N
+    assert abs(st["approx_kl"] - ref[4]) <= TOL * sc["kl"]
+    assert st["n_global"] == N and st["nonfinite"] == 0
+
+
+@pytest.mark.parametrize("name", list(REDUCED))
+@pytest.mark.parametrize("stress", [False, True])
+def test_ppo_step_grad_parity(name, stress):
+    cfg = synth.get_config(name).with_(B=REDUCED[name] * synth.get_config(name).agents)
+    params, b = make_inputs(cfg, seed=11, stress=stress)
+    g = gpu_step(cfg, params, [b], apply=False)
+    o = oracle.ppo_step(cfg, params, [b], apply=False)
+    _check_grads(cfg, g["bucket"][:cfg.n_params], o["grad"])
+    _check_stats(cfg, g["stats"], o, oracle_term_scales(cfg, params, [b], o))
+    assert abs(g["mean_std"][0] - o["mean"]) <= 1e-6 * o["std"]
+    assert abs(g["mean_std"][1] - o["std"]) <= 1e-6 * o["std"]
+    assert g["stats"]["step"] == 0          # apply = 0: no Adam, no version bump
+
+
+@pytest.mark.parametrize("name", ["tiny", "gfootball", "hns"])
+def test_ppo_step_apply_adam(name):
+    """a6/a7 at K=1: Adam on the kernel's own gradient matches the oracle's Adam on that same
+    gradient (C-T5, 'identical G'), t advances, and the fp16 shadow feeds the next forward."""
+    cfg = synth.get_config(name).with_(B=REDUCED[name] * synth.get_config(name).agents)
+    params, b = make_inputs(cfg, seed=5)
+    g = gpu_step(cfg, params, [b], apply=True)
+    G = g["bucket"][:cfg.n_params]
+    p = params.astype(np.float64).copy()
+    m, v = np.zeros_like(p), np.zeros_like(p)
+    oracle.adam(p, m, v, G, 1, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps)
+    dp_ref = p - params
+    dp = g["params"] - params
+    assert np.linalg.norm(dp - dp_ref) / np.linalg.norm(dp_ref) <= 1e-5
+    assert np.abs(g["m"] - m).max() <= 1e-6 * np.abs(m).max()
+    assert g["stats"]["step"] == 1
+    # the step's gradient itself still matches the oracle
+    o = oracle.ppo_step(cfg, params, [b], apply=False)
+    _check_grads(cfg, G, o["grad"])
+
+
+def test_two_steps_uses_updated_shadow():
+    """Second step's gradient is taken at the Adam-updated parameters (fp16 shadow refreshed)."""
+    cfg = synth.get_config("tiny").with_(B=8)
+    params, b = make_inputs(cfg, seed=7)
+    g = gpu_step(cfg, params, [b], apply=True, n_steps=1)
+    p1 = g["params"].astype(np.float32)
+    ctx = g["ctx"]
+    g2 = gpu_step(cfg, params, [b], apply=False, ctx=ctx)
+    o = oracle.ppo_step(cfg, p1, [b], apply=False)
+    _check_grads(cfg, g2["bucket"][:cfg.n_params], o["grad"])
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_virtual_ranks_equal_full_batch(K):
+    """C-T6 on one GPU: K column shards through the same kernels (apply=0, 1/N_global) summed
+    in rank order equal the K=1 gradient; both match the oracle's full batch."""
+    cfg = synth.get_config("gfootball").with_(B=16)
+    params, full = make_inputs(cfg, seed=3)
+    shards = [make_inputs(cfg, seed=3, world=K, rank=k)[1] for k in range(K)]
+    g1 = gpu_step(cfg, params, [full], apply=False)
+    gK = gpu_step(cfg, params, shards, apply=False)
+    a, b = gK["bucket"][:cfg.n_params], g1["bucket"][:cfg.n_params]
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
+    o = oracle.ppo_step(cfg, params, [full], apply=False)
+    _check_grads(cfg, a, o["grad"])
+
+
+@pytest.mark.parametrize("name", ["smac", "hns"])
+def test_clip_decisions_differ_only_near_kink(name):
+    """Raw recipe (no kink margin): the kernel's clip decisions (fp32 from the fp16 forward)
+    may differ from the oracle's (double) only for samples whose oracle log-ratio lies within
+    0.01 of a kink; the clip fraction reflects exactly that."""
+    cfg = synth.get_config(name).with_(B=REDUCED[name] * synth.get_config(name).agents)
+    params, b = make_inputs(cfg, seed=11, margin=0.0)
+    g = gpu_step(cfg, params, [b], apply=False)
+    o = oracle.ppo_step(cfg, params, [b], apply=False)
+    xi = oracle.log_pi(cfg, params, b["obs"], b["actions"]) - b["logp_old"]
+    near = sum(np.sum(np.abs(xi - np.log(1 + s * cfg.clip_eps)) < 0.01) for s in (1, -1))
+    assert abs(g["stats"]["clip_fraction"] - o["sums"][3] / o["N"]) <= near / o["N"] + 1e-7
+
+
+def test_zero_params_uniform_policy():
+    """Zero network: logits 0, entropy = sum ln A_h exactly, V = 0."""
+    import paper_2306_16688_b200 as P
+    cfg = synth.get_config("hns").with_(B=4)
+    params = np.zeros(cfg.n_params, np.float32)
+    _, b = make_inputs(cfg, seed=1)
+    g = gpu_step(cfg, params, [b], apply=False)
+    assert abs(g["stats"]["entropy"] - sum(np.log(a) for a in cfg.heads)) < 1e-5
+
+
+def test_nonfinite_skips_adam():
+    """A NaN observation makes its loss non-finite: the step reports it and Adam is skipped."""
+    cfg = synth.get_config("tiny")
+    params, b = make_inputs(cfg, seed=2)
+    b["obs"] = b["obs"].copy()
+    b["obs"][5, 0] = np.float16(np.nan)
+    g = gpu_step(cfg, params, [b], apply=True)
+    assert g["stats"]["nonfinite"] >= 1
+    assert g["stats"]["step"] == 0
+    assert np.array_equal(g["params"], params.astype(np.float64))
