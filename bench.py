@@ -200,28 +200,13 @@ def main_ours(args, world, rank, local):
                        nccl_id=nccl_id, device=local)
     ctx.load_params(params)
     T, Bk = b["rewards"].shape
-    adv = torch.empty(T, Bk, dtype=torch.float32, device=dev)
-    ret = torch.empty_like(adv)
-    gst = torch.empty(3, dtype=torch.float64, device=dev)
-    ms = torch.empty(2, dtype=torch.float64, device=dev)
     stats = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8, device=dev)
     stats_host = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8).pin_memory()
-    stream = torch.cuda.current_stream()
-    gae_ev = []
 
-    def step(src, timed_gae=False):
-        if timed_gae:
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record()
-        P.gae(src["rewards"], src["values"], src["dones"], cfg.gamma, cfg.lam, adv=adv, ret=ret, stats=gst)
-        if timed_gae:
-            e1.record()
-        P.adv_norm(adv.view(-1), local_stats=gst, ctx=ctx, mean_std=ms)
-        if timed_gae:
-            e2.record()
-            gae_ev.append((e0, e1, e2))
-        ctx.step(N, src["obs"], src["actions"], src["logp_old"], adv.view(-1), ret.view(-1), ms,
-                 apply=True, stats=stats)
+    def step(src):
+        # one C-ABI call: GAE -> global normalisation -> forward/loss/backward -> allreduce -> Adam
+        ctx.train_step(N, src["rewards"], src["values"], src["dones"], src["obs"], src["actions"],
+                       src["logp_old"], stats=stats)
 
     def barrier():
         torch.cuda.synchronize()
@@ -251,16 +236,16 @@ def main_ours(args, world, rank, local):
     barrier()
     wall0 = time.monotonic()
     e_start.record()
+    h0 = time.perf_counter()
     for _ in range(K):
-        step(d, timed_gae=True)
+        step(d)
+    host_ms = (time.perf_counter() - h0) * 1e3 / K
     e_end.record()
     barrier()
     wall1 = time.monotonic()
     ctx.profile(False)
     ms_total = max_over_ranks(e_start.elapsed_time(e_end))
     recs = ctx.prof_records()
-    gae_ms = [a.elapsed_time(b_) for a, b_, _ in gae_ev]
-    norm_ms = [b_.elapsed_time(c) for _, b_, c in gae_ev]
     stats_dev = P.decode_stats(stats)
 
     # ---------------- end to end: host (pinned) inputs copied in, stats copied out, per step
@@ -304,8 +289,6 @@ def main_ours(args, world, rank, local):
     for name, t, fl, by in recs:
         a = agg.setdefault(name, [0.0, 0, 0.0, 0.0])
         a[0] += t; a[1] += 1; a[2] += fl; a[3] += by
-    agg["gae_scan"] = [sum(gae_ms), len(gae_ms), 0.0, 17.0 * n * len(gae_ms)]
-    agg["adv_norm"] = [sum(norm_ms), len(norm_ms), 0.0, 0.0]
     step_ms = ms_total / K
     kernels = []
     for name, (t, cnt, fl, by) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
@@ -330,10 +313,10 @@ def main_ours(args, world, rank, local):
                 "unit": "TFLOP/s", "frac": achieved / tf_sus, "traffic": traffic,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (fp16 dense = bf16 dense, nominal ratio 1)",
                 "flops_per_launch": dfl / dcnt, "ms_per_launch": davg_s * 1e3}
-    # our kernels per step: gae_kernel + merge (srl_gae), merge (srl_adv_norm), the ppo step's
-    # 3L+2 GEMMs, finalize_w + finalize_b + extras, adam, stats (NCCL's kernels not counted)
+    # our kernels per step (srl_ppo_train_step): gae_kernel, moments merge (2 when world > 1),
+    # the 3L+2 GEMMs, finalize_w + finalize_b + extras, adam, stats (NCCL's kernels not counted)
     L = len(cfg.hidden)
-    per_step = 2 + 1 + (L + 1 + (L + 1) + L) + 3 + 1 + 1
+    per_step = 1 + (2 if world > 1 else 1) + (L + 1 + (L + 1) + L) + 3 + 1 + 1
     cpu = None
     if not args.no_cpu_baseline:
         v, cn, Bp, secs = time_oracle(cfg, args.cpu_seconds)
@@ -354,6 +337,7 @@ def main_ours(args, world, rank, local):
                              n * cfg.ld_obs * 2 / 1e6, n * sum(cfg.hidden) * 2 / 1e6,
                              n * max(cfg.hidden) * 4 / 1e6)},
         "frames_per_s": N * cfg.frame_skip * K / (ms_total * 1e-3),
+        "host_submit_ms_per_step": host_ms,
         "e2e": {"value": N * Ke / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes * world,
                 "d2h_bytes_per_step": P.srl.STATS_BYTES * world, "steps": Ke},
         "gpu_launches": per_step * K,

@@ -95,6 +95,8 @@ typedef struct srl_ppo_config {
   float clip_eps, value_coef, entropy_coef;   /* 0.2, 0.5, 0.01 (C-A5) */
   float lr, beta1, beta2, adam_eps;           /* 3e-4, 0.9, 0.999, 1e-8 (C-A13) */
   float adv_eps;            /* 1e-8: A_hat = (A - mu) / (sigma + adv_eps) inside the loss */
+  float gamma, gae_lambda;  /* 0.99, 0.95: GAE of srl_ppo_train_step */
+  int adv_unbiased;         /* 0: population sigma (default, C-A4); 1: N-1 */
   int64_t max_local_n;      /* workspace sizing: largest n_local passed to srl_ppo_step */
   int precision;            /* srl_precision */
 } srl_ppo_config;
@@ -153,6 +155,18 @@ srl_status srl_ppo_step(srl_ctx* ctx, int64_t n_local, int64_t n_global,
                         const uint16_t* obs, const int32_t* actions, const float* logp_old,
                         const float* adv, const float* ret, const double* adv_mean_std,
                         int apply, srl_ppo_stats* stats_out, srl_stream_t stream);
+
+/* One whole trainer step on this rank's shard of a time-major batch (rows a1 -> a7):
+ * srl_gae into context-owned adv/ret (cfg gamma, gae_lambda), global normalisation moments
+ * (NCCL all-gather of {n, mean, M2} when world > 1), then srl_ppo_step(apply = 1).
+ * This is Algorithm.step(sample) (PAPER.md Code 1, L649-654) for PPO.
+ *   rewards f32 [T][B], values f32 [T+1][B], dones u8 [T][B] (dense, ld = B)
+ *   obs f16 bits [T*B][ld_obs], actions i32 [T*B][H], logp_old f32 [T*B] (sample i = t*B + b)
+ *   n_global = sum over ranks of T*B.  T*B <= max_local_n. */
+srl_status srl_ppo_train_step(srl_ctx* ctx, int T, int B, int64_t n_global,
+                              const float* rewards, const float* values, const uint8_t* dones,
+                              const uint16_t* obs, const int32_t* actions, const float* logp_old,
+                              srl_ppo_stats* stats_out, srl_stream_t stream);
 
 /* a6: in-place allreduce over the ctx's ranks of a device f32 buffer (SPEC reduce_gradients
  * S:L505-513): op 0 = sum, op 1 = mean.  world == 1: identity (op 1 leaves values as is). */

@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -115,7 +117,25 @@ struct srl_ctx {
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
   size_t pool_used = 0;
+  // tensor-map cache: encoding is host work; the maps depend only on pointer + shape
+  std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t>, CUtensorMap> tmaps;
+  // train-step buffers (srl_ppo_train_step): adv, ret [max_n] f32; gae partials; mean/std
+  float *adv = nullptr, *ret = nullptr;
+  double *gae_part = nullptr, *gae_stats = nullptr, *mean_std = nullptr;
+  int gae_part_cap = 0;
 };
+
+static bool get_tmap(srl_ctx* c, CUtensorMap* out, const void* base, uint64_t inner,
+                     uint64_t outer, uint64_t row_bytes, uint32_t bi, uint32_t bo,
+                     int swizzle = 128) {
+  auto key = std::make_tuple(base, inner, outer, row_bytes, bi, bo * 1000 + swizzle);
+  auto it = c->tmaps.find(key);
+  if (it != c->tmaps.end()) { *out = it->second; return true; }
+  if (!make_tmap_2d(out, base, inner, outer, row_bytes, bi, bo, swizzle)) return false;
+  if (c->tmaps.size() > 4096) c->tmaps.clear();
+  c->tmaps.emplace(key, *out);
+  return true;
+}
 
 static cudaEvent_t prof_event(srl_ctx* c) {
   if (c->pool_used == c->pool.size()) {
@@ -295,8 +315,9 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   for (int l = 0; l <= c->L; ++l) {
     Lay& y = c->lay[l];
     if ((st = dalloc(c, &y.w16, sizeof(__half) * (size_t)y.w16_rows * y.w16_ld))) return bail(st);
-    y.bn_fwd = (l == c->L) ? kHeadCols : pick_bn(y.out);
-    y.bn_dx = pick_bn(y.in);
+    // epilogue-heavy GEMMs (fwd tanh, dX dtanh) use 128-wide tiles: 4 TMEM accumulators
+    y.bn_fwd = (l == c->L) ? kHeadCols : (y.out % 128 == 0 ? 128 : 64);
+    y.bn_dx = (y.in % 128 == 0) ? 128 : 64;
     // dW: hidden layer: D[out][in] = dZ^T X; head: D^T[in][64] = Y^T g
     const int dM = (l == c->L) ? y.in : y.out;
     const int dN = (l == c->L) ? kHeadCols : y.in;
@@ -316,6 +337,12 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if ((st = dalloc(c, &c->G16, sizeof(__half) * (size_t)n * kHeadCols))) return bail(st);
   for (int k = 0; k < 2; ++k)
     if ((st = dalloc(c, &c->dZ[k], sizeof(__half) * (size_t)n * max_h))) return bail(st);
+  if ((st = dalloc(c, &c->adv, sizeof(float) * n))) return bail(st);
+  if ((st = dalloc(c, &c->ret, sizeof(float) * n))) return bail(st);
+  c->gae_part_cap = (int)((n + 31) / 32) + 1;
+  if ((st = dalloc(c, &c->gae_part, sizeof(double) * 3 * c->gae_part_cap))) return bail(st);
+  if ((st = dalloc(c, &c->gae_stats, sizeof(double) * 4))) return bail(st);
+  if ((st = dalloc(c, &c->mean_std, sizeof(double) * 2))) return bail(st);
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(id.internal, nccl_id, 128);
@@ -424,12 +451,12 @@ extern "C" srl_status srl_allreduce_grads(srl_ctx* c, float* buf, int64_t count,
 
 // ------------------------------------------------------------------ a3..a7
 static srl_status gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
-                       const CUtensorMap& tb, GemmArgs& g, int sms, cudaStream_t s,
-                       int* grid_out = nullptr) {
+                       const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& ty,
+                       GemmArgs& g, int sms, cudaStream_t s, int* grid_out = nullptr) {
   const int units = g.m_tiles * g.n_tiles * g.k_splits;
   const int grid = std::min(units, sms);
   if (grid_out) *grid_out = grid;
-  cudaError_t e = launch_gemm(bn, a_mn, b_mn, epi, ta, tb, g, grid, s);
+  cudaError_t e = launch_gemm(bn, a_mn, b_mn, epi, ta, tb, to, ty, g, grid, s);
   if (e != cudaSuccess) FAIL(SRL_ECUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   return SRL_OK;
 }
@@ -437,6 +464,10 @@ static srl_status gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap&
 #define TM(map, ...)                                                             \
   do {                                                                           \
     if (!make_tmap_2d(&(map), __VA_ARGS__)) FAIL(SRL_ECUDA, "tensor map encode failed"); \
+  } while (0)
+#define TMC(map, ...)                                                            \
+  do {                                                                           \
+    if (!get_tmap(c, &(map), __VA_ARGS__)) FAIL(SRL_ECUDA, "tensor map encode failed"); \
   } while (0)
 
 extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global,
@@ -465,30 +496,32 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     CUtensorMap ta, tb;
     const __half* X = l == 0 ? X0 : c->Y[l - 1];
     const int ldx = l == 0 ? ld_obs : y.in;
-    TM(ta, X, y.in, n, (uint64_t)ldx * 2, 64, 128);
-    TM(tb, y.w16, y.in, y.out, (uint64_t)y.w16_ld * 2, 64, y.bn_fwd);
+    TMC(ta, X, y.in, n, (uint64_t)ldx * 2, 64, 128);
+    TMC(tb, y.w16, y.in, y.out, (uint64_t)y.w16_ld * 2, 64, y.bn_fwd);
+    CUtensorMap to;
+    TMC(to, c->Y[l], y.out, n, (uint64_t)y.out * 2, 32, 32, 64);
     GemmArgs g{};
     g.M = n; g.N = y.out;
     g.m_tiles = (n + 127) / 128; g.n_tiles = y.out / y.bn_fwd; g.k_splits = 1;
     g.kb_total = (y.in + 63) / 64; g.kb_per_split = g.kb_total;
-    g.out = c->Y[l]; g.ld_out = y.out;
     g.bias = c->params + y.b_off;
     ProfScope ps(c, s, l == 0 ? "fwd_l1" : "fwd_hidden", 2.0 * n * y.in * y.out,
                  2.0 * n * (y.in + y.out) + 2.0 * y.in * y.out + 4.0 * y.out);
-    if (srl_status st = gemm(y.bn_fwd, false, false, EPI_TANH, ta, tb, g, sms, s)) return st;
+    if (srl_status st = gemm(y.bn_fwd, false, false, EPI_TANH, ta, tb, to, to, g, sms, s)) return st;
   }
   // ---------------- a4: head GEMM + fused PPO loss -> per-sample dlogits G16
   const Lay& hd = c->lay[L];
   int grid_loss = 0;
   {
     CUtensorMap ta, tb;
-    TM(ta, c->Y[L - 1], hd.in, n, (uint64_t)hd.in * 2, 64, 128);
-    TM(tb, hd.w16, hd.in, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
+    TMC(ta, c->Y[L - 1], hd.in, n, (uint64_t)hd.in * 2, 64, 128);
+    TMC(tb, hd.w16, hd.in, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
+    CUtensorMap to;
+    TMC(to, c->G16, kHeadCols, n, (uint64_t)kHeadCols * 2, 32, 32, 64);
     GemmArgs g{};
     g.M = n; g.N = kHeadCols;
     g.m_tiles = (n + 127) / 128; g.n_tiles = 1; g.k_splits = 1;
     g.kb_total = (hd.in + 63) / 64; g.kb_per_split = g.kb_total;
-    g.out = c->G16; g.ld_out = kHeadCols;
     g.bias = c->params + hd.b_off;
     g.colsum = hd.colsum; g.colsum_ld = kHeadCols;
     g.counters = c->counters;
@@ -500,7 +533,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     g.entropy_coef = c->cfg.entropy_coef; g.adv_eps = c->cfg.adv_eps;
     ProfScope ps(c, s, "head_loss", 2.0 * n * hd.in * hd.out,
                  2.0 * n * hd.in + 2.0 * n * kHeadCols + (16.0 + 4.0 * g.n_heads) * n);
-    if (srl_status st = gemm(64, false, false, EPI_LOSS, ta, tb, g, sms, s, &grid_loss)) return st;
+    if (srl_status st = gemm(64, false, false, EPI_LOSS, ta, tb, to, to, g, sms, s, &grid_loss)) return st;
   }
   // ---------------- a5: backward.  dW via split-K partials, dX with fused dtanh + db sums
   std::vector<int> splits(L + 1, 1), colsum_parts(L + 1, 0);
@@ -510,8 +543,8 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     const int dM = (l == L) ? y.in : y.out;
     const int dN = (l == L) ? kHeadCols : y.in;
     CUtensorMap ta, tb;
-    TM(ta, Amat, dM, n, (uint64_t)lda * 2, 64, 64);
-    TM(tb, Bmat, dN, n, (uint64_t)ldb * 2, 64, 64);
+    TMC(ta, Amat, dM, n, (uint64_t)lda * 2, 64, 64);
+    TMC(tb, Bmat, dN, n, (uint64_t)ldb * 2, 64, 64);
     GemmArgs g{};
     g.M = dM; g.N = dN;
     g.m_tiles = y.dw_m_tiles; g.n_tiles = y.dw_n_tiles;
@@ -525,28 +558,29 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     const int realN = (l == L) ? y.out : dN;
     ProfScope ps(c, s, l == L ? "dW_head" : (l == 0 ? "dW_l1" : "dW_hidden"),
                  2.0 * n * dM * realN, 2.0 * n * (dM + dN) + 4.0 * S * dM * y.ld_part);
-    return gemm(y.bn_dw, true, true, EPI_PART, ta, tb, g, sms, s);
+    return gemm(y.bn_dw, true, true, EPI_PART, ta, tb, ta, ta, g, sms, s);
   };
   auto dX = [&](int l, const __half* dz_in, int k_width, __half* dz_out) -> srl_status {
     // dZ_{in of layer l} = (dZ_out_l W_l) * (1 - Y_{l-1}^2), colsum -> db of layer l-1
     const Lay& y = c->lay[l];
     const Lay& yp = c->lay[l - 1];
     CUtensorMap ta, tb;
-    TM(ta, dz_in, k_width, n, (uint64_t)k_width * 2, 64, 128);
-    TM(tb, y.w16, y.in, y.w16_rows, (uint64_t)y.w16_ld * 2, 64, 64);
+    TMC(ta, dz_in, k_width, n, (uint64_t)k_width * 2, 64, 128);
+    TMC(tb, y.w16, y.in, y.w16_rows, (uint64_t)y.w16_ld * 2, 64, 64);
+    CUtensorMap to, ty;
+    TMC(to, dz_out, y.in, n, (uint64_t)y.in * 2, 32, 32, 64);
+    TMC(ty, c->Y[l - 1], y.in, n, (uint64_t)y.in * 2, 32, 32, 64);
     GemmArgs g{};
     g.M = n; g.N = y.in;
     g.m_tiles = (n + 127) / 128; g.n_tiles = y.in / y.bn_dx; g.k_splits = 1;
     g.kb_total = (k_width + 63) / 64; g.kb_per_split = g.kb_total;
-    g.out = dz_out; g.ld_out = y.in;
-    g.y_prev = c->Y[l - 1]; g.ld_y = y.in;
     g.colsum = yp.colsum; g.colsum_ld = yp.colsum_ld;
     g.counters = c->counters;
     int grid = 0;
     const int realK = (l == L) ? y.out : k_width;
     ProfScope ps(c, s, l == L ? "dX_head" : "dX_hidden", 2.0 * n * realK * y.in,
                  2.0 * n * (k_width + 2.0 * y.in) + 2.0 * y.in * k_width);
-    srl_status st = gemm(y.bn_dx, false, true, EPI_DTANH, ta, tb, g, sms, s, &grid);
+    srl_status st = gemm(y.bn_dx, false, true, EPI_DTANH, ta, tb, to, ty, g, sms, s, &grid);
     colsum_parts[l - 1] = grid;
     return st;
   };
@@ -586,6 +620,41 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   CK(launch_stats(c->grads, c->P, adv_mean_std, n_global, c->cfg.value_coef, c->cfg.entropy_coef,
                   c->t_dev, apply, stats_out, s));
   return SRL_OK;
+}
+
+// ------------------------------------------------------------------ a1..a7 in one call
+extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_global,
+                                         const float* rewards, const float* values,
+                                         const uint8_t* dones, const uint16_t* obs,
+                                         const int32_t* actions, const float* logp_old,
+                                         srl_ppo_stats* stats_out, srl_stream_t stream) {
+  if (!c) FAIL(SRL_EINVAL, "srl_ppo_train_step: null ctx");
+  if (T < 1 || B < 1 || (int64_t)T * B > c->max_n || n_global < (int64_t)T * B)
+    FAIL(SRL_EINVAL, "srl_ppo_train_step: need 1 <= T*B <= max_local_n <= n_global");
+  if (!rewards || !values || !dones) FAIL(SRL_EINVAL, "srl_ppo_train_step: null trajectory input");
+  const int nb = gae_num_blocks(B);
+  if (nb > c->gae_part_cap) FAIL(SRL_EINVAL, "srl_ppo_train_step: B too large");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n = (int64_t)T * B;
+  {
+    ProfScope ps(c, s, "gae_scan", 0.0, 17.0 * n);
+    CK(launch_gae(T, B, B, rewards, values, dones, c->cfg.gamma, c->cfg.gae_lambda, c->adv,
+                  c->ret, c->gae_part, s));
+  }
+  {
+    ProfScope ps(c, s, "adv_norm", 0.0, 24.0 * nb);
+    if (c->world > 1) {
+      CK(launch_merge_moments(c->gae_part, nb, c->gae_stats, nullptr, 0, s));
+      double* gathered = c->norm_scratch;
+      CKN(ncclAllGather(c->gae_stats, gathered, 3, ncclDouble, c->comm, s));
+      CK(launch_merge_moments(gathered, c->world, nullptr, c->mean_std, c->cfg.adv_unbiased, s));
+    } else {
+      CK(launch_merge_moments(c->gae_part, nb, c->gae_stats, c->mean_std, c->cfg.adv_unbiased, s));
+    }
+  }
+  return srl_ppo_step(c, n, n_global, obs, actions, logp_old, c->adv, c->ret, c->mean_std, 1,
+                      stats_out, stream);
 }
 
 // ------------------------------------------------------------------ profiling
@@ -657,7 +726,7 @@ extern "C" srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int
   float* part = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * S * g.part_split_stride, s));
   g.part = part;
-  if (srl_status st = gemm(bn, a_mn != 0, b_mn != 0, EPI_PART, ta, tb, g, num_sms(), s)) return st;
+  if (srl_status st = gemm(bn, a_mn != 0, b_mn != 0, EPI_PART, ta, tb, ta, ta, g, num_sms(), s)) return st;
   sum_parts_kernel<<<256, 256, 0, s>>>(part, S, g.part_split_stride, M, N, g.ld_part, D);
   CK(cudaGetLastError());
   CK(cudaFreeAsync(part, s));

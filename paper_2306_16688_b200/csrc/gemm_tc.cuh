@@ -4,15 +4,17 @@
 //   A(m,k): K-major = row-major [M][K] (A_MN=false)  |  MN-major = row-major [K][M] (A_MN=true)
 //   B(n,k): K-major = row-major [N][K] (B_MN=false)  |  MN-major = row-major [K][N] (B_MN=true)
 //
-// Tile 128 x BN x 64, SWIZZLE_128B smem operands fed by TMA through an mbarrier ring,
-// one elected thread issues tcgen05.mma (kind::f16, M=128), two TMEM accumulators so the
-// epilogue of tile i overlaps the MMAs of tile i+1.  Persistent CTAs walk the work units
-// (m tile, n tile, k split) with a static stride, so every per-CTA partial is deterministic.
+// Tile 128 x BN x 64, SWIZZLE_128B smem operands fed by TMA through an mbarrier ring of
+// args.stages slots; one elected thread issues tcgen05.mma (kind::f16, M=128) into 512/BN
+// TMEM accumulators, so the MMA runs up to 512/BN - 1 tiles ahead of the epilogue.
+// Persistent CTAs walk the work units (m tile, n tile, k split) with a static stride, so every
+// per-CTA partial is deterministic.
 //
 // Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w3 idle,
-// w4..w11 epilogue in two warpgroups g = 0, 1 that take alternate tiles (group g owns TMEM
-// accumulator stage g), so each group has two MMA periods to drain a tile; warp w reads TMEM
-// lanes 32(w%4)..32(w%4)+31 = tile rows of that quadrant.
+// w4..w11 epilogue in two warpgroups g = 0, 1 that take alternate tiles (tile i uses TMEM
+// stage i % ACC_STAGES, drained by group i % 2); warp w reads TMEM lanes 32(w%4)..+31.
+// Epilogue output goes through per-warp 32x32 fp16 staging tiles (64-byte swizzle, conflict
+// free) and leaves by TMA bulk-tensor stores; y_prev tiles arrive by TMA loads.
 //
 // Epilogues (rows a3-a5):
 //   EPI_TANH  : out16 = tanh(acc + bias)                          (forward hidden layer, a3)
@@ -37,11 +39,10 @@ struct GemmArgs {
   int M, N;                       // valid rows / cols of D
   int m_tiles, n_tiles, k_splits;
   int kb_total, kb_per_split;     // 64-wide k blocks
-  // outputs / epilogue inputs
-  __half* out; int64_t ld_out;                    // TANH, DTANH, LOSS
+  int stages;                     // operand ring slots (<= 8), from gemm_stages()
+  // outputs / epilogue inputs (TANH/DTANH/LOSS write through the output tensor map)
   float* part; int64_t ld_part; int64_t part_split_stride;   // PART
   const float* bias;                              // TANH, LOSS
-  const __half* y_prev; int64_t ld_y;             // DTANH
   float* colsum; int colsum_ld;                   // DTANH, LOSS: [grid][colsum_ld]
   unsigned long long* counters;                   // [0] nonfinite, [1] fp16 saturations
   // loss (a4)
@@ -52,20 +53,52 @@ struct GemmArgs {
   float clip_eps, value_coef, entropy_coef, adv_eps;
 };
 
+// Shared-memory layout (identical on host and device):
+//   [operand ring][out staging 32 KB][y staging 32 KB (DTANH)][colsum 8 x ld][bias 4 KB][bars]
+struct SmemLayout {
+  uint32_t ring, ostage, ystage, colsum, bias, bars, total;
+};
+constexpr int kStageTile = 32 * 32 * 2;           // one 32x32 fp16 staging tile
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kBarBytes = 512;
+constexpr uint32_t kSmemLimit = 232448;           // 227 KB per CTA
+
+__host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, int colsum_ld) {
+  SmemLayout L;
+  const uint32_t stage_bytes = (uint32_t)(128 + bn) * 64 * 2;
+  L.ring = 0;
+  L.ostage = stages * stage_bytes;
+  const uint32_t ost = (epi == EPI_PART) ? 0 : kEpiWarps * 2 * kStageTile;
+  L.ystage = L.ostage + ost;
+  const uint32_t yst = (epi == EPI_DTANH) ? kEpiWarps * 2 * kStageTile : 0;
+  L.colsum = L.ystage + yst;
+  const uint32_t cs = (epi == EPI_DTANH || epi == EPI_LOSS) ? kEpiWarps * colsum_ld * 4 : 0;
+  L.bias = L.colsum + cs;
+  const uint32_t bs = (epi == EPI_TANH || epi == EPI_LOSS) ? 4096 : 0;
+  L.bars = L.bias + bs;
+  L.total = L.bars + kBarBytes;
+  return L;
+}
+
+// largest ring (<= 8 slots) that fits next to the epilogue buffers; 1 KB alignment slack and
+// 512 B for the kernel's static shared memory
+inline int gemm_stages(int bn, int epi, int colsum_ld) {
+  const uint32_t stage_bytes = (uint32_t)(128 + bn) * 64 * 2;
+  const SmemLayout z = smem_layout(bn, epi, 0, colsum_ld);
+  const int64_t avail = (int64_t)kSmemLimit - 1024 - 512 - z.total;
+  const int st = (int)(avail / stage_bytes);
+  return st > 8 ? 8 : st;
+}
+
 template <int BN>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;        // 128 / 256 / 512: power of two
-  static constexpr int BAR_BYTES = 256;
-  static constexpr int EPI_WARPS = 8;
-  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static size_t smem_bytes(int colsum_ld) {
-    return 1024 + (size_t)STAGES * STAGE_BYTES + BAR_BYTES + (size_t)EPI_WARPS * colsum_ld * 4;
-  }
+  static constexpr int ACC_STAGES = 512 / BN;     // TMEM accumulators: 2 / 4 / 8
+  static constexpr int TMEM_COLS = 512;
 };
 
 __device__ __forceinline__ void wait_bounded(uint64_t* bar, uint32_t parity) {
@@ -106,32 +139,38 @@ __device__ __forceinline__ float sat_f16(float x, uint32_t& nsat) {
   return x;
 }
 
-__device__ __forceinline__ void store32_f16(__half* dst, const float (&v)[32]) {
-  uint4* d4 = reinterpret_cast<uint4*>(dst);
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// row `r` (0..31) of a 32x32 fp16 staging tile in the TMA 64-byte swizzle: the 16-byte chunk
+// q of a row lives at chunk q ^ ((r >> 1) & 3).  Eight consecutive rows then hit 8 distinct
+// 16-byte bank groups: the row-per-thread writes/reads are conflict free.
+__device__ __forceinline__ uint32_t stile_off(int r, int q) {
+  return (uint32_t)(r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+}
+
+__device__ __forceinline__ void stile_write_row(uint8_t* tile, int r, const float (&v)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    __half2 h0 = __floats2half2_rn(v[8 * q + 0], v[8 * q + 1]);
-    __half2 h1 = __floats2half2_rn(v[8 * q + 2], v[8 * q + 3]);
-    __half2 h2 = __floats2half2_rn(v[8 * q + 4], v[8 * q + 5]);
-    __half2 h3 = __floats2half2_rn(v[8 * q + 6], v[8 * q + 7]);
     uint4 u;
-    u.x = *reinterpret_cast<uint32_t*>(&h0);
-    u.y = *reinterpret_cast<uint32_t*>(&h1);
-    u.z = *reinterpret_cast<uint32_t*>(&h2);
-    u.w = *reinterpret_cast<uint32_t*>(&h3);
-    d4[q] = u;
+    u.x = pack_half2(v[8 * q + 0], v[8 * q + 1]);
+    u.y = pack_half2(v[8 * q + 2], v[8 * q + 3]);
+    u.z = pack_half2(v[8 * q + 4], v[8 * q + 5]);
+    u.w = pack_half2(v[8 * q + 6], v[8 * q + 7]);
+    *reinterpret_cast<uint4*>(tile + stile_off(r, q)) = u;
   }
 }
 
-__device__ __forceinline__ void load32_f16(const __half* src, float (&y)[32]) {
-  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+__device__ __forceinline__ void stile_read_row(const uint8_t* tile, int r, float (&y)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    uint4 u = __ldg(s4 + q);
+    const uint4 u = *reinterpret_cast<const uint4*>(tile + stile_off(r, q));
     const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      float2 f = __half22float2(h[e]);
+      const float2 f = __half22float2(h[e]);
       y[8 * q + 2 * e] = f.x;
       y[8 * q + 2 * e + 1] = f.y;
     }
@@ -145,7 +184,7 @@ __device__ __forceinline__ void count_warp(unsigned long long* ctr, uint32_t n) 
 }
 
 // ---------------------------------------------------------------------------------------
-// a4: PPO loss on one row held in registers (z: 64 logits incl. bias; g out: dloss_i/dz).
+// a4: PPO loss on one row held in registers (z: 64 logits incl. bias in, dloss_i/dz out).
 // Formulas: DESIGN.md §3.1 (SURVEY C-4).
 __device__ __forceinline__ void ppo_row(const GemmArgs& a, float (&z)[64], const int* act,
                                         float Ahat, float lp_old, float R, double (&st)[5],
@@ -225,23 +264,48 @@ __device__ __forceinline__ void ppo_row(const GemmArgs& a, float (&z)[64], const
   st[4] += lp_old - logpi;
 }
 
+// Per-warp output staging: two 32x32 tiles, recycled once the TMA store has read them.
+struct OutStage {
+  uint8_t* buf;       // 2 x kStageTile, 1024-aligned
+  int k;              // tiles issued so far
+  __device__ __forceinline__ uint8_t* acquire() {
+    uint8_t* t = buf + (k & 1) * kStageTile;
+    if (k >= 2 && lane_id() == 0) bulk_wait_read<1>();   // the store 2 tiles ago has read t
+    __syncwarp();
+    return t;
+  }
+  __device__ __forceinline__ void release(uint8_t* t, const CUtensorMap* map, int col, int row) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane_id() == 0) {
+      tma_store_2d(map, t, col, row);
+      bulk_commit();
+    }
+    ++k;
+  }
+};
+
 // ---------------------------------------------------------------------------------------
 template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
+__global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmY,
                const GemmArgs args) {
   using Cfg = GemmCfg<BN>;
-  constexpr int STAGES = Cfg::STAGES;
   static_assert(EPI != EPI_LOSS || BN == kHeadCols, "loss epilogue works on the 64-col head");
+  const int STAGES = args.stages;
+  const SmemLayout SL = smem_layout(BN, EPI, STAGES, args.colsum_ld);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* colsum_s = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SL.bars);
+  uint64_t* empty = full + 8;
+  uint64_t* tfull = empty + 8;
+  uint64_t* tempty = tfull + 8;
+  uint64_t* ybar = tempty + 8;                    // [8 warps][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ybar + 16);
+  float* colsum_s = reinterpret_cast<float*>(smem + SL.colsum);
+  float* bias_s = reinterpret_cast<float*>(smem + SL.bias);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = lane_id();
@@ -254,10 +318,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < Cfg::ACC_STAGES; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4);
     }
+    for (int s = 0; s < 16; ++s) mbar_init(&ybar[s], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -305,12 +370,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     constexpr uint32_t IDESC = umma_idesc_f16(128, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
       const int ks = u / (args.n_tiles * args.m_tiles);
       const int kb0 = ks * args.kb_per_split;
       const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+      const int acc = it % Cfg::ACC_STAGES;
+      const uint32_t acc_phase = (uint32_t)(it / Cfg::ACC_STAGES) & 1u;
       wait_bounded(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -335,73 +401,103 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       if (lane == 0) tc_commit(&tfull[acc]);
       __syncwarp();
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
   } else if (warp >= 4) {
     // ============================ epilogue (two warpgroups, alternate tiles)
     const int ew = warp - 4;                 // 0..7
-    const int grp = ew >> 2;                 // warpgroup = TMEM accumulator stage it drains
-    const int quad = warp & 3;               // TMEM lane quadrant
-    const int trow = quad * 32 + (int)lane;
+    const int grp = ew >> 2;                 // warpgroup
+    const int quad = warp & 3;               // TMEM lane quadrant = 32-row slice of the tile
     float* my_colsum = colsum_s + ew * args.colsum_ld;
+    OutStage ost{smem + SL.ostage + ew * 2 * kStageTile, 0};
+    uint8_t* ystage = smem + SL.ystage + ew * 2 * kStageTile;
+    uint64_t* my_ybar = ybar + 2 * ew;
+    uint32_t yph0 = 0, yph1 = 0;
     if (EPI == EPI_DTANH || EPI == EPI_LOSS) {
       for (int i = lane; i < args.colsum_ld; i += 32) my_colsum[i] = 0.f;
       __syncwarp();
     }
+    if (EPI == EPI_TANH || EPI == EPI_LOSS) {
+      const int nb = (EPI == EPI_LOSS) ? args.A + 1 : args.N;
+      for (int i = ew * 32 + lane; i < 1024; i += 256) bias_s[i] = i < nb ? __ldg(args.bias + i) : 0.f;
+      named_bar_sync(1, 256);
+    }
     uint32_t nsat = 0, nonfinite = 0;
     double st[5] = {0, 0, 0, 0, 0};
-    uint32_t acc_phase = 0;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
       if ((it & 1) != grp) continue;
+      const int acc = it % Cfg::ACC_STAGES;
+      const uint32_t acc_phase = (uint32_t)(it / Cfg::ACC_STAGES) & 1u;
       const int nt = u % args.n_tiles;
       const int mt = (u / args.n_tiles) % args.m_tiles;
       const int ks = u / (args.n_tiles * args.m_tiles);
-      const int row = mt * 128 + trow;
+      const int row0 = mt * 128 + quad * 32;   // first row of this warp's slice
+      const int row = row0 + (int)lane;
       const int n0 = nt * BN;
       const bool rvalid = row < args.M;
-      wait_bounded(&tfull[grp], acc_phase);
+      if constexpr (EPI == EPI_DTANH) {
+        // first y_prev chunk of this tile (TMA; rows past M read as zero)
+        if (lane == 0) {
+          fence_proxy_async_smem();
+          mbar_expect_tx(&my_ybar[0], kStageTile);
+          tma_load_2d(ystage, &tmY, &my_ybar[0], n0, row0);
+        }
+      }
+      wait_bounded(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + grp * BN;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
 
       if constexpr (EPI == EPI_TANH) {
+        float nxt[32];
+        tmem_ld32(taddr, nxt);
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           float v[32];
-          tmem_ld32(taddr + c * 32, v);
           tc_wait_ld();
-          const int col0 = n0 + c * 32;
-          if (rvalid) {
-            const float4* b4 = reinterpret_cast<const float4*>(args.bias + col0);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float4 bb = __ldg(b4 + q);
-              v[4 * q + 0] = tanh_fast_accurate(v[4 * q + 0] + bb.x);
-              v[4 * q + 1] = tanh_fast_accurate(v[4 * q + 1] + bb.y);
-              v[4 * q + 2] = tanh_fast_accurate(v[4 * q + 2] + bb.z);
-              v[4 * q + 3] = tanh_fast_accurate(v[4 * q + 3] + bb.w);
-            }
-            store32_f16(args.out + (int64_t)row * args.ld_out + col0, v);
+          for (int j = 0; j < 32; ++j) v[j] = nxt[j];
+          if (c + 1 < BN / 32) tmem_ld32(taddr + (c + 1) * 32, nxt);   // overlap next TMEM read
+          const int col0 = n0 + c * 32;
+          const float4* b4 = reinterpret_cast<const float4*>(bias_s + col0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 bb = b4[q];
+            v[4 * q + 0] = tanh_fast_accurate(v[4 * q + 0] + bb.x);
+            v[4 * q + 1] = tanh_fast_accurate(v[4 * q + 1] + bb.y);
+            v[4 * q + 2] = tanh_fast_accurate(v[4 * q + 2] + bb.z);
+            v[4 * q + 3] = tanh_fast_accurate(v[4 * q + 3] + bb.w);
           }
+          uint8_t* t = ost.acquire();
+          stile_write_row(t, (int)lane, v);
+          ost.release(t, &tmO, col0, row0);      // rows >= M are clipped by TMA
         }
       } else if constexpr (EPI == EPI_DTANH) {
+        float nxt[32];
+        tmem_ld32(taddr, nxt);
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
-          float v[32];
-          tmem_ld32(taddr + c * 32, v);
-          tc_wait_ld();
-          const int col0 = n0 + c * 32;
-          if (rvalid) {
-            float y[32];
-            load32_f16(args.y_prev + (int64_t)row * args.ld_y + col0, y);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = sat_f16(v[j] * (1.f - y[j] * y[j]), nsat);
-            store32_f16(args.out + (int64_t)row * args.ld_out + col0, v);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          const int yb = c & 1;
+          if (c + 1 < BN / 32 && lane == 0) {      // prefetch the next y_prev chunk
+            fence_proxy_async_smem();
+            mbar_expect_tx(&my_ybar[yb ^ 1], kStageTile);
+            tma_load_2d(ystage + (yb ^ 1) * kStageTile, &tmY, &my_ybar[yb ^ 1], n0 + (c + 1) * 32, row0);
           }
+          float v[32];
+          tc_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = nxt[j];
+          if (c + 1 < BN / 32) tmem_ld32(taddr + (c + 1) * 32, nxt);
+          const int col0 = n0 + c * 32;
+          if (yb == 0) { wait_bounded(&my_ybar[0], yph0); yph0 ^= 1; }
+          else { wait_bounded(&my_ybar[1], yph1); yph1 ^= 1; }
+          float y[32];
+          stile_read_row(ystage + yb * kStageTile, (int)lane, y);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = sat_f16(v[j] * (1.f - y[j] * y[j]), nsat);  // rows >= M: 0
+          uint8_t* t = ost.acquire();
+          stile_write_row(t, (int)lane, v);
+          ost.release(t, &tmO, col0, row0);
           const float s = transpose_reduce32(v);
           my_colsum[col0 + lane] += s;
         }
@@ -420,40 +516,51 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
         }
       } else {  // EPI_LOSS
+        int act[kMaxHeads];
+        float Ahat = 0.f, lp = 0.f, R = 0.f;
+        if (rvalid) {   // per-row inputs: coalesced across lanes, issued before the TMEM wait
+          for (int h = 0; h < args.n_heads; ++h) act[h] = __ldg(args.actions + (int64_t)row * args.n_heads + h);
+          Ahat = __ldg(args.adv + row);
+          lp = __ldg(args.logp_old + row);
+          R = __ldg(args.ret + row);
+        }
         float z[64];
         tmem_ld32(taddr, z);
         tmem_ld32(taddr + 32, z + 32);
         tc_wait_ld();
         if (rvalid) {
 #pragma unroll
-          for (int j = 0; j < 64; ++j) z[j] += (j <= args.A) ? __ldg(args.bias + j) : 0.f;
-          int act[kMaxHeads];
-          for (int h = 0; h < args.n_heads; ++h) act[h] = __ldg(args.actions + (int64_t)row * args.n_heads + h);
-          float Ahat = __ldg(args.adv + row);
+          for (int j = 0; j < 64; ++j) z[j] += bias_s[j];
           if (args.mean_std) {
             const double mu = args.mean_std[0], sd = args.mean_std[1];
             Ahat = (float)(((double)Ahat - mu) / (sd + (double)args.adv_eps));
           }
-          ppo_row(args, z, act, Ahat, __ldg(args.logp_old + row), __ldg(args.ret + row), st,
-                  nonfinite);
+          ppo_row(args, z, act, Ahat, lp, R, st, nonfinite);
 #pragma unroll
           for (int j = 0; j < 64; ++j) z[j] = sat_f16(z[j], nsat);
-          store32_f16(args.out + (int64_t)row * args.ld_out, *reinterpret_cast<float(*)[32]>(z));
-          store32_f16(args.out + (int64_t)row * args.ld_out + 32, *reinterpret_cast<float(*)[32]>(z + 32));
         } else {
 #pragma unroll
           for (int j = 0; j < 64; ++j) z[j] = 0.f;
         }
-        const float s0 = transpose_reduce32(*reinterpret_cast<float(*)[32]>(z));
+        float (&z0)[32] = *reinterpret_cast<float(*)[32]>(z);
+        float (&z1)[32] = *reinterpret_cast<float(*)[32]>(z + 32);
+        uint8_t* t0 = ost.acquire();
+        stile_write_row(t0, (int)lane, z0);
+        ost.release(t0, &tmO, 0, row0);
+        uint8_t* t1 = ost.acquire();
+        stile_write_row(t1, (int)lane, z1);
+        ost.release(t1, &tmO, 32, row0);
+        const float s0 = transpose_reduce32(z0);
         my_colsum[lane] += s0;
-        const float s1 = transpose_reduce32(*reinterpret_cast<float(*)[32]>(z + 32));
+        const float s1 = transpose_reduce32(z1);
         my_colsum[32 + lane] += s1;
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[grp]);
-      acc_phase ^= 1;
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (EPI != EPI_PART && lane == 0) bulk_wait<0>();   // all TMA stores of this warp done
+    __syncwarp();
     // ---- per-CTA partials (deterministic: fixed unit set per CTA, fixed reduction order)
     if (args.counters) {
       count_warp(args.counters + 1, nsat);

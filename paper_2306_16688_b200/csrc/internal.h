@@ -36,11 +36,12 @@ cudaError_t launch_normalize(float* x, int64_t n, const double* mean_std, float 
 // ---- GEMM (mlp.cu)
 bool tmap_init();
 bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                  uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+                  uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle = 128);
 // D = A * B^T over the given shape; picks the instantiation (bn, a_mn, b_mn, epi).
+// to: epilogue output map (fp16, box 32x32, 64-byte swizzle); ty: y_prev map (DTANH).
 cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
-                        const CUtensorMap& tb, const GemmArgs& args, int grid, cudaStream_t s);
-size_t gemm_smem_bytes(int bn, int colsum_ld);
+                        const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& ty,
+                        const GemmArgs& args, int grid, cudaStream_t s);
 
 // ---- parameter segments (misc.cu): one weight matrix or bias vector of the flat layout
 struct Segment {

@@ -23,9 +23,10 @@ bool tmap_init() {
 }
 
 // fp16 row-major matrix with `outer` rows of `inner` elements, row pitch row_bytes;
-// box {box_inner, box_outer}, 128-byte swizzle, out-of-bounds elements read as zero.
+// box {box_inner, box_outer}, 128-byte (operands) or 64-byte (epilogue 32x32 tiles) swizzle;
+// out-of-bounds elements read as zero and are clipped on store.
 bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                  uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+                  uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle) {
   if (!tmap_init()) return false;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_bytes};
@@ -33,46 +34,41 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-size_t gemm_smem_bytes(int bn, int colsum_ld) {
-  switch (bn) {
-    case 64: return GemmCfg<64>::smem_bytes(colsum_ld);
-    case 128: return GemmCfg<128>::smem_bytes(colsum_ld);
-    default: return GemmCfg<256>::smem_bytes(colsum_ld);
-  }
-}
-
 template <int BN, bool AM, bool BM, int EPI>
-static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
-                              int grid, cudaStream_t s) {
+static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
+                              const CUtensorMap& ty, GemmArgs a, int grid, cudaStream_t s) {
   auto kern = gemm_tc_kernel<BN, AM, BM, EPI>;
-  const size_t smem = GemmCfg<BN>::smem_bytes(a.colsum_ld);
+  if (a.stages <= 0) a.stages = gemm_stages(BN, EPI, a.colsum_ld);
+  if (a.stages < 2) return cudaErrorInvalidConfiguration;
+  const size_t smem = 1024 + smem_layout(BN, EPI, a.stages, a.colsum_ld).total;
+  if (smem + 512 > kSmemLimit) return cudaErrorInvalidConfiguration;
   static size_t configured = 0;
   if (smem > configured) {
-    // attribute is set for the largest size ever requested (epilogue colsum area varies)
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(GemmCfg<BN>::smem_bytes(1024)));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = GemmCfg<BN>::smem_bytes(1024);
+    configured = smem;
   }
-  kern<<<grid, GemmCfg<BN>::THREADS, smem, s>>>(ta, tb, a);
+  kern<<<grid, kThreads, smem, s>>>(ta, tb, to, ty, a);
   return cudaGetLastError();
 }
 
-#define SRL_DISPATCH_BN(AM, BM, EPI)                                         \
-  switch (bn) {                                                              \
-    case 64: return launch_one<64, AM, BM, EPI>(ta, tb, args, grid, s);      \
-    case 128: return launch_one<128, AM, BM, EPI>(ta, tb, args, grid, s);    \
-    case 256: return launch_one<256, AM, BM, EPI>(ta, tb, args, grid, s);    \
-    default: return cudaErrorInvalidValue;                                   \
+#define SRL_DISPATCH_BN(AM, BM, EPI)                                                 \
+  switch (bn) {                                                                      \
+    case 64: return launch_one<64, AM, BM, EPI>(ta, tb, to, ty, args, grid, s);      \
+    case 128: return launch_one<128, AM, BM, EPI>(ta, tb, to, ty, args, grid, s);    \
+    case 256: return launch_one<256, AM, BM, EPI>(ta, tb, to, ty, args, grid, s);    \
+    default: return cudaErrorInvalidValue;                                           \
   }
 
 cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
-                        const CUtensorMap& tb, const GemmArgs& args, int grid, cudaStream_t s) {
+                        const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& ty,
+                        const GemmArgs& args, int grid, cudaStream_t s) {
   if (grid < 1) grid = 1;
   switch (epi) {
     case EPI_TANH:
@@ -82,7 +78,7 @@ cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap
       if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_DTANH) }
       break;
     case EPI_LOSS:
-      if (!a_mn && !b_mn && bn == 64) return launch_one<64, false, false, EPI_LOSS>(ta, tb, args, grid, s);
+      if (!a_mn && !b_mn && bn == 64) return launch_one<64, false, false, EPI_LOSS>(ta, tb, to, ty, args, grid, s);
       break;
     case EPI_PART:
       if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_PART) }

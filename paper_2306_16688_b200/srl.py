@@ -18,7 +18,7 @@ SRL_OK, SRL_EINVAL, SRL_ECUDA, SRL_ENCCL, SRL_ENOMEM, SRL_EUNSUPPORTED, SRL_ESTA
 # every symbol include/srl.h declares (checked by tests/test_abi.py)
 EXPORTS = ("srl_last_error", "srl_abi_version", "srl_gae", "srl_adv_norm", "srl_nccl_unique_id",
            "srl_ppo_create", "srl_ppo_destroy", "srl_ppo_params", "srl_ppo_adam_state",
-           "srl_ppo_load_params", "srl_ppo_step", "srl_allreduce_grads", "srl_prof_enable",
+           "srl_ppo_load_params", "srl_ppo_step", "srl_ppo_train_step", "srl_allreduce_grads", "srl_prof_enable",
            "srl_prof_reset", "srl_prof_count", "srl_prof_read", "srl_debug_gemm")
 
 
@@ -33,6 +33,7 @@ class PPOConfigC(C.Structure):
                 ("clip_eps", C.c_float), ("value_coef", C.c_float), ("entropy_coef", C.c_float),
                 ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
                 ("adam_eps", C.c_float), ("adv_eps", C.c_float),
+                ("gamma", C.c_float), ("gae_lambda", C.c_float), ("adv_unbiased", C.c_int),
                 ("max_local_n", C.c_int64), ("precision", C.c_int)]
 
 
@@ -70,6 +71,7 @@ def lib():
     L.srl_ppo_adam_state.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64)]
     L.srl_ppo_load_params.argtypes = [vp, vp, vp]
     L.srl_ppo_step.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
+    L.srl_ppo_train_step.argtypes = [vp, C.c_int, C.c_int, i64, vp, vp, vp, vp, vp, vp, vp, vp]
     L.srl_allreduce_grads.argtypes = [vp, vp, i64, C.c_int, vp]
     L.srl_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
                                  C.c_int, C.c_int, C.c_int, vp, vp]
@@ -171,11 +173,15 @@ class NetSpec:
     beta2: float = 0.999
     adam_eps: float = 1e-8
     adv_eps: float = 1e-8
+    gamma: float = 0.99
+    gae_lambda: float = 0.95
+    adv_unbiased: int = 0
 
     @classmethod
     def from_config(cls, cfg):
         return cls(cfg.obs_dim, tuple(cfg.hidden), tuple(cfg.heads), cfg.ld_obs, cfg.clip_eps,
-                   cfg.value_coef, cfg.entropy_coef, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps)
+                   cfg.value_coef, cfg.entropy_coef, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps,
+                   1e-8, cfg.gamma, cfg.lam, 0)
 
 
 class PPOContext:
@@ -192,6 +198,7 @@ class PPOContext:
         self.cfg = PPOConfigC(spec.obs_dim, ld, len(spec.hidden), self._hid, len(spec.heads),
                               self._heads, spec.clip_eps, spec.value_coef, spec.entropy_coef,
                               spec.lr, spec.beta1, spec.beta2, spec.adam_eps, spec.adv_eps,
+                              spec.gamma, spec.gae_lambda, int(spec.adv_unbiased),
                               int(max_local_n), 0)
         h = C.c_void_p()
         _check(lib().srl_ppo_create(C.byref(self.cfg), rank, world, nccl_id, self.device,
@@ -265,6 +272,17 @@ class PPOContext:
                                        C.byref(by)))
             out.append((nm.value.decode(), ms.value, fl.value, by.value))
         return out
+
+    def train_step(self, n_global, rewards, values, dones, obs, actions, logp_old, stats=None,
+                   stream=None):
+        """srl_ppo_train_step: GAE -> normalisation -> update in one call (device inputs)."""
+        T, B = rewards.shape
+        if stats is None:
+            stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
+        _check(lib().srl_ppo_train_step(self.handle, T, B, int(n_global), _ptr(rewards),
+                                        _ptr(values), _ptr(dones), _ptr(obs), _ptr(actions),
+                                        _ptr(logp_old), _ptr(stats), _stream(stream)))
+        return stats
 
     def allreduce_grads(self, buf: torch.Tensor, op: int = 0, stream=None):
         _cuda(buf, torch.float32, "buf")

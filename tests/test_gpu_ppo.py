@@ -130,3 +130,28 @@ def test_nonfinite_skips_adam():
     assert g["stats"]["nonfinite"] >= 1
     assert g["stats"]["step"] == 0
     assert np.array_equal(g["params"], params.astype(np.float64))
+
+
+@pytest.mark.parametrize("name", ["tiny", "gfootball"])
+def test_train_step_equals_composed_calls(name):
+    """srl_ppo_train_step (GAE -> norm -> update in one call) is bit-identical to the three
+    separate ABI calls, and its GAE / normalisation / gradient match the oracle."""
+    import paper_2306_16688_b200 as P
+    cfg = synth.get_config(name).with_(B=REDUCED[name] * synth.get_config(name).agents)
+    params, b = make_inputs(cfg, seed=21)
+    g = gpu_step(cfg, params, [b], apply=True)
+    ctx = P.PPOContext(P.NetSpec.from_config(cfg), max_local_n=b["n"])
+    ctx.load_params(torch.from_numpy(params).cuda())
+    d = {k: torch.from_numpy(np.ascontiguousarray(b[k])).cuda()
+         for k in ("rewards", "values", "dones", "obs", "actions", "logp_old")}
+    st = P.decode_stats(ctx.train_step(b["n"], d["rewards"], d["values"], d["dones"], d["obs"],
+                                       d["actions"], d["logp_old"]))
+    torch.cuda.synchronize()
+    p2 = ctx.params().cpu().numpy().astype(np.float64)
+    G2 = ctx.grads().cpu().numpy().astype(np.float64)
+    assert np.array_equal(p2, g["params"]) and np.array_equal(G2, g["bucket"])
+    assert st["step"] == 1
+    o = oracle.ppo_step(cfg, params, [b], apply=False)
+    _check_grads(cfg, G2[:cfg.n_params], o["grad"])
+    assert abs(st["adv_mean"] - o["mean"]) <= 1e-6 * o["std"]
+    assert abs(st["adv_std"] - o["std"]) <= 1e-6 * o["std"]
