@@ -188,10 +188,12 @@ srl_status srl_prof_read(srl_ctx* ctx, int i, const char** name, float* ms, doub
  * D[M][N] (device f32, dense) = sum_k A(m,k) * B(n,k) through the tcgen05 GEMM core with
  * its split-K epilogue (the dW path of a5).  A: a_mn == 0 -> fp16 [M][lda] (K contiguous),
  * a_mn == 1 -> fp16 [K][lda] (M contiguous); B likewise with N.  lda, ldb % 8 == 0.
- * bn in {64, 128, 256} is the N tile; splits >= 1 the K split count.  Used by tests only. */
+ * bn in {64, 128, 256} is the N tile; splits >= 1 the K split count; cg = 1 (one SM per
+ * 128-row tile) or 2 (CTA pair, tcgen05 cta_group::2, 256-row tiles; bn >= 128).
+ * Used by tests only. */
 srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int a_mn, int lda,
-                          const uint16_t* B, int b_mn, int ldb, int bn, int splits, float* D,
-                          srl_stream_t stream);
+                          const uint16_t* B, int b_mn, int ldb, int bn, int splits, int cg,
+                          float* D, srl_stream_t stream);
 
 #ifdef __cplusplus
 }

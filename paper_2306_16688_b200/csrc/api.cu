@@ -84,9 +84,9 @@ struct Lay {
   int64_t w_off, b_off;    // flat offsets
   __half* w16;
   int w16_ld, w16_rows;
-  int bn_fwd;              // N tile of the GEMM producing this layer's output (fwd)
-  int bn_dx;               // N tile of the dX GEMM that produces dZ of this layer's INPUT
-  int bn_dw, dw_n_tiles, dw_m_tiles, splits_max;
+  int bn_fwd, cg_fwd;      // N tile / CTA-group of the GEMM producing this layer's output
+  int bn_dx, cg_dx;        // same for the dX GEMM that produces dZ of this layer's INPUT
+  int bn_dw, cg_dw, dw_n_tiles, dw_m_tiles, splits_max;
   float* part;             // dW partials [splits][out or in][ld_part]
   int64_t part_rows, ld_part;
   float* colsum;           // db partials of this layer: [sms][4][out] (hidden) / [sms][4][64] (head)
@@ -316,15 +316,21 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
     Lay& y = c->lay[l];
     if ((st = dalloc(c, &y.w16, sizeof(__half) * (size_t)y.w16_rows * y.w16_ld))) return bail(st);
     // epilogue-heavy GEMMs (fwd tanh, dX dtanh) use 128-wide tiles: 4 TMEM accumulators
-    y.bn_fwd = (l == c->L) ? kHeadCols : (y.out % 128 == 0 ? 128 : 64);
-    y.bn_dx = (y.in % 128 == 0) ? 128 : 64;
+    // 256-wide outputs run on CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles): half the
+    // shared-memory operand traffic per FLOP of a 1-SM 128 x 128 tile
+    if (l == c->L) { y.bn_fwd = kHeadCols; y.cg_fwd = 1; }
+    else if (y.out % 256 == 0) { y.bn_fwd = 256; y.cg_fwd = 2; }
+    else { y.bn_fwd = (y.out % 128 == 0) ? 128 : 64; y.cg_fwd = 1; }
+    if (y.in % 256 == 0) { y.bn_dx = 256; y.cg_dx = 2; }
+    else { y.bn_dx = (y.in % 128 == 0) ? 128 : 64; y.cg_dx = 1; }
     // dW: hidden layer: D[out][in] = dZ^T X; head: D^T[in][64] = Y^T g
     const int dM = (l == c->L) ? y.in : y.out;
     const int dN = (l == c->L) ? kHeadCols : y.in;
     y.bn_dw = (l == c->L) ? kHeadCols : pick_bn(dN);
-    y.dw_m_tiles = (dM + 127) / 128;
+    y.cg_dw = (l < c->L && dM >= 256 && y.bn_dw >= 128) ? 2 : 1;
+    y.dw_m_tiles = (dM + 128 * y.cg_dw - 1) / (128 * y.cg_dw);
     y.dw_n_tiles = (dN + y.bn_dw - 1) / y.bn_dw;
-    y.splits_max = std::max(1, c->sms / (y.dw_m_tiles * y.dw_n_tiles));
+    y.splits_max = std::max(1, (c->sms / y.cg_dw) / (y.dw_m_tiles * y.dw_n_tiles));
     y.part_rows = dM;
     y.ld_part = (int64_t)y.dw_n_tiles * y.bn_dw;
     if ((st = dalloc(c, &y.part, sizeof(float) * y.splits_max * y.part_rows * y.ld_part))) return bail(st);
@@ -450,13 +456,13 @@ extern "C" srl_status srl_allreduce_grads(srl_ctx* c, float* buf, int64_t count,
 }
 
 // ------------------------------------------------------------------ a3..a7
-static srl_status gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
+static srl_status gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUtensorMap& ta,
                        const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& ty,
                        GemmArgs& g, int sms, cudaStream_t s, int* grid_out = nullptr) {
-  const int units = g.m_tiles * g.n_tiles * g.k_splits;
-  const int grid = std::min(units, sms);
+  const int units = g.m_tiles * g.n_tiles * g.k_splits;   // m_tiles of 128 * cg rows
+  const int grid = cg * std::min(units, sms / cg);
   if (grid_out) *grid_out = grid;
-  cudaError_t e = launch_gemm(bn, a_mn, b_mn, epi, ta, tb, to, ty, g, grid, s);
+  cudaError_t e = launch_gemm(bn, a_mn, b_mn, epi, cg, ta, tb, to, ty, g, grid, s);
   if (e != cudaSuccess) FAIL(SRL_ECUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   return SRL_OK;
 }
@@ -497,17 +503,17 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     const __half* X = l == 0 ? X0 : c->Y[l - 1];
     const int ldx = l == 0 ? ld_obs : y.in;
     TMC(ta, X, y.in, n, (uint64_t)ldx * 2, 64, 128);
-    TMC(tb, y.w16, y.in, y.out, (uint64_t)y.w16_ld * 2, 64, y.bn_fwd);
+    TMC(tb, y.w16, y.in, y.out, (uint64_t)y.w16_ld * 2, 64, y.bn_fwd / y.cg_fwd);
     CUtensorMap to;
     TMC(to, c->Y[l], y.out, n, (uint64_t)y.out * 2, 32, 32, 64);
     GemmArgs g{};
     g.M = n; g.N = y.out;
-    g.m_tiles = (n + 127) / 128; g.n_tiles = y.out / y.bn_fwd; g.k_splits = 1;
+    g.m_tiles = (n + 128 * y.cg_fwd - 1) / (128 * y.cg_fwd); g.n_tiles = y.out / y.bn_fwd; g.k_splits = 1;
     g.kb_total = (y.in + 63) / 64; g.kb_per_split = g.kb_total;
     g.bias = c->params + y.b_off;
     ProfScope ps(c, s, l == 0 ? "fwd_l1" : "fwd_hidden", 2.0 * n * y.in * y.out,
                  2.0 * n * (y.in + y.out) + 2.0 * y.in * y.out + 4.0 * y.out);
-    if (srl_status st = gemm(y.bn_fwd, false, false, EPI_TANH, ta, tb, to, to, g, sms, s)) return st;
+    if (srl_status st = gemm(y.bn_fwd, false, false, EPI_TANH, y.cg_fwd, ta, tb, to, to, g, sms, s)) return st;
   }
   // ---------------- a4: head GEMM + fused PPO loss -> per-sample dlogits G16
   const Lay& hd = c->lay[L];
@@ -533,7 +539,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     g.entropy_coef = c->cfg.entropy_coef; g.adv_eps = c->cfg.adv_eps;
     ProfScope ps(c, s, "head_loss", 2.0 * n * hd.in * hd.out,
                  2.0 * n * hd.in + 2.0 * n * kHeadCols + (16.0 + 4.0 * g.n_heads) * n);
-    if (srl_status st = gemm(64, false, false, EPI_LOSS, ta, tb, to, to, g, sms, s, &grid_loss)) return st;
+    if (srl_status st = gemm(64, false, false, EPI_LOSS, 1, ta, tb, to, to, g, sms, s, &grid_loss)) return st;
   }
   // ---------------- a5: backward.  dW via split-K partials, dX with fused dtanh + db sums
   std::vector<int> splits(L + 1, 1), colsum_parts(L + 1, 0);
@@ -558,7 +564,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     const int realN = (l == L) ? y.out : dN;
     ProfScope ps(c, s, l == L ? "dW_head" : (l == 0 ? "dW_l1" : "dW_hidden"),
                  2.0 * n * dM * realN, 2.0 * n * (dM + dN) + 4.0 * S * dM * y.ld_part);
-    return gemm(y.bn_dw, true, true, EPI_PART, ta, tb, ta, ta, g, sms, s);
+    return gemm(y.bn_dw, true, true, EPI_PART, y.cg_dw, ta, tb, ta, ta, g, sms, s);
   };
   auto dX = [&](int l, const __half* dz_in, int k_width, __half* dz_out) -> srl_status {
     // dZ_{in of layer l} = (dZ_out_l W_l) * (1 - Y_{l-1}^2), colsum -> db of layer l-1
@@ -572,7 +578,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     TMC(ty, c->Y[l - 1], y.in, n, (uint64_t)y.in * 2, 32, 32, 64);
     GemmArgs g{};
     g.M = n; g.N = y.in;
-    g.m_tiles = (n + 127) / 128; g.n_tiles = y.in / y.bn_dx; g.k_splits = 1;
+    g.m_tiles = (n + 128 * y.cg_dx - 1) / (128 * y.cg_dx); g.n_tiles = y.in / y.bn_dx; g.k_splits = 1;
     g.kb_total = (k_width + 63) / 64; g.kb_per_split = g.kb_total;
     g.colsum = yp.colsum; g.colsum_ld = yp.colsum_ld;
     g.counters = c->counters;
@@ -580,7 +586,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     const int realK = (l == L) ? y.out : k_width;
     ProfScope ps(c, s, l == L ? "dX_head" : "dX_hidden", 2.0 * n * realK * y.in,
                  2.0 * n * (k_width + 2.0 * y.in) + 2.0 * y.in * k_width);
-    srl_status st = gemm(y.bn_dx, false, true, EPI_DTANH, ta, tb, to, ty, g, sms, s, &grid);
+    srl_status st = gemm(y.bn_dx, false, true, EPI_DTANH, y.cg_dx, ta, tb, to, ty, g, sms, s, &grid);
     colsum_parts[l - 1] = grid;
     return st;
   };
@@ -702,20 +708,22 @@ __global__ void sum_parts_kernel(const float* part, int S, int64_t split_stride,
 
 extern "C" srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int a_mn, int lda,
                                      const uint16_t* B, int b_mn, int ldb, int bn, int splits,
-                                     float* D, srl_stream_t stream) {
+                                     int cg, float* D, srl_stream_t stream) {
   if (M < 1 || N < 1 || K < 1 || !A || !B || !D || lda % 8 || ldb % 8 || splits < 1)
     FAIL(SRL_EINVAL, "srl_debug_gemm: bad args");
   if (bn != 64 && bn != 128 && bn != 256) FAIL(SRL_EINVAL, "srl_debug_gemm: bn");
+  if (cg != 1 && cg != 2) FAIL(SRL_EINVAL, "srl_debug_gemm: cg");
+  if (cg == 2 && bn == 64) FAIL(SRL_EINVAL, "srl_debug_gemm: cg = 2 needs bn >= 128");
   if (srl_status st = require_device()) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CUtensorMap ta, tb;
   if (!a_mn) TM(ta, A, K, M, (uint64_t)lda * 2, 64, 128);
   else TM(ta, A, M, K, (uint64_t)lda * 2, 64, 64);
-  if (!b_mn) TM(tb, B, K, N, (uint64_t)ldb * 2, 64, bn);
+  if (!b_mn) TM(tb, B, K, N, (uint64_t)ldb * 2, 64, bn / cg);
   else TM(tb, B, N, K, (uint64_t)ldb * 2, 64, 64);
   GemmArgs g{};
   g.M = M; g.N = N;
-  g.m_tiles = (M + 127) / 128; g.n_tiles = (N + bn - 1) / bn;
+  g.m_tiles = (M + 128 * cg - 1) / (128 * cg); g.n_tiles = (N + bn - 1) / bn;
   g.kb_total = (K + 63) / 64;
   int S = std::min(splits, g.kb_total);
   g.kb_per_split = (g.kb_total + S - 1) / S;
@@ -726,7 +734,7 @@ extern "C" srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int
   float* part = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * S * g.part_split_stride, s));
   g.part = part;
-  if (srl_status st = gemm(bn, a_mn != 0, b_mn != 0, EPI_PART, ta, tb, ta, ta, g, num_sms(), s)) return st;
+  if (srl_status st = gemm(bn, a_mn != 0, b_mn != 0, EPI_PART, cg, ta, tb, ta, ta, g, num_sms(), s)) return st;
   sum_parts_kernel<<<256, 256, 0, s>>>(part, S, g.part_split_stride, M, N, g.ld_part, D);
   CK(cudaGetLastError());
   CK(cudaFreeAsync(part, s));

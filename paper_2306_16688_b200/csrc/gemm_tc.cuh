@@ -64,9 +64,10 @@ constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kBarBytes = 512;
 constexpr uint32_t kSmemLimit = 232448;           // 227 KB per CTA
 
-__host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, int colsum_ld) {
+__host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, int colsum_ld,
+                                                  int cg = 1) {
   SmemLayout L;
-  const uint32_t stage_bytes = (uint32_t)(128 + bn) * 64 * 2;
+  const uint32_t stage_bytes = (uint32_t)(128 + bn / cg) * 64 * 2;
   L.ring = 0;
   L.ostage = stages * stage_bytes;
   const uint32_t ost = (epi == EPI_PART) ? 0 : kEpiWarps * 2 * kStageTile;
@@ -83,20 +84,24 @@ __host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, i
 
 // largest ring (<= 8 slots) that fits next to the epilogue buffers; 1 KB alignment slack and
 // 512 B for the kernel's static shared memory
-inline int gemm_stages(int bn, int epi, int colsum_ld) {
-  const uint32_t stage_bytes = (uint32_t)(128 + bn) * 64 * 2;
-  const SmemLayout z = smem_layout(bn, epi, 0, colsum_ld);
+inline int gemm_stages(int bn, int epi, int colsum_ld, int cg = 1) {
+  const uint32_t stage_bytes = (uint32_t)(128 + bn / cg) * 64 * 2;
+  const SmemLayout z = smem_layout(bn, epi, 0, colsum_ld, cg);
   const int64_t avail = (int64_t)kSmemLimit - 1024 - 512 - z.total;
   const int st = (int)(avail / stage_bytes);
   return st > 8 ? 8 : st;
 }
 
-template <int BN>
+// CG = 1: one CTA computes a 128 x BN tile.  CG = 2: a CTA pair (cluster of 2) computes a
+// 256 x BN tile with tcgen05.mma.cta_group::2 issued by the leader: each CTA holds its 128
+// rows of A and half of B (BN/2 columns) in smem, and its 128 rows of D in its own TMEM.
+template <int BN, int CG = 1>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TX_BYTES = CG * STAGE_BYTES;   // bytes the leader's full barrier expects
   static constexpr int ACC_STAGES = 512 / BN;     // TMEM accumulators: 2 / 4 / 8
   static constexpr int TMEM_COLS = 512;
 };
@@ -286,15 +291,19 @@ struct OutStage {
 };
 
 // ---------------------------------------------------------------------------------------
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmY,
                const GemmArgs args) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   static_assert(EPI != EPI_LOSS || BN == kHeadCols, "loss epilogue works on the 64-col head");
+  static_assert(CG == 1 || (BN / CG) % 64 == 0 || !B_MN, "MN-major B halves must be 64-wide");
   const int STAGES = args.stages;
-  const SmemLayout SL = smem_layout(BN, EPI, STAGES, args.colsum_ld);
+  const SmemLayout SL = smem_layout(BN, EPI, STAGES, args.colsum_ld, CG);
+  const int rank = (CG == 2) ? (int)cluster_ctarank() : 0;   // CTA rank in the pair
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;      // pair (cluster) index / count
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -320,14 +329,15 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int s = 0; s < Cfg::ACC_STAGES; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], 4 * CG);     // every epilogue warp of the group, in both CTAs
     }
     for (int s = 0; s < 16; ++s) mbar_init(&ybar[s], 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 2) tmem_alloc_cg<CG>(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();   // peer barriers initialised before remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -336,42 +346,47 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      auto load = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+        if constexpr (CG == 1) tma_load_2d(dst, m, bar, c0, c1);
+        else tma_load_2d_cg2(dst, m, bar, c0, c1);   // bytes counted on the leader's barrier
+      };
+      for (int u = cid; u < units; u += ncl) {
         const int nt = u % args.n_tiles;
         const int mt = (u / args.n_tiles) % args.m_tiles;
         const int ks = u / (args.n_tiles * args.m_tiles);
         const int kb0 = ks * args.kb_per_split;
         const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
-        const int m0 = mt * 128, n0 = nt * BN;
+        const int m0 = mt * 128 * CG + rank * 128;           // this CTA's A rows
+        const int n0 = nt * BN + rank * (BN / CG);           // this CTA's B columns
         for (int kb = kb0; kb < kb1; ++kb) {
           wait_bounded(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          if (leader) mbar_expect_tx(&full[stage], Cfg::TX_BYTES);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
           const int k0 = kb * 64;
           if (!A_MN) {
-            tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+            load(sa, &tmA, &full[stage], k0, m0);
           } else {
-            tma_load_2d(sa, &tmA, &full[stage], m0, k0);
-            tma_load_2d(sa + 8192, &tmA, &full[stage], m0 + 64, k0);
+            load(sa, &tmA, &full[stage], m0, k0);
+            load(sa + 8192, &tmA, &full[stage], m0 + 64, k0);
           }
           if (!B_MN) {
-            tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            load(sb, &tmB, &full[stage], k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / CG / 64; ++j) load(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    // ============================ MMA issuer
-    constexpr uint32_t IDESC = umma_idesc_f16(128, BN, A_MN, B_MN);
+  } else if (warp == 1 && leader) {
+    // ============================ MMA issuer (the pair's leader CTA only)
+    constexpr uint32_t IDESC = umma_idesc_f16(128 * CG, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    for (int u = cid; u < units; u += ncl, ++it) {
       const int ks = u / (args.n_tiles * args.m_tiles);
       const int kb0 = ks * args.kb_per_split;
       const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
@@ -392,14 +407,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                      : umma_desc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
                                      : umma_desc_sw128(b_base + k * 32, 16, 1024);
-            tc_mma_f16(d_tmem, ad, bd, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+            tc_mma_f16_cg<CG>(d_tmem, ad, bd, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);
+          tc_commit_cg<CG>(&empty[stage]);      // frees the slot in both CTAs
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) tc_commit(&tfull[acc]);
+      if (lane == 0) tc_commit_cg<CG>(&tfull[acc]);   // both CTAs' epilogues
       __syncwarp();
     }
   } else if (warp >= 4) {
@@ -424,14 +439,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint32_t nsat = 0, nonfinite = 0;
     double st[5] = {0, 0, 0, 0, 0};
     int it = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    for (int u = cid; u < units; u += ncl, ++it) {
       if ((it & 1) != grp) continue;
       const int acc = it % Cfg::ACC_STAGES;
       const uint32_t acc_phase = (uint32_t)(it / Cfg::ACC_STAGES) & 1u;
       const int nt = u % args.n_tiles;
       const int mt = (u / args.n_tiles) % args.m_tiles;
       const int ks = u / (args.n_tiles * args.m_tiles);
-      const int row0 = mt * 128 + quad * 32;   // first row of this warp's slice
+      const int row0 = mt * 128 * CG + rank * 128 + quad * 32;   // first row of this warp's slice
       const int row = row0 + (int)lane;
       const int n0 = nt * BN;
       const bool rvalid = row < args.M;
@@ -557,7 +572,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_leader(&tempty[acc]);   // the leader's MMA waits on it
+      }
     }
     if (EPI != EPI_PART && lane == 0) bulk_wait<0>();   // all TMA stores of this warp done
     __syncwarp();
@@ -594,9 +612,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();   // no CTA leaves while its peer may still signal it
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    tmem_dealloc_cg<CG>(tmem_base, Cfg::TMEM_COLS);
   }
 }
 

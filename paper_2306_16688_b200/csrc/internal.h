@@ -39,7 +39,8 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
                   uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle = 128);
 // D = A * B^T over the given shape; picks the instantiation (bn, a_mn, b_mn, epi).
 // to: epilogue output map (fp16, box 32x32, 64-byte swizzle); ty: y_prev map (DTANH).
-cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
+// cg = 2: CTA pairs (cluster 2x1) with tcgen05 cta_group::2, 256-row tiles; grid even.
+cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUtensorMap& ta,
                         const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& ty,
                         const GemmArgs& args, int grid, cudaStream_t s);
 

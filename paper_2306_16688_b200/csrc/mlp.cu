@@ -40,13 +40,13 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool AM, bool BM, int EPI>
+template <int BN, bool AM, bool BM, int EPI, int CG>
 static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                               const CUtensorMap& ty, GemmArgs a, int grid, cudaStream_t s) {
-  auto kern = gemm_tc_kernel<BN, AM, BM, EPI>;
-  if (a.stages <= 0) a.stages = gemm_stages(BN, EPI, a.colsum_ld);
+  auto kern = gemm_tc_kernel<BN, AM, BM, EPI, CG>;
+  if (a.stages <= 0) a.stages = gemm_stages(BN, EPI, a.colsum_ld, CG);
   if (a.stages < 2) return cudaErrorInvalidConfiguration;
-  const size_t smem = 1024 + smem_layout(BN, EPI, a.stages, a.colsum_ld).total;
+  const size_t smem = 1024 + smem_layout(BN, EPI, a.stages, a.colsum_ld, CG).total;
   if (smem + 512 > kSmemLimit) return cudaErrorInvalidConfiguration;
   static size_t configured = 0;
   if (smem > configured) {
@@ -54,37 +54,59 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  kern<<<grid, kThreads, smem, s>>>(ta, tb, to, ty, a);
+  if constexpr (CG == 1) {
+    kern<<<grid, kThreads, smem, s>>>(ta, tb, to, ty, a);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, to, ty, a);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
-#define SRL_DISPATCH_BN(AM, BM, EPI)                                                 \
-  switch (bn) {                                                                      \
-    case 64: return launch_one<64, AM, BM, EPI>(ta, tb, to, ty, args, grid, s);      \
-    case 128: return launch_one<128, AM, BM, EPI>(ta, tb, to, ty, args, grid, s);    \
-    case 256: return launch_one<256, AM, BM, EPI>(ta, tb, to, ty, args, grid, s);    \
-    default: return cudaErrorInvalidValue;                                           \
+#define SRL_DISPATCH_BN(AM, BM, EPI, CG)                                                 \
+  switch (bn) {                                                                          \
+    case 64: return launch_one<64, AM, BM, EPI, 1>(ta, tb, to, ty, args, grid, s);       \
+    case 128: return CG == 2 ? launch_one<128, AM, BM, EPI, 2>(ta, tb, to, ty, args, grid, s) \
+                             : launch_one<128, AM, BM, EPI, 1>(ta, tb, to, ty, args, grid, s); \
+    case 256: return CG == 2 ? launch_one<256, AM, BM, EPI, 2>(ta, tb, to, ty, args, grid, s) \
+                             : launch_one<256, AM, BM, EPI, 1>(ta, tb, to, ty, args, grid, s); \
+    default: return cudaErrorInvalidValue;                                               \
   }
 
-cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, const CUtensorMap& ta,
+cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUtensorMap& ta,
                         const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& ty,
                         const GemmArgs& args, int grid, cudaStream_t s) {
   if (grid < 1) grid = 1;
+  if (cg != 1 && cg != 2) return cudaErrorInvalidValue;
+  if (cg == 2 && (grid & 1)) return cudaErrorInvalidConfiguration;
   switch (epi) {
     case EPI_TANH:
-      if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_TANH) }
+      if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_TANH, cg) }
       break;
     case EPI_DTANH:
-      if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_DTANH) }
+      if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_DTANH, cg) }
       break;
     case EPI_LOSS:
-      if (!a_mn && !b_mn && bn == 64) return launch_one<64, false, false, EPI_LOSS>(ta, tb, to, ty, args, grid, s);
+      if (!a_mn && !b_mn && bn == 64 && cg == 1)
+        return launch_one<64, false, false, EPI_LOSS, 1>(ta, tb, to, ty, args, grid, s);
       break;
     case EPI_PART:
-      if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_PART) }
-      if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_PART) }
-      if (a_mn && !b_mn) { SRL_DISPATCH_BN(true, false, EPI_PART) }
-      if (a_mn && b_mn) { SRL_DISPATCH_BN(true, true, EPI_PART) }
+      if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_PART, cg) }
+      if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_PART, cg) }
+      if (a_mn && !b_mn) { SRL_DISPATCH_BN(true, false, EPI_PART, cg) }
+      if (a_mn && b_mn) { SRL_DISPATCH_BN(true, true, EPI_PART, cg) }
       break;
   }
   return cudaErrorInvalidValue;

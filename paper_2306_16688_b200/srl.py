@@ -74,7 +74,7 @@ def lib():
     L.srl_ppo_train_step.argtypes = [vp, C.c_int, C.c_int, i64, vp, vp, vp, vp, vp, vp, vp, vp]
     L.srl_allreduce_grads.argtypes = [vp, vp, i64, C.c_int, vp]
     L.srl_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
-                                 C.c_int, C.c_int, C.c_int, vp, vp]
+                                 C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
     L.srl_prof_enable.argtypes = [vp, C.c_int]
     L.srl_prof_reset.argtypes = [vp]
     L.srl_prof_count.argtypes = [vp]
@@ -296,9 +296,9 @@ def decode_stats(stats_u8: torch.Tensor) -> dict:
     return {k: getattr(s, k) for k in STATS_FIELDS}
 
 
-def debug_gemm(A, a_mn, B, b_mn, M, N, K, bn=128, splits=1, stream=None):
+def debug_gemm(A, a_mn, B, b_mn, M, N, K, bn=128, splits=1, cg=1, stream=None):
     """Test hook: D[M][N] = sum_k A(m,k) B(n,k) through the tcgen05 GEMM (EPI_PART path)."""
     D = torch.empty(M, N, dtype=torch.float32, device=A.device)
     _check(lib().srl_debug_gemm(M, N, K, _ptr(A), int(a_mn), A.shape[1], _ptr(B), int(b_mn),
-                                B.shape[1], bn, splits, _ptr(D), _stream(stream)))
+                                B.shape[1], bn, splits, cg, _ptr(D), _stream(stream)))
     return D

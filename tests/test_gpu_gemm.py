@@ -13,22 +13,31 @@ def _ref(A, a_mn, B, b_mn):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M,N,K,bn,splits", [
-    (128, 128, 64, 128, 1),
-    (256, 256, 512, 256, 1),
-    (200, 192, 136, 64, 1),      # ragged M and K tails, N tile 64
-    (384, 512, 1000, 128, 3),    # split-K with a ragged last split
-    (64, 64, 4096, 64, 8),
+@pytest.mark.parametrize("M,N,K,bn,splits,cg", [
+    (128, 128, 64, 128, 1, 1),
+    (256, 256, 512, 256, 1, 1),
+    (200, 192, 136, 64, 1, 1),      # ragged M and K tails, N tile 64
+    (384, 512, 1000, 128, 3, 1),    # split-K with a ragged last split
+    (64, 64, 4096, 64, 8, 1),
+    (256, 256, 512, 256, 1, 2),     # CTA pair (tcgen05 cta_group::2), one 256x256 tile
+    (640, 512, 520, 256, 1, 2),     # CTA pairs, ragged M (2.5 pair tiles) and K
+    (512, 384, 2048, 128, 5, 2),    # CTA pairs, BN 128 (64-col halves), split-K
+    (100, 256, 64, 256, 1, 2),      # a single partial pair tile (peer rows all out of bounds)
 ])
-def test_gemm_majors(a_mn, b_mn, M, N, K, bn, splits):
+def test_gemm_majors(a_mn, b_mn, M, N, K, bn, splits, cg):
     import paper_2306_16688_b200 as P
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
     A = torch.randn((K, M) if a_mn else (M, K), generator=g, device="cuda").half()
     B = torch.randn((K, N) if b_mn else (N, K), generator=g, device="cuda").half()
-    if A.shape[1] % 8:
-        A = torch.nn.functional.pad(A, (0, 8 - A.shape[1] % 8))[:, :A.shape[1]].contiguous()
-    D = P.debug_gemm(A, a_mn, B, b_mn, M, N, K, bn=bn, splits=splits)
     ref = _ref(A, a_mn, B, b_mn)
+
+    def padded(X):       # rows stored with a 16-byte-multiple stride (TMA rule), pad = garbage
+        w = (X.shape[1] + 7) // 8 * 8
+        Y = torch.full((X.shape[0], w), 3.0, device="cuda").half()
+        Y[:, :X.shape[1]] = X
+        return Y
+
+    D = P.debug_gemm(padded(A), a_mn, padded(B), b_mn, M, N, K, bn=bn, splits=splits, cg=cg)
     torch.cuda.synchronize()
     err = (D - ref).abs().max().item()
     assert err <= 1e-3 * ref.abs().max().item() + 1e-4, err
