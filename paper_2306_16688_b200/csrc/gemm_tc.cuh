@@ -56,8 +56,9 @@ struct GemmArgs {
 // Shared-memory layout (identical on host and device):
 //   [operand ring][out staging 32 KB][y staging 32 KB (DTANH)][colsum 8 x ld][bias 4 KB][bars]
 struct SmemLayout {
-  uint32_t ring, ostage, ystage, colsum, bias, bars, total;
+  uint32_t ring, ostage, ystage, colsum, bias, zbuf, bars, total;
 };
+constexpr int kZPitch = 33;                       // loss row buffer [64 cols][33] per warp
 constexpr int kStageTile = 32 * 32 * 2;           // one 32x32 fp16 staging tile
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
@@ -77,7 +78,9 @@ __host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, i
   const uint32_t cs = (epi == EPI_DTANH || epi == EPI_LOSS) ? kEpiWarps * colsum_ld * 4 : 0;
   L.bias = L.colsum + cs;
   const uint32_t bs = (epi == EPI_TANH || epi == EPI_LOSS) ? 4096 : 0;
-  L.bars = L.bias + bs;
+  L.zbuf = L.bias + bs;
+  const uint32_t zs = (epi == EPI_LOSS) ? kEpiWarps * 64 * kZPitch * 4 : 0;
+  L.bars = L.zbuf + zs;
   L.total = L.bars + kBarBytes;
   return L;
 }
@@ -189,75 +192,67 @@ __device__ __forceinline__ void count_warp(unsigned long long* ctr, uint32_t n) 
 }
 
 // ---------------------------------------------------------------------------------------
-// a4: PPO loss on one row held in registers (z: 64 logits incl. bias in, dloss_i/dz out).
+// a4: PPO loss for the warp's 32 rows.  zb[j * kZPitch + lane] holds logit j (bias added) of
+// row `lane`; on return it holds dloss_i/dz_j (j <= A), the per-sample logit gradient.
+// Compact runtime loops over the A+1 real columns only (no 64-wide unrolling).
 // Formulas: DESIGN.md §3.1 (SURVEY C-4).
-__device__ __forceinline__ void ppo_row(const GemmArgs& a, float (&z)[64], const int* act,
-                                        float Ahat, float lp_old, float R, double (&st)[5],
-                                        uint32_t& nonfinite) {
+__device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, const int* act,
+                                              float Ahat, float lp_old, float R, bool rvalid,
+                                              double (&st)[5], uint32_t& nonfinite) {
+  const uint32_t lane = lane_id();
+  float* z = zb + lane;                       // z[j * kZPitch]: this row's column j
   float logpi = 0.f, ent = 0.f;
   float Hh[kMaxHeads];
   int off = 0;
+#pragma unroll 1
   for (int h = 0; h < a.n_heads; ++h) {
     const int sz = a.head_size[h];
-    const int ah = off + act[h];
     float mx = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 64; ++j)
-      if (j >= off && j < off + sz) mx = fmaxf(mx, z[j]);
+#pragma unroll 4
+    for (int j = off; j < off + sz; ++j) mx = fmaxf(mx, z[j * kZPitch]);
     float se = 0.f;
-#pragma unroll
-    for (int j = 0; j < 64; ++j)
-      if (j >= off && j < off + sz) se += __expf(z[j] - mx);
+#pragma unroll 4
+    for (int j = off; j < off + sz; ++j) se += __expf(z[j * kZPitch] - mx);
     const float lse = mx + __logf(se);
-    float hh = 0.f, la = 0.f;
-#pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      if (j >= off && j < off + sz) {
-        const float l = z[j] - lse;        // log-softmax, kept in z
-        z[j] = l;
-        hh -= __expf(l) * l;
-        if (j == ah) la = l;
-      }
+    float hh = 0.f;
+#pragma unroll 4
+    for (int j = off; j < off + sz; ++j) {
+      const float l = z[j * kZPitch] - lse;    // log-softmax, kept in place
+      z[j * kZPitch] = l;
+      hh -= __expf(l) * l;
     }
     Hh[h] = hh;
     ent += hh;
-    logpi += la;
+    logpi += z[(off + act[h]) * kZPitch];
     off += sz;
   }
   const float rho = expf(logpi - lp_old);
   const float lo = 1.f - a.clip_eps, hi = 1.f + a.clip_eps;
   const float rc = fminf(fmaxf(rho, lo), hi);
   const float lpg = -fminf(rho * Ahat, rc * Ahat);
-  float V = 0.f;
-#pragma unroll
-  for (int j = 0; j < 64; ++j)
-    if (j == a.A) V = z[j];   // unrolled select keeps z in registers
-  const float dv = V - R;
+  const float dv = z[a.A * kZPitch] - R;
   const float lv = dv * dv;
   const float mask = (Ahat >= 0.f) ? (rho <= hi ? 1.f : 0.f) : (rho >= lo ? 1.f : 0.f);
-  const float pol = -mask * Ahat * rho;   // coefficient of (onehot - p)
+  const float pol = -mask * Ahat * rho;      // coefficient of (onehot - p)
   const float li = lpg + a.value_coef * lv - a.entropy_coef * ent;
-  const bool ok = isfinite(li);
+  const bool ok = rvalid && isfinite(li);
   off = 0;
+#pragma unroll 1
   for (int h = 0; h < a.n_heads; ++h) {
     const int sz = a.head_size[h];
     const int ah = off + act[h];
     const float H = Hh[h];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      if (j >= off && j < off + sz) {
-        const float l = z[j];
-        const float p = __expf(l);
-        z[j] = pol * ((j == ah ? 1.f : 0.f) - p) + a.entropy_coef * p * (l + H);
-      }
+#pragma unroll 4
+    for (int j = off; j < off + sz; ++j) {
+      const float l = z[j * kZPitch];
+      const float p = __expf(l);
+      const float g = pol * ((j == ah ? 1.f : 0.f) - p) + a.entropy_coef * p * (l + H);
+      z[j * kZPitch] = ok ? g : 0.f;
     }
     off += sz;
   }
-#pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    if (j == a.A) z[j] = 2.f * a.value_coef * dv;
-    else if (j > a.A || !ok) z[j] = 0.f;
-  }
+  z[a.A * kZPitch] = ok ? 2.f * a.value_coef * dv : 0.f;
+  if (!rvalid) return;
   if (!ok) {
     ++nonfinite;
     return;
@@ -477,10 +472,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 bb = b4[q];
-            v[4 * q + 0] = tanh_fast_accurate(v[4 * q + 0] + bb.x);
-            v[4 * q + 1] = tanh_fast_accurate(v[4 * q + 1] + bb.y);
-            v[4 * q + 2] = tanh_fast_accurate(v[4 * q + 2] + bb.z);
-            v[4 * q + 3] = tanh_fast_accurate(v[4 * q + 3] + bb.w);
+            v[4 * q + 0] = tanh_mufu(v[4 * q + 0] + bb.x);
+            v[4 * q + 1] = tanh_mufu(v[4 * q + 1] + bb.y);
+            v[4 * q + 2] = tanh_mufu(v[4 * q + 2] + bb.z);
+            v[4 * q + 3] = tanh_mufu(v[4 * q + 3] + bb.w);
           }
           uint8_t* t = ost.acquire();
           stile_write_row(t, (int)lane, v);
@@ -508,8 +503,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           float y[32];
           stile_read_row(ystage + yb * kStageTile, (int)lane, y);
           __syncwarp();
+          float mx = 0.f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = sat_f16(v[j] * (1.f - y[j] * y[j]), nsat);  // rows >= M: 0
+          for (int j = 0; j < 32; ++j) {
+            v[j] *= fmaf(-y[j], y[j], 1.f);      // rows >= M: acc = 0, y = 0 -> 0
+            mx = fmaxf(mx, fabsf(v[j]));
+          }
+          if (mx > 65504.f) {                    // rare: clamp to the fp16 range and count
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = sat_f16(v[j], nsat);
+          }
           uint8_t* t = ost.acquire();
           stile_write_row(t, (int)lane, v);
           ost.release(t, &tmO, col0, row0);
@@ -533,42 +536,50 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       } else {  // EPI_LOSS
         int act[kMaxHeads];
         float Ahat = 0.f, lp = 0.f, R = 0.f;
+        for (int h = 0; h < args.n_heads; ++h) act[h] = 0;
         if (rvalid) {   // per-row inputs: coalesced across lanes, issued before the TMEM wait
           for (int h = 0; h < args.n_heads; ++h) act[h] = __ldg(args.actions + (int64_t)row * args.n_heads + h);
           Ahat = __ldg(args.adv + row);
           lp = __ldg(args.logp_old + row);
           R = __ldg(args.ret + row);
         }
-        float z[64];
-        tmem_ld32(taddr, z);
-        tmem_ld32(taddr + 32, z + 32);
-        tc_wait_ld();
-        if (rvalid) {
+        float* zb = reinterpret_cast<float*>(smem + SL.zbuf) + ew * 64 * kZPitch;
+        {
+          float z[64];
+          tmem_ld32(taddr, z);
+          tmem_ld32(taddr + 32, z + 32);
+          tc_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 64; ++j) z[j] += bias_s[j];
-          if (args.mean_std) {
-            const double mu = args.mean_std[0], sd = args.mean_std[1];
-            Ahat = (float)(((double)Ahat - mu) / (sd + (double)args.adv_eps));
-          }
-          ppo_row(args, z, act, Ahat, lp, R, st, nonfinite);
-#pragma unroll
-          for (int j = 0; j < 64; ++j) z[j] = sat_f16(z[j], nsat);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) z[j] = 0.f;
+          for (int j = 0; j < 64; ++j)
+            if (j <= args.A) zb[j * kZPitch + lane] = z[j] + bias_s[j];
         }
-        float (&z0)[32] = *reinterpret_cast<float(*)[32]>(z);
-        float (&z1)[32] = *reinterpret_cast<float(*)[32]>(z + 32);
+        if (args.mean_std) {
+          const double mu = args.mean_std[0], sd = args.mean_std[1];
+          Ahat = (float)(((double)Ahat - mu) / (sd + (double)args.adv_eps));
+        }
+        ppo_rows_smem(args, zb, act, Ahat, lp, R, rvalid, st, nonfinite);
+        __syncwarp();
+        // per-CTA bias-gradient partials: lane j sums column j over the warp's 32 rows
+        for (int j = lane; j <= args.A; j += 32) {
+          float cs = 0.f;
+#pragma unroll 8
+          for (int r = 0; r < 32; ++r) cs += zb[j * kZPitch + r];
+          my_colsum[j] += cs;
+        }
+        // this row's 64 fp16 outputs (zero pad past A), saturated, through TMA stores
+        float z0[32], z1[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          z0[j] = (j <= args.A) ? sat_f16(zb[j * kZPitch + lane], nsat) : 0.f;
+          z1[j] = (j + 32 <= args.A) ? sat_f16(zb[(j + 32) * kZPitch + lane], nsat) : 0.f;
+        }
+        __syncwarp();
         uint8_t* t0 = ost.acquire();
         stile_write_row(t0, (int)lane, z0);
         ost.release(t0, &tmO, 0, row0);
         uint8_t* t1 = ost.acquire();
         stile_write_row(t1, (int)lane, z1);
         ost.release(t1, &tmO, 32, row0);
-        const float s0 = transpose_reduce32(z0);
-        my_colsum[lane] += s0;
-        const float s1 = transpose_reduce32(z1);
-        my_colsum[32 + lane] += s1;
       }
       tc_fence_before();
       __syncwarp();
