@@ -313,10 +313,11 @@ def main_ours(args, world, rank, local):
                 "unit": "TFLOP/s", "frac": achieved / tf_sus, "traffic": traffic,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (fp16 dense = bf16 dense, nominal ratio 1)",
                 "flops_per_launch": dfl / dcnt, "ms_per_launch": davg_s * 1e3}
-    # our kernels per step (srl_ppo_train_step): gae_kernel, moments merge (2 when world > 1),
-    # the 3L+2 GEMMs, finalize_w + finalize_b + extras, adam, stats (NCCL's kernels not counted)
+    # our kernels per step (srl_ppo_train_step): gae_kernel (merges the moments itself),
+    # + moments merge when world > 1, the 3L+2 GEMMs, finalize_w + finalize_b + extras, adam,
+    # stats (NCCL's kernels are not counted)
     L = len(cfg.hidden)
-    per_step = 1 + (2 if world > 1 else 1) + (L + 1 + (L + 1) + L) + 3 + 1 + 1
+    per_step = 1 + (1 if world > 1 else 0) + (L + 1 + (L + 1) + L) + 3 + 1 + 1
     cpu = None
     if not args.no_cpu_baseline:
         v, cn, Bp, secs = time_oracle(cfg, args.cpu_seconds)

@@ -122,6 +122,7 @@ struct srl_ctx {
   // train-step buffers (srl_ppo_train_step): adv, ret [max_n] f32; gae partials; mean/std
   float *adv = nullptr, *ret = nullptr;
   double *gae_part = nullptr, *gae_stats = nullptr, *mean_std = nullptr;
+  unsigned int* gae_counter = nullptr;
   int gae_part_cap = 0;
 };
 
@@ -349,6 +350,7 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if ((st = dalloc(c, &c->gae_part, sizeof(double) * 3 * c->gae_part_cap))) return bail(st);
   if ((st = dalloc(c, &c->gae_stats, sizeof(double) * 4))) return bail(st);
   if ((st = dalloc(c, &c->mean_std, sizeof(double) * 2))) return bail(st);
+  if ((st = dalloc(c, &c->gae_counter, sizeof(unsigned int) * 4))) return bail(st);
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(id.internal, nccl_id, 128);
@@ -644,20 +646,18 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t n = (int64_t)T * B;
   {
+    // a1 + a2 (local): the scan's last block merges the moments (world 1: straight to mean/std)
     ProfScope ps(c, s, "gae_scan", 0.0, 17.0 * n);
     CK(launch_gae(T, B, B, rewards, values, dones, c->cfg.gamma, c->cfg.gae_lambda, c->adv,
-                  c->ret, c->gae_part, s));
+                  c->ret, c->gae_part, s, c->gae_counter, c->gae_stats,
+                  c->world == 1 ? c->mean_std : nullptr, c->cfg.adv_unbiased));
   }
-  {
-    ProfScope ps(c, s, "adv_norm", 0.0, 24.0 * nb);
-    if (c->world > 1) {
-      CK(launch_merge_moments(c->gae_part, nb, c->gae_stats, nullptr, 0, s));
-      double* gathered = c->norm_scratch;
-      CKN(ncclAllGather(c->gae_stats, gathered, 3, ncclDouble, c->comm, s));
-      CK(launch_merge_moments(gathered, c->world, nullptr, c->mean_std, c->cfg.adv_unbiased, s));
-    } else {
-      CK(launch_merge_moments(c->gae_part, nb, c->gae_stats, c->mean_std, c->cfg.adv_unbiased, s));
-    }
+  if (c->world > 1) {
+    // a2 (global): all-gather the ranks' {n, mean, M2} and merge them in rank order
+    ProfScope ps(c, s, "adv_norm", 0.0, 24.0 * c->world);
+    double* gathered = c->norm_scratch;
+    CKN(ncclAllGather(c->gae_stats, gathered, 3, ncclDouble, c->comm, s));
+    CK(launch_merge_moments(gathered, c->world, nullptr, c->mean_std, c->cfg.adv_unbiased, s));
   }
   return srl_ppo_step(c, n, n_global, obs, actions, logp_old, c->adv, c->ret, c->mean_std, 1,
                       stats_out, stream);

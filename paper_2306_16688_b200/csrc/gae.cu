@@ -49,11 +49,31 @@ __device__ __forceinline__ void warp_merge(double& n, double& mean, double& m2) 
   }
 }
 
+// warp 0 merges `count` partial triples in index order: lane l folds a contiguous range, then a
+// fixed butterfly; writes {n, mean, M2} and optionally {mean, sigma}
+__device__ void warp0_merge_parts(const double* part, int count, double* out, double* ms,
+                                  int unbiased) {
+  const int lane = threadIdx.x & 31;
+  double n = 0, mean = 0, m2 = 0;
+  const int lo = (int)((int64_t)count * lane / 32), hi = (int)((int64_t)count * (lane + 1) / 32);
+  for (int k = lo; k < hi; ++k) chan_merge(n, mean, m2, part[3 * k], part[3 * k + 1], part[3 * k + 2]);
+  warp_merge(n, mean, m2);
+  if (lane == 0) {
+    if (out) { out[0] = n; out[1] = mean; out[2] = m2; }
+    if (ms) {
+      const double denom = unbiased ? n - 1.0 : n;
+      ms[0] = mean;
+      ms[1] = denom > 0 ? sqrt(m2 / denom) : 0.0;
+    }
+  }
+}
+
 template <int TC>
 __global__ void __launch_bounds__(TC <= 8 ? 1024 : 512)
 gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __restrict__ v,
            const uint8_t* __restrict__ d, float gamma, float gl, float* __restrict__ adv,
-           float* __restrict__ ret, double* __restrict__ part) {
+           float* __restrict__ ret, double* __restrict__ part, unsigned int* counter,
+           double* stats_out, double* mean_std_out, int unbiased) {
   __shared__ float s_a[32][33];
   __shared__ float s_p[32][33];
   __shared__ float s_carry[32];
@@ -128,28 +148,42 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
   warp_merge(n, mean, m2);
   if (lane == 0) { s_mom[w][0] = n; s_mom[w][1] = mean; s_mom[w][2] = m2; }
   __syncthreads();
+  __shared__ bool s_last;
   if (threadIdx.x == 0) {
     double N = 0, M = 0, Q = 0;
     for (int k = 0; k < W; ++k) chan_merge(N, M, Q, s_mom[k][0], s_mom[k][1], s_mom[k][2]);
     part[blockIdx.x * 3 + 0] = N;
     part[blockIdx.x * 3 + 1] = M;
     part[blockIdx.x * 3 + 2] = Q;
+    if (counter) {   // the last block to finish merges every block's triple (fixed order)
+      __threadfence();
+      s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
   }
+  if (!counter) return;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < 32) warp0_merge_parts(part, gridDim.x, stats_out, mean_std_out, unbiased);
+  if (threadIdx.x == 0) *counter = 0;   // ready for the next launch
 }
 
 int gae_num_blocks(int B) { return (B + 31) / 32; }
 
 cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
                        float gamma, float lambda, float* adv, float* ret, double* part,
-                       cudaStream_t s) {
+                       cudaStream_t s, unsigned int* counter, double* stats_out,
+                       double* mean_std_out, int unbiased) {
   const int blocks = gae_num_blocks(B);
   const float gl = gamma * lambda;
   if (T <= 32 * 8) {            // <= 32 warps of 8 rows, one pass
     const int W = (T + 7) / 8;
-    gae_kernel<8><<<blocks, 32 * W, 0, s>>>(T, B, ld, r, v, d, gamma, gl, adv, ret, part);
+    gae_kernel<8><<<blocks, 32 * W, 0, s>>>(T, B, ld, r, v, d, gamma, gl, adv, ret, part,
+                                            counter, stats_out, mean_std_out, unbiased);
   } else {                       // <= 16 warps of 16 rows per super-chunk of 256 rows
     const int W = std::min(16, (T + 15) / 16);
-    gae_kernel<16><<<blocks, 32 * W, 0, s>>>(T, B, ld, r, v, d, gamma, gl, adv, ret, part);
+    gae_kernel<16><<<blocks, 32 * W, 0, s>>>(T, B, ld, r, v, d, gamma, gl, adv, ret, part,
+                                             counter, stats_out, mean_std_out, unbiased);
   }
   return cudaGetLastError();
 }

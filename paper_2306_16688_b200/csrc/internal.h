@@ -19,9 +19,13 @@ int num_sms();
 
 // ---- a1 / a2 kernels (gae.cu)
 // Moments triple {n, mean, M2} as 3 doubles.
+// counter != null: the last block merges the partials into stats_out {n, mean, M2} and
+// mean_std_out {mean, sigma} (either may be null) and resets *counter to 0.
 cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
                        float gamma, float lambda, float* adv, float* ret,
-                       double* part /* [gae_num_blocks(B)][3] or null */, cudaStream_t s);
+                       double* part /* [gae_num_blocks(B)][3] or null */, cudaStream_t s,
+                       unsigned int* counter = nullptr, double* stats_out = nullptr,
+                       double* mean_std_out = nullptr, int unbiased = 0);
 int gae_num_blocks(int B);
 constexpr int kMomentBlocks = 256;
 cudaError_t launch_moments(const float* x, int64_t n, double* part /*[kMomentBlocks][3]*/,
@@ -59,6 +63,7 @@ struct Segment {
   // fp16 shadow (weights only)
   __half* w16;
   int w16_ld;
+  int64_t item0;        // finalize: first work item (4 partial-buffer entries) of this segment
 };
 constexpr int kMaxSegs = 20;
 struct SegTable {

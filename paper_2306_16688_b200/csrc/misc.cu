@@ -18,25 +18,53 @@ __device__ __forceinline__ int find_seg(const SegTable& t, int64_t p) {
   return k;
 }
 
-// weight gradients: dW = (1/N) * sum over the split-K partials, in split order
-__global__ void __launch_bounds__(256) finalize_w_kernel(const SegTable t, int64_t P, float inv_n,
-                                                         float* __restrict__ bucket,
+// weight gradients: dW = (1/N) * sum over the split-K partials, in split order.  Work item =
+// 4 consecutive entries along the partial buffer's contiguous dimension (float4 loads of every
+// split, coalesced across threads): W[r][c..c+3] for hidden layers; for the head, whose
+// partial holds dW^T[in][64], entries [i][j..j+3] written to W[j..j+3][i].
+__global__ void __launch_bounds__(256) finalize_w_kernel(const SegTable t, int64_t items,
+                                                         float inv_n, float* __restrict__ bucket,
                                                          unsigned long long* counters) {
   uint32_t bad = 0;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const Segment& s = t.s[find_seg(t, p)];
-    if (s.is_bias) continue;
-    const int64_t idx = p - s.off;
-    const int r = (int)(idx / s.cols), cc = (int)(idx % s.cols);
-    const float* src = s.transposed ? s.part + (int64_t)cc * s.ld_part + r
-                                    : s.part + (int64_t)r * s.ld_part + cc;
-    float acc = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < s.splits; ++k) acc += __ldg(src + (int64_t)k * s.split_stride);
-    const float g = acc * inv_n;
-    if (!isfinite(g)) ++bad;
-    bucket[p] = g;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < items;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int k = 0;
+    for (int i = 0; i < t.n; ++i)
+      if (!t.s[i].is_bias && q >= t.s[i].item0) k = i;
+    const Segment& s = t.s[k];
+    const int prow_len = s.transposed ? (int)s.ld_part : s.cols;   // contiguous extent
+    const int per_row = (prow_len + 3) / 4;                        // work items per row
+    const int64_t qi = q - s.item0;
+    const int pr = (int)(qi / per_row), pc = 4 * (int)(qi % per_row);
+    const float* src = s.part + (int64_t)pr * s.ld_part + pc;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    if ((s.ld_part & 3) == 0 && pc + 4 <= prow_len) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      const int64_t st4 = s.split_stride / 4;
+#pragma unroll 8
+      for (int sp = 0; sp < s.splits; ++sp) {
+        const float4 x = __ldg(s4 + sp * st4);
+        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+      }
+    } else {
+      const int cnt = min(4, prow_len - pc);
+      for (int sp = 0; sp < s.splits; ++sp)
+        for (int e = 0; e < cnt; ++e) a[e] += __ldg(src + (int64_t)sp * s.split_stride + e);
+    }
+    for (int e = 0; e < 4; ++e) {
+      const int c = pc + e;
+      if (c >= prow_len) break;
+      int64_t p;
+      if (s.transposed) {                    // partial [i = pr][j = c] -> W[j][i]
+        if (c >= s.rows) break;
+        p = s.off + (int64_t)c * s.cols + pr;
+      } else {
+        p = s.off + (int64_t)pr * s.cols + c;
+      }
+      const float g = a[e] * inv_n;
+      if (!isfinite(g)) ++bad;
+      bucket[p] = g;
+    }
   }
   const uint32_t tot = __reduce_add_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0 && tot) atomicAdd(counters, (unsigned long long)tot);
@@ -67,14 +95,24 @@ __global__ void __launch_bounds__(256) finalize_b_kernel(const SegTable t, float
   }
 }
 
-cudaError_t launch_finalize_grads(const SegTable& t, int64_t P, float inv_n, float* bucket,
+cudaError_t launch_finalize_grads(const SegTable& t0, int64_t P, float inv_n, float* bucket,
                                   unsigned long long* counters, cudaStream_t s) {
-  int64_t blocks = (P + 255) / 256;
-  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
-  finalize_w_kernel<<<(int)blocks, 256, 0, s>>>(t, P, inv_n, bucket, counters);
+  (void)P;
+  SegTable t = t0;
+  int64_t items = 0;
   int nb = 0;
-  for (int i = 0; i < t.n; ++i)
-    if (t.s[i].is_bias) nb += t.s[i].cols;
+  for (int i = 0; i < t.n; ++i) {
+    Segment& g = t.s[i];
+    if (g.is_bias) { nb += g.cols; continue; }
+    g.item0 = items;
+    const int64_t prow = g.transposed ? g.ld_part : g.cols;   // contiguous extent
+    const int64_t nrow = g.transposed ? g.cols : g.rows;      // head partial: [in][64]
+    items += nrow * ((prow + 3) / 4);
+  }
+  int64_t blocks = (items + 255) / 256;
+  if (blocks > 16 * num_sms()) blocks = 16 * num_sms();
+  if (blocks < 1) blocks = 1;
+  finalize_w_kernel<<<(int)blocks, 256, 0, s>>>(t, items, inv_n, bucket, counters);
   finalize_b_kernel<<<(nb + 7) / 8, 256, 0, s>>>(t, inv_n, bucket, counters);
   return cudaGetLastError();
 }
@@ -102,7 +140,16 @@ cudaError_t launch_extras(int64_t P, float inv_n, const double* stats_part, int 
 }
 
 // a7: Adam, PyTorch semantics (C-A13); skipped entirely if any rank saw a
-// non-finite loss or gradient (bucket[P+5] > 0 after the allreduce).
+// non-finite loss or gradient (bucket[P+5] > 0 after the allreduce).  4 parameters per
+// thread (float4 p, m, v, g); segment offsets are multiples of 4 (hidden widths % 64 == 0).
+__device__ __forceinline__ float adam_one(float& p, float& m, float& v, float g, float b1, float b2,
+                                          float step_size, float bc2_sqrt, float eps) {
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  p = p - step_size * (m / (sqrtf(v) / bc2_sqrt + eps));
+  return p;
+}
+
 __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
                                                    float* __restrict__ p, float* __restrict__ m,
                                                    float* __restrict__ v,
@@ -114,21 +161,53 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
   const float bc1 = (float)(1.0 - pow((double)b1, step));
   const float bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, step));
   const float step_size = lr / bc1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i];
-    const float mi = b1 * m[i] + (1.f - b1) * gi;
-    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
-    m[i] = mi;
-    v[i] = vi;
-    const float denom = sqrtf(vi) / bc2_sqrt + eps;
-    const float pi = p[i] - step_size * (mi / denom);
-    p[i] = pi;
-    const Segment& s = t.s[find_seg(t, i)];
-    if (!s.is_bias) {
-      const int64_t idx = i - s.off;
-      const int r = (int)(idx / s.cols), c = (int)(idx % s.cols);
-      s.w16[(int64_t)r * s.w16_ld + c] = __float2half_rn(pi);
+  const int64_t nq = (P + 3) / 4;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = 4 * q;
+    if (i0 + 4 <= P) {
+      float4 pp = *reinterpret_cast<const float4*>(p + i0);
+      float4 mm = *reinterpret_cast<const float4*>(m + i0);
+      float4 vv = *reinterpret_cast<const float4*>(v + i0);
+      const float4 gg = *reinterpret_cast<const float4*>(g + i0);
+      adam_one(pp.x, mm.x, vv.x, gg.x, b1, b2, step_size, bc2_sqrt, eps);
+      adam_one(pp.y, mm.y, vv.y, gg.y, b1, b2, step_size, bc2_sqrt, eps);
+      adam_one(pp.z, mm.z, vv.z, gg.z, b1, b2, step_size, bc2_sqrt, eps);
+      adam_one(pp.w, mm.w, vv.w, gg.w, b1, b2, step_size, bc2_sqrt, eps);
+      *reinterpret_cast<float4*>(p + i0) = pp;
+      *reinterpret_cast<float4*>(m + i0) = mm;
+      *reinterpret_cast<float4*>(v + i0) = vv;
+      const float pv[4] = {pp.x, pp.y, pp.z, pp.w};
+      const Segment& s = t.s[find_seg(t, i0)];
+      if (!s.is_bias) {
+        const int64_t idx = i0 - s.off;
+        const int r = (int)(idx / s.cols), c = (int)(idx % s.cols);
+        if ((s.cols & 3) == 0 && (s.w16_ld & 3) == 0) {          // 4 entries of one row
+          __half2 h0 = __floats2half2_rn(pv[0], pv[1]), h1 = __floats2half2_rn(pv[2], pv[3]);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&h0);
+          u.y = *reinterpret_cast<uint32_t*>(&h1);
+          *reinterpret_cast<uint2*>(s.w16 + (int64_t)r * s.w16_ld + c) = u;
+        } else {
+          for (int e = 0; e < 4; ++e) {
+            const Segment& se = t.s[find_seg(t, i0 + e)];
+            if (se.is_bias) continue;
+            const int64_t ix = i0 + e - se.off;
+            se.w16[(ix / se.cols) * se.w16_ld + ix % se.cols] = __float2half_rn(pv[e]);
+          }
+        }
+      }
+    } else {
+      for (int64_t i = i0; i < P; ++i) {
+        float pi = p[i], mi = m[i], vi = v[i];
+        adam_one(pi, mi, vi, g[i], b1, b2, step_size, bc2_sqrt, eps);
+        p[i] = pi; m[i] = mi; v[i] = vi;
+        const Segment& se = t.s[find_seg(t, i)];
+        if (!se.is_bias) {
+          const int64_t ix = i - se.off;
+          se.w16[(ix / se.cols) * se.w16_ld + ix % se.cols] = __float2half_rn(pi);
+        }
+      }
     }
   }
 }
@@ -136,7 +215,7 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
 cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float* v,
                         const float* bucket, const int64_t* t_dev, float lr, float b1, float b2,
                         float eps, cudaStream_t s) {
-  int64_t blocks = (P + 255) / 256;
+  int64_t blocks = ((P + 3) / 4 + 255) / 256;
   if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
   adam_kernel<<<(int)blocks, 256, 0, s>>>(t, P, p, m, v, bucket, t_dev, lr, b1, b2, eps);
   return cudaGetLastError();
