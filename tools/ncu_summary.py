@@ -1,0 +1,95 @@
+"""Summarise ncu captures into profiles/ (tracked).
+
+    python tools/ncu_summary.py launches <launches.csv> <round> [config]
+        -> profiles/<round>_launches.csv (copy), profiles/<round>_launches.md (one step, per-kernel
+           duration / DRAM bytes / share), profiles/ncu_traffic.json[config][kernel] = DRAM bytes
+    python tools/ncu_summary.py full <report.ncu-rep> <round> <name>
+        -> profiles/<round>_<name>_ncu.txt (SOL, tensor pipe, DRAM, stall reasons)
+"""
+import collections
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROF = os.path.join(ROOT, "profiles")
+
+# launch order of one srl_ppo_train_step for an L=2 MLP (see api.cu)
+STEP_ORDER = ["gae_scan", "fwd_l1", "fwd_hidden", "head_loss", "dW_head", "dX_head", "dW_hidden",
+              "dX_hidden", "dW_l1", "finalize_w", "finalize_b", "extras", "adam", "stats"]
+
+
+def launches(path, rnd, config="atari"):
+    os.makedirs(PROF, exist_ok=True)
+    shutil.copy(path, os.path.join(PROF, f"{rnd}_launches.csv"))
+    txt = open(path).read()
+    rows = list(csv.DictReader(io.StringIO(txt[txt.index('"ID"'):])))
+    by = collections.OrderedDict()
+    for r in rows:
+        by.setdefault(int(r["ID"]), {"kernel": r["Kernel Name"]})[r["Metric Name"]] = float(
+            r["Metric Value"].replace(",", ""))
+    recs = list(by.values())
+    start = next(i for i, r in enumerate(recs) if r["kernel"].startswith("void gae_kernel"))
+    step = recs[start:start + len(STEP_ORDER)]
+    tot = sum(r["gpu__time_duration.sum"] for r in step)
+    lines = [f"# {rnd}: ncu launch list, one `srl_ppo_train_step` ({config}-shaped, 1 x B200)", "",
+             "Cold-cache, serialised per-launch durations (`--metrics gpu__time_duration.sum,"
+             "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none`); compare shares.", "",
+             "| kernel | ncu name | us | share | DRAM read MB | DRAM write MB |",
+             "|---|---|---|---|---|---|"]
+    traffic = {}
+    for name, r in zip(STEP_ORDER, step):
+        t = r["gpu__time_duration.sum"] / 1e3
+        rd, wr = r.get("dram__bytes_read.sum", 0.0), r.get("dram__bytes_write.sum", 0.0)
+        traffic[name] = rd + wr
+        lines.append(f"| {name} | `{r['kernel'][:60]}` | {t:.1f} | {100 * t * 1e3 / tot:.1f}% | "
+                     f"{rd / 1e6:.1f} | {wr / 1e6:.1f} |")
+    lines.append(f"| **step** | | {tot / 1e3:.1f} | 100% | | |")
+    traffic["grad_finalize"] = traffic["finalize_w"] + traffic["finalize_b"] + traffic["extras"]
+    open(os.path.join(PROF, f"{rnd}_launches.md"), "w").write("\n".join(lines) + "\n")
+    jp = os.path.join(PROF, "ncu_traffic.json")
+    data = json.load(open(jp)) if os.path.exists(jp) else {}
+    data.setdefault(config, {}).update(traffic)
+    data.setdefault("_source", {})[config] = f"profiles/{rnd}_launches.csv"
+    json.dump(data, open(jp, "w"), indent=1)
+    print("\n".join(lines))
+
+
+def full(rep, rnd, name):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units, r = rows[0], rows[1], rows[2]
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "lts__t_sectors.sum.pct_of_peak_sustained_elapsed",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+            "launch__cluster_dim_x"]
+    out = [f"# {rnd} ncu --set full: {name}", f"kernel: {r[h.index('Kernel Name')]}", ""]
+    for k in keys:
+        if k in h:
+            out.append(f"{k} = {r[h.index(k)]} {units[h.index(k)]}")
+    out.append("")
+    out.append("stall reasons (warps per issue-active cycle):")
+    st = {}
+    for i, k in enumerate(h):
+        if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+            st[k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = float(r[i])
+    for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:10]:
+        out.append(f"  {k:24s} {v:.3f}")
+    open(os.path.join(PROF, f"{rnd}_{name}_ncu.txt"), "w").write("\n".join(out) + "\n")
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3], *(sys.argv[4:5] or ["atari"]))
+    else:
+        full(sys.argv[2], sys.argv[3], sys.argv[4])
