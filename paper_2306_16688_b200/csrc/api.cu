@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -16,6 +17,15 @@ namespace srl {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SRL_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
 
 int num_sms() {
   static int sms = 0;
@@ -496,7 +506,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   const float inv_n = (float)(1.0 / (double)n_global);
   const __half* X0 = reinterpret_cast<const __half*>(obs);
   const int ld_obs = c->cfg.ld_obs;
-  CK(cudaMemsetAsync(c->counters, 0, sizeof(unsigned long long) * 4, s));
+  // c->counters are zero here: zeroed at create, re-zeroed by the stats kernel of every step
 
   // ---------------- a3: forward hidden layers Y_l = tanh(Y_{l-1} W_l^T + b_l)
   for (int l = 0; l < L; ++l) {
@@ -626,7 +636,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
                    c->cfg.beta1, c->cfg.beta2, c->cfg.adam_eps, s));
   }
   CK(launch_stats(c->grads, c->P, adv_mean_std, n_global, c->cfg.value_coef, c->cfg.entropy_coef,
-                  c->t_dev, apply, stats_out, s));
+                  c->t_dev, apply, stats_out, s, c->counters));
   return SRL_OK;
 }
 
@@ -697,6 +707,7 @@ extern "C" srl_status srl_prof_read(srl_ctx* c, int i, const char** name, float*
 // ------------------------------------------------------------------ test hook
 __global__ void sum_parts_kernel(const float* part, int S, int64_t split_stride, int M, int N,
                                  int64_t ld_part, float* D) {
+  griddep_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)M * N;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / N), cc = (int)(i % N);
@@ -735,7 +746,8 @@ extern "C" srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int
   CK(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * S * g.part_split_stride, s));
   g.part = part;
   if (srl_status st = gemm(bn, a_mn != 0, b_mn != 0, EPI_PART, cg, ta, tb, ta, ta, g, num_sms(), s)) return st;
-  sum_parts_kernel<<<256, 256, 0, s>>>(part, S, g.part_split_stride, M, N, g.ld_part, D);
+  CK(launch_k(sum_parts_kernel, dim3(256), dim3(256), 0, s, 1, (const float*)part, S,
+              (int64_t)g.part_split_stride, M, N, (int64_t)g.ld_part, D));
   CK(cudaGetLastError());
   CK(cudaFreeAsync(part, s));
   return SRL_OK;

@@ -74,6 +74,8 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
            const uint8_t* __restrict__ d, float gamma, float gl, float* __restrict__ adv,
            float* __restrict__ ret, double* __restrict__ part, unsigned int* counter,
            double* stats_out, double* mean_std_out, int unbiased) {
+  griddep_wait();
+  griddep_launch();
   __shared__ float s_a[32][33];
   __shared__ float s_p[32][33];
   __shared__ float s_carry[32];
@@ -178,12 +180,12 @@ cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, con
   const float gl = gamma * lambda;
   if (T <= 32 * 8) {            // <= 32 warps of 8 rows, one pass
     const int W = (T + 7) / 8;
-    gae_kernel<8><<<blocks, 32 * W, 0, s>>>(T, B, ld, r, v, d, gamma, gl, adv, ret, part,
-                                            counter, stats_out, mean_std_out, unbiased);
+    return launch_k(gae_kernel<8>, dim3(blocks), dim3(32 * W), 0, s, 1, T, B, ld, r, v, d, gamma,
+                    gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased);
   } else {                       // <= 16 warps of 16 rows per super-chunk of 256 rows
     const int W = std::min(16, (T + 15) / 16);
-    gae_kernel<16><<<blocks, 32 * W, 0, s>>>(T, B, ld, r, v, d, gamma, gl, adv, ret, part,
-                                             counter, stats_out, mean_std_out, unbiased);
+    return launch_k(gae_kernel<16>, dim3(blocks), dim3(32 * W), 0, s, 1, T, B, ld, r, v, d, gamma,
+                    gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased);
   }
   return cudaGetLastError();
 }
@@ -191,6 +193,8 @@ cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, con
 // ---------------------------------------------------------------- a2: moments of a vector
 __global__ void __launch_bounds__(256) moments_kernel(const float* __restrict__ x, int64_t n,
                                                       double* __restrict__ part) {
+  griddep_wait();
+  griddep_launch();
   __shared__ double s_mom[8][3];
   // block k owns the contiguous range [k*n/G, (k+1)*n/G); threads stride inside it
   const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
@@ -221,14 +225,15 @@ __global__ void __launch_bounds__(256) moments_kernel(const float* __restrict__ 
 }
 
 cudaError_t launch_moments(const float* x, int64_t n, double* part, cudaStream_t s) {
-  moments_kernel<<<kMomentBlocks, 256, 0, s>>>(x, n, part);
-  return cudaGetLastError();
+  return launch_k(moments_kernel, dim3(kMomentBlocks), dim3(256), 0, s, 1, x, n, part);
 }
 
 // merge partial triples in index order (contiguous ranges per thread, then a fixed tree)
 __global__ void __launch_bounds__(256) merge_moments_kernel(const double* __restrict__ part,
                                                             int count, double* out,
                                                             double* mean_std, int unbiased) {
+  griddep_wait();
+  griddep_launch();
   __shared__ double sn[256], sm[256], sq[256];
   const int t = threadIdx.x;
   const int lo = (int)((int64_t)count * t / 256), hi = (int)((int64_t)count * (t + 1) / 256);
@@ -256,12 +261,14 @@ __global__ void __launch_bounds__(256) merge_moments_kernel(const double* __rest
 
 cudaError_t launch_merge_moments(const double* part, int count, double* out, double* mean_std,
                                  int unbiased, cudaStream_t s) {
-  merge_moments_kernel<<<1, 256, 0, s>>>(part, count, out, mean_std, unbiased);
-  return cudaGetLastError();
+  return launch_k(merge_moments_kernel, dim3(1), dim3(256), 0, s, 1, part, count, out, mean_std,
+                  unbiased);
 }
 
 __global__ void normalize_kernel(float* __restrict__ x, int64_t n, const double* __restrict__ ms,
                                  float eps) {
+  griddep_wait();
+  griddep_launch();
   const double mu = ms[0], sd = ms[1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -273,8 +280,7 @@ cudaError_t launch_normalize(float* x, int64_t n, const double* mean_std, float 
   int64_t blocks = (n + 255) / 256;
   if (blocks > 4 * 148) blocks = 4 * 148;
   if (blocks < 1) blocks = 1;
-  normalize_kernel<<<(int)blocks, 256, 0, s>>>(x, n, mean_std, eps);
-  return cudaGetLastError();
+  return launch_k(normalize_kernel, dim3((unsigned)blocks), dim3(256), 0, s, 1, x, n, mean_std, eps);
 }
 
 }  // namespace srl

@@ -334,6 +334,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();   // peer barriers initialised before remote use
   tc_fence_after();
+  // PDL: everything above overlapped the previous kernel's tail; its outputs are read below
+  griddep_wait();
+  griddep_launch();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {

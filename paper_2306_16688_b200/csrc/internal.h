@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "gemm_tc.cuh"
 
@@ -16,6 +17,37 @@ void set_error(const std::string& msg);
 
 // ---- device info
 int num_sms();
+
+// ---- launches: every kernel goes out with programmatic stream serialisation (PDL) so its
+// prologue overlaps the previous kernel's tail; kernels call griddep_wait() before reading
+// what the previous kernel wrote.  SRL_PDL=0 in the environment turns it off.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster_x > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster_x;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---- a1 / a2 kernels (gae.cu)
 // Moments triple {n, mean, M2} as 3 doubles.
@@ -80,6 +112,7 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
 cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s);
 cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,
                          int64_t n_global, float value_coef, float entropy_coef,
-                         int64_t* t_dev, int apply, void* stats_out, cudaStream_t s);
+                         int64_t* t_dev, int apply, void* stats_out, cudaStream_t s,
+                         unsigned long long* counters = nullptr);
 
 }  // namespace srl

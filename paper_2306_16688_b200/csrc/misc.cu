@@ -25,6 +25,8 @@ __device__ __forceinline__ int find_seg(const SegTable& t, int64_t p) {
 __global__ void __launch_bounds__(256) finalize_w_kernel(const SegTable t, int64_t items,
                                                          float inv_n, float* __restrict__ bucket,
                                                          unsigned long long* counters) {
+  griddep_wait();
+  griddep_launch();
   uint32_t bad = 0;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < items;
        q += (int64_t)gridDim.x * blockDim.x) {
@@ -75,6 +77,8 @@ __global__ void __launch_bounds__(256) finalize_w_kernel(const SegTable t, int64
 __global__ void __launch_bounds__(256) finalize_b_kernel(const SegTable t, float inv_n,
                                                          float* __restrict__ bucket,
                                                          unsigned long long* counters) {
+  griddep_wait();
+  griddep_launch();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   int e = warp;
@@ -112,13 +116,17 @@ cudaError_t launch_finalize_grads(const SegTable& t0, int64_t P, float inv_n, fl
   int64_t blocks = (items + 255) / 256;
   if (blocks > 16 * num_sms()) blocks = 16 * num_sms();
   if (blocks < 1) blocks = 1;
-  finalize_w_kernel<<<(int)blocks, 256, 0, s>>>(t, items, inv_n, bucket, counters);
-  finalize_b_kernel<<<(nb + 7) / 8, 256, 0, s>>>(t, inv_n, bucket, counters);
-  return cudaGetLastError();
+  cudaError_t e = launch_k(finalize_w_kernel, dim3((unsigned)blocks), dim3(256), 0, s, 1, t, items,
+                           inv_n, bucket, counters);
+  if (e != cudaSuccess) return e;
+  return launch_k(finalize_b_kernel, dim3((nb + 7) / 8), dim3(256), 0, s, 1, t, inv_n, bucket,
+                  counters);
 }
 
 __global__ void extras_kernel(int64_t P, float inv_n, const double* __restrict__ stats_part,
                               int nstats, const unsigned long long* counters, float* bucket) {
+  griddep_wait();
+  griddep_launch();
   const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (k < 5) {
     double s = 0.0;
@@ -135,8 +143,8 @@ __global__ void extras_kernel(int64_t P, float inv_n, const double* __restrict__
 
 cudaError_t launch_extras(int64_t P, float inv_n, const double* stats_part, int nstats,
                           const unsigned long long* counters, float* bucket, cudaStream_t s) {
-  extras_kernel<<<1, 192, 0, s>>>(P, inv_n, stats_part, nstats, counters, bucket);
-  return cudaGetLastError();
+  return launch_k(extras_kernel, dim3(1), dim3(192), 0, s, 1, P, inv_n, stats_part, nstats,
+                  counters, bucket);
 }
 
 // a7: Adam, PyTorch semantics (C-A13); skipped entirely if any rank saw a
@@ -156,6 +164,8 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
                                                    const float* __restrict__ g,
                                                    const int64_t* __restrict__ t_dev, float lr,
                                                    float b1, float b2, float eps) {
+  griddep_wait();
+  griddep_launch();
   if (g[P + 5] > 0.f) return;
   const double step = (double)(t_dev[0] + 1);
   const float bc1 = (float)(1.0 - pow((double)b1, step));
@@ -217,11 +227,13 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
                         float eps, cudaStream_t s) {
   int64_t blocks = ((P + 3) / 4 + 255) / 256;
   if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
-  adam_kernel<<<(int)blocks, 256, 0, s>>>(t, P, p, m, v, bucket, t_dev, lr, b1, b2, eps);
-  return cudaGetLastError();
+  return launch_k(adam_kernel, dim3((unsigned)blocks), dim3(256), 0, s, 1, t, P, p, m, v, bucket,
+                  t_dev, lr, b1, b2, eps);
 }
 
 __global__ void shadow_kernel(const SegTable t, const float* __restrict__ p) {
+  griddep_wait();
+  griddep_launch();
   for (int k = 0; k < t.n; ++k) {
     const Segment& s = t.s[k];
     if (s.is_bias) continue;
@@ -235,14 +247,17 @@ __global__ void shadow_kernel(const SegTable t, const float* __restrict__ p) {
 }
 
 cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s) {
-  shadow_kernel<<<2 * num_sms(), 256, 0, s>>>(t, p);
-  return cudaGetLastError();
+  return launch_k(shadow_kernel, dim3(2 * num_sms()), dim3(256), 0, s, 1, t, p);
 }
 
 __global__ void stats_kernel(const float* __restrict__ bucket, int64_t P,
                              const double* __restrict__ mean_std, int64_t n_global, float cv,
-                             float ce, int64_t* t_dev, int apply, srl_ppo_stats* out) {
+                             float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
+                             unsigned long long* counters) {
+  griddep_wait();
+  griddep_launch();
   const float* ex = bucket + P;
+  if (counters) { counters[0] = 0; counters[1] = 0; }   // ready for the next step
   if (apply && ex[5] == 0.f) t_dev[0] += 1;   // policy version (Code 1 inc_version)
   if (!out) return;
   out->policy_loss = ex[0];
@@ -261,10 +276,10 @@ __global__ void stats_kernel(const float* __restrict__ bucket, int64_t P,
 
 cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,
                          int64_t n_global, float value_coef, float entropy_coef, int64_t* t_dev,
-                         int apply, void* stats_out, cudaStream_t s) {
-  stats_kernel<<<1, 1, 0, s>>>(bucket, P, mean_std, n_global, value_coef, entropy_coef, t_dev,
-                               apply, static_cast<srl_ppo_stats*>(stats_out));
-  return cudaGetLastError();
+                         int apply, void* stats_out, cudaStream_t s, unsigned long long* counters) {
+  return launch_k(stats_kernel, dim3(1), dim3(1), 0, s, 1, bucket, P, mean_std, n_global,
+                  value_coef, entropy_coef, t_dev, apply, static_cast<srl_ppo_stats*>(stats_out),
+                  counters);
 }
 
 }  // namespace srl

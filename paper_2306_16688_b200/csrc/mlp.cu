@@ -54,24 +54,8 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  if constexpr (CG == 1) {
-    kern<<<grid, kThreads, smem, s>>>(ta, tb, to, ty, a);
-  } else {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, to, ty, a);
-    if (e != cudaSuccess) return e;
-  }
+  cudaError_t e = launch_k(kern, dim3((unsigned)grid), dim3(kThreads), smem, s, CG, ta, tb, to, ty, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -88,6 +88,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// wait until the preceding grid in the stream has completed and its writes are visible
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// allow the next grid in the stream to start launching (its own griddep_wait still orders it)
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ clusters (CTA pairs)
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;   // shared::cluster address -> CTA rank 0 copy
 __device__ __forceinline__ uint32_t cluster_ctarank() {
