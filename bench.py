@@ -26,6 +26,16 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "PPO trainer samples/sec (GAE+update, device-timed) at 1/2/4/8 B200"
+_OUT_FD = None
+
+
+def emit(obj):
+    line = (json.dumps(obj) + "\n").encode()
+    if _OUT_FD is not None:
+        os.write(_OUT_FD, line)
+    else:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
 UNIT = "samples/s"
 
 
@@ -160,7 +170,7 @@ def reference_arm(args, world, rank):
            "data": "synthetic", "config": {"workload": cfg.name, "T": cfg.T, "B_per_step": Bp * cfg.agents},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 # ------------------------------------------------------------------ our arm
@@ -191,11 +201,8 @@ def main_ours(args, world, rank, local):
 
     nccl_id = None
     if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
+        from paper_2306_16688_b200.dist import broadcast_unique_id
+        nccl_id = broadcast_unique_id(device=dev)
     ctx = P.PPOContext(P.NetSpec.from_config(cfg), max_local_n=n, rank=rank, world=world,
                        nccl_id=nccl_id, device=local)
     ctx.load_params(params)
@@ -363,7 +370,7 @@ def main_ours(args, world, rank, local):
     }
     if any(math.isnan(x) for x in (out["value"],)):
         raise SystemExit("nan throughput")
-    print(json.dumps(out), flush=True)
+    emit(out)
     if dist:
         dist.destroy_process_group()
 
@@ -371,6 +378,11 @@ def main_ours(args, world, rank, local):
 def main():
     args = parse()
     world, rank, local = dist_env()
+    # keep stdout for the one JSON line: library / NCCL chatter on fd 1 goes to stderr
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
+    global _OUT_FD
+    _OUT_FD = out_fd
     if args.impl == "reference":
         reference_arm(args, world, rank)
         return

@@ -18,6 +18,16 @@ namespace srl {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
+// SRL_TANH=accurate: rational tanh (rel. err ~2e-7) instead of MUFU.TANH (~5e-4)
+static bool tanh_accurate() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SRL_TANH");
+    on = (e && e[0] == 'a') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -523,6 +533,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     g.m_tiles = (n + 128 * y.cg_fwd - 1) / (128 * y.cg_fwd); g.n_tiles = y.out / y.bn_fwd; g.k_splits = 1;
     g.kb_total = (y.in + 63) / 64; g.kb_per_split = g.kb_total;
     g.bias = c->params + y.b_off;
+    g.flags = tanh_accurate() ? 1 : 0;
     ProfScope ps(c, s, l == 0 ? "fwd_l1" : "fwd_hidden", 2.0 * n * y.in * y.out,
                  2.0 * n * (y.in + y.out) + 2.0 * y.in * y.out + 4.0 * y.out);
     if (srl_status st = gemm(y.bn_fwd, false, false, EPI_TANH, y.cg_fwd, ta, tb, to, to, g, sms, s)) return st;

@@ -51,6 +51,7 @@ struct GemmArgs {
   int n_heads, A;
   int head_size[kMaxHeads];
   float clip_eps, value_coef, entropy_coef, adv_eps;
+  int flags;                                      // bit 0: accurate tanh (TANH epilogue)
 };
 
 // Shared-memory layout (identical on host and device):
@@ -475,10 +476,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 bb = b4[q];
-            v[4 * q + 0] = tanh_mufu(v[4 * q + 0] + bb.x);
-            v[4 * q + 1] = tanh_mufu(v[4 * q + 1] + bb.y);
-            v[4 * q + 2] = tanh_mufu(v[4 * q + 2] + bb.z);
-            v[4 * q + 3] = tanh_mufu(v[4 * q + 3] + bb.w);
+            if (args.flags & 1) {
+              v[4 * q + 0] = tanh_fast_accurate(v[4 * q + 0] + bb.x);
+              v[4 * q + 1] = tanh_fast_accurate(v[4 * q + 1] + bb.y);
+              v[4 * q + 2] = tanh_fast_accurate(v[4 * q + 2] + bb.z);
+              v[4 * q + 3] = tanh_fast_accurate(v[4 * q + 3] + bb.w);
+            } else {
+              v[4 * q + 0] = tanh_mufu(v[4 * q + 0] + bb.x);
+              v[4 * q + 1] = tanh_mufu(v[4 * q + 1] + bb.y);
+              v[4 * q + 2] = tanh_mufu(v[4 * q + 2] + bb.z);
+              v[4 * q + 3] = tanh_mufu(v[4 * q + 3] + bb.w);
+            }
           }
           uint8_t* t = ost.acquire();
           stile_write_row(t, (int)lane, v);

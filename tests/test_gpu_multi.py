@@ -1,0 +1,82 @@
+"""a2/a6 over real NCCL with one process per GPU (needs >= 2 GPUs; skipped otherwise):
+K ranks' train steps on disjoint column shards give bit-identical parameters on every rank,
+a global normalisation identical to the full batch, and the full-batch oracle gradient."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        import synth
+        import paper_2306_16688_b200 as P
+        from paper_2306_16688_b200.dist import broadcast_unique_id
+        from ppo_harness import make_inputs, to_dev
+        cfg = synth.get_config("gfootball").with_(B=16)
+        params, sh = make_inputs(cfg, seed=3, world=world, rank=rank)
+        uid = broadcast_unique_id(device=torch.device("cuda", rank))
+        ctx = P.PPOContext(P.NetSpec.from_config(cfg), max_local_n=sh["n"], rank=rank, world=world,
+                           nccl_id=uid, device=rank)
+        ctx.load_params(torch.from_numpy(params).cuda())
+        d = to_dev(sh)
+        st = P.decode_stats(ctx.train_step(cfg.N, d["rewards"], d["values"], d["dones"], d["obs"],
+                                           d["actions"], d["logp_old"]))
+        torch.cuda.synchronize()
+        q.put((rank, st, ctx.params().cpu().numpy(), ctx.grads().cpu().numpy()))
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_nccl_ranks_match_full_batch(world):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle
+    import synth
+    from ppo_harness import grad_errors, make_inputs
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg = synth.get_config("gfootball").with_(B=16)
+    params, full = make_inputs(cfg, seed=3)
+    o = oracle.ppo_step(cfg, params, [full], apply=False)
+    for r in res[1:]:                                     # S:L522 parameters bit-identical
+        assert np.array_equal(r[2], res[0][2]) and np.array_equal(r[3], res[0][3])
+    st = res[0][1]
+    assert st["n_global"] == cfg.N and st["step"] == 1
+    assert abs(st["adv_mean"] - o["mean"]) <= 1e-6 * o["std"] and abs(st["adv_std"] - o["std"]) <= 1e-6 * o["std"]
+    G = res[0][3][:cfg.n_params].astype(np.float64)
+    errs = grad_errors(cfg, G, o["grad"])
+    assert all(v[0] <= 2e-3 and v[1] <= 2e-3 for v in errs.values()), errs
