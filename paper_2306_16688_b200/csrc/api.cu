@@ -533,10 +533,10 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     g.m_tiles = (n + 128 * y.cg_fwd - 1) / (128 * y.cg_fwd); g.n_tiles = y.out / y.bn_fwd; g.k_splits = 1;
     g.kb_total = (y.in + 63) / 64; g.kb_per_split = g.kb_total;
     g.bias = c->params + y.b_off;
-    g.flags = tanh_accurate() ? 1 : 0;
     ProfScope ps(c, s, l == 0 ? "fwd_l1" : "fwd_hidden", 2.0 * n * y.in * y.out,
                  2.0 * n * (y.in + y.out) + 2.0 * y.in * y.out + 4.0 * y.out);
-    if (srl_status st = gemm(y.bn_fwd, false, false, EPI_TANH, y.cg_fwd, ta, tb, to, to, g, sms, s)) return st;
+    if (srl_status st = gemm(y.bn_fwd, false, false, tanh_accurate() ? EPI_TANH_ACC : EPI_TANH, y.cg_fwd,
+                             ta, tb, to, to, g, sms, s)) return st;
   }
   // ---------------- a4: head GEMM + fused PPO loss -> per-sample dlogits G16
   const Lay& hd = c->lay[L];

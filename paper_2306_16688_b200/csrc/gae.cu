@@ -79,7 +79,6 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
   __shared__ float s_a[32][33];
   __shared__ float s_p[32][33];
   __shared__ float s_carry[32];
-  __shared__ double s_mom[32][3];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int b = blockIdx.x * 32 + lane;
   const bool col_ok = b < B;
@@ -143,20 +142,42 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
     carry = s_carry[lane];
   }
   if (!part) return;
-  // thread moments -> warp -> block (fixed order)
+  // moments: shifted sums (n, shift c, S1 = sum(a - c), S2 = sum(a - c)^2) re-centred to a
+  // common shift and added -- no divisions until the block's final (mean, M2)
+  auto recenter = [](double n, double c_from, double& s1, double& s2, double c_to) {
+    const double dd = c_from - c_to;
+    s2 += 2.0 * dd * s1 + n * dd * dd;
+    s1 += n * dd;
+  };
   double n = (double)cnt_all;
-  double mean = n > 0 ? sh + s1 / n : 0.0;
-  double m2 = n > 0 ? fmax(s2 - s1 * s1 / n, 0.0) : 0.0;
-  warp_merge(n, mean, m2);
-  if (lane == 0) { s_mom[w][0] = n; s_mom[w][1] = mean; s_mom[w][2] = m2; }
+  const unsigned valid = __ballot_sync(0xffffffffu, cnt_all > 0);
+  const double cw = __shfl_sync(0xffffffffu, sh, valid ? __ffs(valid) - 1 : 0);
+  recenter(n, sh, s1, s2, cw);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {     // butterfly: both partners form the same sums
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  __shared__ double s_sum[32][4];
+  if (lane == 0) { s_sum[w][0] = n; s_sum[w][1] = cw; s_sum[w][2] = s1; s_sum[w][3] = s2; }
   __syncthreads();
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
-    double N = 0, M = 0, Q = 0;
-    for (int k = 0; k < W; ++k) chan_merge(N, M, Q, s_mom[k][0], s_mom[k][1], s_mom[k][2]);
+    double N = 0, C = 0, S1 = 0, S2 = 0;
+    bool have = false;
+    for (int k = 0; k < W; ++k) {          // warp order
+      if (s_sum[k][0] == 0.0) continue;
+      double a1 = s_sum[k][2], a2 = s_sum[k][3];
+      if (!have) { C = s_sum[k][1]; have = true; }
+      recenter(s_sum[k][0], s_sum[k][1], a1, a2, C);
+      N += s_sum[k][0];
+      S1 += a1;
+      S2 += a2;
+    }
     part[blockIdx.x * 3 + 0] = N;
-    part[blockIdx.x * 3 + 1] = M;
-    part[blockIdx.x * 3 + 2] = Q;
+    part[blockIdx.x * 3 + 1] = N > 0 ? C + S1 / N : 0.0;
+    part[blockIdx.x * 3 + 2] = N > 0 ? fmax(S2 - S1 * S1 / N, 0.0) : 0.0;
     if (counter) {   // the last block to finish merges every block's triple (fixed order)
       __threadfence();
       s_last = atomicAdd(counter, 1u) == gridDim.x - 1;

@@ -30,7 +30,7 @@
 
 namespace srl {
 
-enum { EPI_TANH = 0, EPI_DTANH = 1, EPI_PART = 2, EPI_LOSS = 3 };
+enum { EPI_TANH = 0, EPI_DTANH = 1, EPI_PART = 2, EPI_LOSS = 3, EPI_TANH_ACC = 4 };
 
 constexpr int kMaxHeads = 8;
 constexpr int kHeadCols = 64;   // padded head width G (logits + value + zero pad)
@@ -51,7 +51,6 @@ struct GemmArgs {
   int n_heads, A;
   int head_size[kMaxHeads];
   float clip_eps, value_coef, entropy_coef, adv_eps;
-  int flags;                                      // bit 0: accurate tanh (TANH epilogue)
 };
 
 // Shared-memory layout (identical on host and device):
@@ -287,11 +286,14 @@ struct OutStage {
 };
 
 // ---------------------------------------------------------------------------------------
-template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+template <int BN, bool A_MN, bool B_MN, int EPI_KIND, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmY,
                const GemmArgs args) {
+  // EPI_TANH_ACC: the TANH epilogue with the accurate rational tanh (SRL_TANH=accurate)
+  constexpr int EPI = EPI_KIND == EPI_TANH_ACC ? EPI_TANH : EPI_KIND;
+  constexpr bool ACC_TANH = EPI_KIND == EPI_TANH_ACC;
   using Cfg = GemmCfg<BN, CG>;
   static_assert(EPI != EPI_LOSS || BN == kHeadCols, "loss epilogue works on the 64-col head");
   static_assert(CG == 1 || (BN / CG) % 64 == 0 || !B_MN, "MN-major B halves must be 64-wide");
@@ -476,7 +478,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 bb = b4[q];
-            if (args.flags & 1) {
+            if constexpr (ACC_TANH) {
               v[4 * q + 0] = tanh_fast_accurate(v[4 * q + 0] + bb.x);
               v[4 * q + 1] = tanh_fast_accurate(v[4 * q + 1] + bb.y);
               v[4 * q + 2] = tanh_fast_accurate(v[4 * q + 2] + bb.z);

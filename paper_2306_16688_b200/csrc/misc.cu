@@ -6,6 +6,8 @@
 // over ranks (a6) yields global means (C-A14).
 #include <math.h>
 
+#include <algorithm>
+
 #include "internal.h"
 #include "srl.h"
 
@@ -43,10 +45,14 @@ __global__ void __launch_bounds__(256) finalize_w_kernel(const SegTable t, int64
     if ((s.ld_part & 3) == 0 && pc + 4 <= prow_len) {
       const float4* s4 = reinterpret_cast<const float4*>(src);
       const int64_t st4 = s.split_stride / 4;
-#pragma unroll 8
-      for (int sp = 0; sp < s.splits; ++sp) {
-        const float4 x = __ldg(s4 + sp * st4);
-        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+      for (int k0 = 0; k0 < s.splits; k0 += 16) {   // 16 loads in flight, summed in split order
+        float4 x[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (k0 + j < s.splits) x[j] = __ldg(s4 + (int64_t)(k0 + j) * st4);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (k0 + j < s.splits) { a[0] += x[j].x; a[1] += x[j].y; a[2] += x[j].z; a[3] += x[j].w; }
       }
     } else {
       const int cnt = min(4, prow_len - pc);
@@ -167,15 +173,20 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
   griddep_wait();
   griddep_launch();
   if (g[P + 5] > 0.f) return;
+  const Segment& s = t.s[blockIdx.y];            // one segment per grid row
+  const int cnt = s.rows * s.cols;
+  const int nq = (cnt + 3) >> 2;
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
   const double step = (double)(t_dev[0] + 1);
   const float bc1 = (float)(1.0 - pow((double)b1, step));
   const float bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, step));
   const float step_size = lr / bc1;
-  const int64_t nq = (P + 3) / 4;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i0 = 4 * q;
-    if (i0 + 4 <= P) {
+  const bool vec_w16 = !s.is_bias && (s.cols & 3) == 0 && (s.w16_ld & 3) == 0;
+  for (; q < nq; q += gridDim.x * blockDim.x) {
+    const int e0 = 4 * q;
+    const int64_t i0 = s.off + e0;
+    if (e0 + 4 <= cnt) {
       float4 pp = *reinterpret_cast<const float4*>(p + i0);
       float4 mm = *reinterpret_cast<const float4*>(m + i0);
       float4 vv = *reinterpret_cast<const float4*>(v + i0);
@@ -187,35 +198,29 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
       *reinterpret_cast<float4*>(p + i0) = pp;
       *reinterpret_cast<float4*>(m + i0) = mm;
       *reinterpret_cast<float4*>(v + i0) = vv;
-      const float pv[4] = {pp.x, pp.y, pp.z, pp.w};
-      const Segment& s = t.s[find_seg(t, i0)];
-      if (!s.is_bias) {
-        const int64_t idx = i0 - s.off;
-        const int r = (int)(idx / s.cols), c = (int)(idx % s.cols);
-        if ((s.cols & 3) == 0 && (s.w16_ld & 3) == 0) {          // 4 entries of one row
-          __half2 h0 = __floats2half2_rn(pv[0], pv[1]), h1 = __floats2half2_rn(pv[2], pv[3]);
-          uint2 u;
-          u.x = *reinterpret_cast<uint32_t*>(&h0);
-          u.y = *reinterpret_cast<uint32_t*>(&h1);
-          *reinterpret_cast<uint2*>(s.w16 + (int64_t)r * s.w16_ld + c) = u;
-        } else {
-          for (int e = 0; e < 4; ++e) {
-            const Segment& se = t.s[find_seg(t, i0 + e)];
-            if (se.is_bias) continue;
-            const int64_t ix = i0 + e - se.off;
-            se.w16[(ix / se.cols) * se.w16_ld + ix % se.cols] = __float2half_rn(pv[e]);
-          }
+      if (vec_w16) {                              // 4 entries of one row of the fp16 shadow
+        const int r = e0 / s.cols, c = e0 - r * s.cols;
+        __half2 h0 = __floats2half2_rn(pp.x, pp.y), h1 = __floats2half2_rn(pp.z, pp.w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&h0);
+        u.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(s.w16 + (int64_t)r * s.w16_ld + c) = u;
+      } else if (!s.is_bias) {
+        const float pv[4] = {pp.x, pp.y, pp.z, pp.w};
+        for (int e = 0; e < 4; ++e) {
+          const int r = (e0 + e) / s.cols, c = (e0 + e) - r * s.cols;
+          s.w16[(int64_t)r * s.w16_ld + c] = __float2half_rn(pv[e]);
         }
       }
     } else {
-      for (int64_t i = i0; i < P; ++i) {
+      for (int e = e0; e < cnt; ++e) {
+        const int64_t i = s.off + e;
         float pi = p[i], mi = m[i], vi = v[i];
         adam_one(pi, mi, vi, g[i], b1, b2, step_size, bc2_sqrt, eps);
         p[i] = pi; m[i] = mi; v[i] = vi;
-        const Segment& se = t.s[find_seg(t, i)];
-        if (!se.is_bias) {
-          const int64_t ix = i - se.off;
-          se.w16[(ix / se.cols) * se.w16_ld + ix % se.cols] = __float2half_rn(pi);
+        if (!s.is_bias) {
+          const int r = e / s.cols, c = e - r * s.cols;
+          s.w16[(int64_t)r * s.w16_ld + c] = __float2half_rn(pi);
         }
       }
     }
@@ -225,10 +230,12 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
 cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float* v,
                         const float* bucket, const int64_t* t_dev, float lr, float b1, float b2,
                         float eps, cudaStream_t s) {
-  int64_t blocks = ((P + 3) / 4 + 255) / 256;
-  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
-  return launch_k(adam_kernel, dim3((unsigned)blocks), dim3(256), 0, s, 1, t, P, p, m, v, bucket,
-                  t_dev, lr, b1, b2, eps);
+  int64_t maxq = 1;
+  for (int i = 0; i < t.n; ++i) maxq = std::max<int64_t>(maxq, ((int64_t)t.s[i].rows * t.s[i].cols + 3) / 4);
+  int64_t bx = (maxq + 255) / 256;
+  if (bx > 4 * num_sms()) bx = 4 * num_sms();
+  return launch_k(adam_kernel, dim3((unsigned)bx, (unsigned)t.n), dim3(256), 0, s, 1, t, P, p, m,
+                  v, bucket, t_dev, lr, b1, b2, eps);
 }
 
 __global__ void shadow_kernel(const SegTable t, const float* __restrict__ p) {

@@ -44,9 +44,10 @@ template <int BN, bool AM, bool BM, int EPI, int CG>
 static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                               const CUtensorMap& ty, GemmArgs a, int grid, cudaStream_t s) {
   auto kern = gemm_tc_kernel<BN, AM, BM, EPI, CG>;
-  if (a.stages <= 0) a.stages = gemm_stages(BN, EPI, a.colsum_ld, CG);
+  constexpr int E = EPI == EPI_TANH_ACC ? EPI_TANH : EPI;   // same smem layout
+  if (a.stages <= 0) a.stages = gemm_stages(BN, E, a.colsum_ld, CG);
   if (a.stages < 2) return cudaErrorInvalidConfiguration;
-  const size_t smem = 1024 + smem_layout(BN, EPI, a.stages, a.colsum_ld, CG).total;
+  const size_t smem = 1024 + smem_layout(BN, E, a.stages, a.colsum_ld, CG).total;
   if (smem + 512 > kSmemLimit) return cudaErrorInvalidConfiguration;
   static size_t configured = 0;
   if (smem > configured) {
@@ -78,6 +79,9 @@ cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUt
   switch (epi) {
     case EPI_TANH:
       if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_TANH, cg) }
+      break;
+    case EPI_TANH_ACC:
+      if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_TANH_ACC, cg) }
       break;
     case EPI_DTANH:
       if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_DTANH, cg) }
