@@ -60,9 +60,11 @@ struct SmemLayout {
 };
 constexpr int kZPitch = 33;                       // loss row buffer [64 cols][33] per warp
 constexpr int kStageTile = 32 * 32 * 2;           // one 32x32 fp16 staging tile
+constexpr int kYSlots = 2;                        // y_prev ring per warp (1 chunk in flight)
+constexpr int kOutSlots = 4;                      // output staging tiles per warp
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr int kBarBytes = 512;
+constexpr int kBarBytes = 640;                    // 64 mbarriers + TMEM slot
 constexpr uint32_t kSmemLimit = 232448;           // 227 KB per CTA
 
 __host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, int colsum_ld,
@@ -71,9 +73,9 @@ __host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, i
   const uint32_t stage_bytes = (uint32_t)(128 + bn / cg) * 64 * 2;
   L.ring = 0;
   L.ostage = stages * stage_bytes;
-  const uint32_t ost = (epi == EPI_PART) ? 0 : kEpiWarps * 2 * kStageTile;
+  const uint32_t ost = (epi == EPI_PART) ? 0 : kEpiWarps * kOutSlots * kStageTile;
   L.ystage = L.ostage + ost;
-  const uint32_t yst = (epi == EPI_DTANH) ? kEpiWarps * 2 * kStageTile : 0;
+  const uint32_t yst = (epi == EPI_DTANH) ? kEpiWarps * kYSlots * kStageTile : 0;
   L.colsum = L.ystage + yst;
   const uint32_t cs = (epi == EPI_DTANH || epi == EPI_LOSS) ? kEpiWarps * colsum_ld * 4 : 0;
   L.bias = L.colsum + cs;
@@ -264,13 +266,15 @@ __device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, cons
   st[4] += lp_old - logpi;
 }
 
-// Per-warp output staging: two 32x32 tiles, recycled once the TMA store has read them.
+// Per-warp output staging: kOutSlots 32x32 tiles, a tile is reused once the TMA store issued
+// kOutSlots tiles ago has read it (the TMA unit also serves the operand loads, so stores can
+// queue for a while).
 struct OutStage {
-  uint8_t* buf;       // 2 x kStageTile, 1024-aligned
+  uint8_t* buf;       // kOutSlots x kStageTile, 1024-aligned
   int k;              // tiles issued so far
   __device__ __forceinline__ uint8_t* acquire() {
-    uint8_t* t = buf + (k & 1) * kStageTile;
-    if (k >= 2 && lane_id() == 0) bulk_wait_read<1>();   // the store 2 tiles ago has read t
+    uint8_t* t = buf + (k % kOutSlots) * kStageTile;
+    if (k >= kOutSlots && lane_id() == 0) bulk_wait_read<kOutSlots - 1>();
     __syncwarp();
     return t;
   }
@@ -294,6 +298,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   // EPI_TANH_ACC: the TANH epilogue with the accurate rational tanh (SRL_TANH=accurate)
   constexpr int EPI = EPI_KIND == EPI_TANH_ACC ? EPI_TANH : EPI_KIND;
   constexpr bool ACC_TANH = EPI_KIND == EPI_TANH_ACC;
+  // SPLIT: both epilogue warpgroups drain every tile, each half of its 32-column chunks, which
+  // halves the per-tile epilogue latency the MMA waits on (only 512/BN accumulators exist).
+  // The loss epilogue needs whole rows: its groups take alternate tiles instead.
+  constexpr bool SPLIT = EPI != EPI_LOSS && BN >= 64;
+  constexpr int NCH_ALL = BN / 32;
+  constexpr int NCH = SPLIT ? NCH_ALL / 2 : NCH_ALL;     // chunks per warp per tile
   using Cfg = GemmCfg<BN, CG>;
   static_assert(EPI != EPI_LOSS || BN == kHeadCols, "loss epilogue works on the 64-col head");
   static_assert(CG == 1 || (BN / CG) % 64 == 0 || !B_MN, "MN-major B halves must be 64-wide");
@@ -309,8 +319,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t* empty = full + 8;
   uint64_t* tfull = empty + 8;
   uint64_t* tempty = tfull + 8;
-  uint64_t* ybar = tempty + 8;                    // [8 warps][2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ybar + 16);
+  uint64_t* ybar = tempty + 8;                    // [8 warps][kYSlots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ybar + kEpiWarps * kYSlots);
   float* colsum_s = reinterpret_cast<float*>(smem + SL.colsum);
   float* bias_s = reinterpret_cast<float*>(smem + SL.bias);
 
@@ -327,9 +337,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int s = 0; s < Cfg::ACC_STAGES; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4 * CG);     // every epilogue warp of the group, in both CTAs
+      mbar_init(&tempty[s], (SPLIT ? 8 : 4) * CG);   // every epilogue warp on the tile, both CTAs
     }
-    for (int s = 0; s < 16; ++s) mbar_init(&ybar[s], 1);
+    for (int s = 0; s < kEpiWarps * kYSlots; ++s) mbar_init(&ybar[s], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_cg<CG>(tmem_slot, Cfg::TMEM_COLS);
@@ -424,10 +434,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int grp = ew >> 2;                 // warpgroup
     const int quad = warp & 3;               // TMEM lane quadrant = 32-row slice of the tile
     float* my_colsum = colsum_s + ew * args.colsum_ld;
-    OutStage ost{smem + SL.ostage + ew * 2 * kStageTile, 0};
-    uint8_t* ystage = smem + SL.ystage + ew * 2 * kStageTile;
-    uint64_t* my_ybar = ybar + 2 * ew;
-    uint32_t yph0 = 0, yph1 = 0;
+    OutStage ost{smem + SL.ostage + ew * kOutSlots * kStageTile, 0};
+    uint8_t* ystage = smem + SL.ystage + ew * kYSlots * kStageTile;
+    uint64_t* my_ybar = ybar + kYSlots * ew;
+    uint32_t yph = 0;                        // phase bit per y slot
+    int yslot = 0;                           // next slot to fill (ring over tiles)
     if (EPI == EPI_DTANH || EPI == EPI_LOSS) {
       for (int i = lane; i < args.colsum_ld; i += 32) my_colsum[i] = 0.f;
       __syncwarp();
@@ -441,7 +452,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     double st[5] = {0, 0, 0, 0, 0};
     int it = 0;
     for (int u = cid; u < units; u += ncl, ++it) {
-      if ((it & 1) != grp) continue;
+      if (!SPLIT && (it & 1) != grp) continue;
       const int acc = it % Cfg::ACC_STAGES;
       const uint32_t acc_phase = (uint32_t)(it / Cfg::ACC_STAGES) & 1u;
       const int nt = u % args.n_tiles;
@@ -449,30 +460,41 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int ks = u / (args.n_tiles * args.m_tiles);
       const int row0 = mt * 128 * CG + rank * 128 + quad * 32;   // first row of this warp's slice
       const int row = row0 + (int)lane;
-      const int n0 = nt * BN;
+      const int n0 = nt * BN + (SPLIT ? grp * NCH * 32 : 0);   // this warp's first column
       const bool rvalid = row < args.M;
+      int ybase = 0;
       if constexpr (EPI == EPI_DTANH) {
-        // first y_prev chunk of this tile (TMA; rows past M read as zero)
+        // the first kYSlots-1 y_prev chunks of this tile, before waiting for the accumulator
+        // (TMA; rows past M read as zero).  Slots were released by __syncwarp after their reads.
+        ybase = yslot;
         if (lane == 0) {
           fence_proxy_async_smem();
-          mbar_expect_tx(&my_ybar[0], kStageTile);
-          tma_load_2d(ystage, &tmY, &my_ybar[0], n0, row0);
+#pragma unroll
+          for (int c = 0; c < kYSlots - 1; ++c) {
+            if (c < NCH) {
+              const int sl = (ybase + c) % kYSlots;
+              mbar_expect_tx(&my_ybar[sl], kStageTile);
+              tma_load_2d(ystage + sl * kStageTile, &tmY, &my_ybar[sl], n0 + c * 32, row0);
+            }
+          }
         }
+        yslot = (ybase + NCH) % kYSlots;
       }
       wait_bounded(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN +
+                             (SPLIT ? grp * NCH * 32 : 0);
 
       if constexpr (EPI == EPI_TANH) {
         float nxt[32];
         tmem_ld32(taddr, nxt);
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < NCH; ++c) {
           float v[32];
           tc_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = nxt[j];
-          if (c + 1 < BN / 32) tmem_ld32(taddr + (c + 1) * 32, nxt);   // overlap next TMEM read
+          if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, nxt);   // overlap next TMEM read
           const int col0 = n0 + c * 32;
           const float4* b4 = reinterpret_cast<const float4*>(bias_s + col0);
 #pragma unroll
@@ -490,29 +512,32 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               v[4 * q + 3] = tanh_mufu(v[4 * q + 3] + bb.w);
             }
           }
-          uint8_t* t = ost.acquire();
-          stile_write_row(t, (int)lane, v);
-          ost.release(t, &tmO, col0, row0);      // rows >= M are clipped by TMA
+          {
+            uint8_t* t = ost.acquire();
+            stile_write_row(t, (int)lane, v);
+            ost.release(t, &tmO, col0, row0);      // rows >= M are clipped by TMA
+          }
         }
       } else if constexpr (EPI == EPI_DTANH) {
         float nxt[32];
         tmem_ld32(taddr, nxt);
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          const int yb = c & 1;
-          if (c + 1 < BN / 32 && lane == 0) {      // prefetch the next y_prev chunk
+        for (int c = 0; c < NCH; ++c) {
+          const int yb = (ybase + c) % kYSlots;
+          if (c + kYSlots - 1 < NCH && lane == 0) {   // keep kYSlots-1 chunks in flight
+            const int sl = (ybase + c + kYSlots - 1) % kYSlots;
             fence_proxy_async_smem();
-            mbar_expect_tx(&my_ybar[yb ^ 1], kStageTile);
-            tma_load_2d(ystage + (yb ^ 1) * kStageTile, &tmY, &my_ybar[yb ^ 1], n0 + (c + 1) * 32, row0);
+            mbar_expect_tx(&my_ybar[sl], kStageTile);
+            tma_load_2d(ystage + sl * kStageTile, &tmY, &my_ybar[sl], n0 + (c + kYSlots - 1) * 32, row0);
           }
           float v[32];
           tc_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = nxt[j];
-          if (c + 1 < BN / 32) tmem_ld32(taddr + (c + 1) * 32, nxt);
+          if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, nxt);
           const int col0 = n0 + c * 32;
-          if (yb == 0) { wait_bounded(&my_ybar[0], yph0); yph0 ^= 1; }
-          else { wait_bounded(&my_ybar[1], yph1); yph1 ^= 1; }
+          wait_bounded(&my_ybar[yb], (yph >> yb) & 1u);
+          yph ^= 1u << yb;
           float y[32];
           stile_read_row(ystage + yb * kStageTile, (int)lane, y);
           __syncwarp();
@@ -534,7 +559,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
       } else if constexpr (EPI == EPI_PART) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < NCH; ++c) {
           float v[32];
           tmem_ld32(taddr + c * 32, v);
           tc_wait_ld();

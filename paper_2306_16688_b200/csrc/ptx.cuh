@@ -237,6 +237,13 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N, bool a_mn, b
 // ------------------------------------------------------------------ misc
 // MUFU.TANH: one instruction, max relative error 2^-10.99 (~4.9e-4), the same size as the
 // fp16 rounding the activation takes next.
+// two fp16 tanh per MUFU op (input rounded to fp16 first): result already packed for storage
+__device__ __forceinline__ uint32_t tanh_mufu_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  uint32_t x = *reinterpret_cast<uint32_t*>(&h), y;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
 __device__ __forceinline__ float tanh_mufu(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
