@@ -266,18 +266,25 @@ def main_ours(args, world, rank, local):
     prof_ms = max_over_ranks(p_start.elapsed_time(p_end)) / Kp
     recs = ctx.prof_records()
 
-    # ---------------- end to end: host (pinned) inputs copied in, stats copied out, per step
+    # ---------------- end to end: every step's batch goes host (pinned) -> device inside the timed
+    # region through the library's pre-fetch slots (NEXT-1, §4.1): the upload of batch
+    # k+1 on the context's copy stream overlaps the step on batch k; stats are copied back
     Ke = args.e2e_steps or min(K, 100)
-    for _ in range(2):
-        dd = {k: host[k].to(dev, non_blocking=True) for k in keys}
-        step(dd)
+    hb = [host[k] for k in keys]
+    ctx.upload(0, *hb)
+    for j in range(2):
+        ctx.upload((j + 1) % 2, *hb)
+        ctx.train_step_slot(j % 2, N, stats=stats)
         stats_host.copy_(stats, non_blocking=True)
+    ctx.train_step_slot(0, N, stats=stats)          # drain the primed slot
     barrier()
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     x0.record()
-    for _ in range(Ke):
-        dd = {k: host[k].to(dev, non_blocking=True) for k in keys}
-        step(dd)
+    ctx.upload(0, *hb)
+    for j in range(Ke):
+        if j + 1 < Ke:
+            ctx.upload((j + 1) % 2, *hb)
+        ctx.train_step_slot(j % 2, N, stats=stats)
         stats_host.copy_(stats, non_blocking=True)
     x1.record()
     barrier()

@@ -168,6 +168,22 @@ srl_status srl_ppo_train_step(srl_ctx* ctx, int T, int B, int64_t n_global,
                               const uint16_t* obs, const int32_t* actions, const float* logp_old,
                               srl_ppo_stats* stats_out, srl_stream_t stream);
 
+/* NEXT-1: trainer data pre-fetching (§4.1: "we reserve GPU memory for two
+ * batches of training samples ... while the GPU computes the gradient on this sample batch,
+ * another sample batch is pre-fetched into the other memory block").  The context owns two
+ * device batch slots (allocated on first use, sized for max_local_n).
+ *   srl_batch_upload copies one host batch (same layouts as srl_ppo_train_step; pinned host
+ *   memory makes the copies asynchronous) into slot 0 or 1 on the context's own copy stream,
+ *   after the last step that read that slot has finished with it.  It returns immediately.
+ *   srl_ppo_train_step_slot makes `stream` wait for that upload, runs srl_ppo_train_step on the
+ *   slot, and releases the slot for the next upload.
+ * Alternating slots overlaps the H2D copy of batch k+1 with the step on batch k. */
+srl_status srl_batch_upload(srl_ctx* ctx, int slot, int T, int B, const float* rewards,
+                            const float* values, const uint8_t* dones, const uint16_t* obs,
+                            const int32_t* actions, const float* logp_old);
+srl_status srl_ppo_train_step_slot(srl_ctx* ctx, int slot, int64_t n_global,
+                                   srl_ppo_stats* stats_out, srl_stream_t stream);
+
 /* a6: in-place allreduce over the ctx's ranks of a device f32 buffer (SPEC reduce_gradients
  * S:L505-513): op 0 = sum, op 1 = mean.  world == 1: identity (op 1 leaves values as is). */
 srl_status srl_allreduce_grads(srl_ctx* ctx, float* buf, int64_t count, int op,

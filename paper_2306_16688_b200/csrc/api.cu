@@ -141,6 +141,17 @@ struct srl_ctx {
   std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t>, CUtensorMap> tmaps;
   // train-step buffers (srl_ppo_train_step): adv, ret [max_n] f32; gae partials; mean/std
   float *adv = nullptr, *ret = nullptr;
+  // NEXT-1 pre-fetch slots (srl_batch_upload / srl_ppo_train_step_slot)
+  struct Slot {
+    float *rewards = nullptr, *values = nullptr, *logp_old = nullptr;
+    uint8_t* dones = nullptr;
+    __half* obs = nullptr;
+    int32_t* actions = nullptr;
+    int T = 0, B = 0;
+    bool ready = false;
+    cudaEvent_t uploaded = nullptr, released = nullptr;
+  } slot[2];
+  cudaStream_t copy_stream = nullptr;
   double *gae_part = nullptr, *gae_stats = nullptr, *mean_std = nullptr;
   unsigned int* gae_counter = nullptr;
   int gae_part_cap = 0;
@@ -213,6 +224,11 @@ static srl_status dalloc(srl_ctx* c, T** p, size_t bytes) {
 static void free_ctx(srl_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  for (auto& sl : c->slot) {
+    if (sl.uploaded) cudaEventDestroy(sl.uploaded);
+    if (sl.released) cudaEventDestroy(sl.released);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);
@@ -682,6 +698,63 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
   }
   return srl_ppo_step(c, n, n_global, obs, actions, logp_old, c->adv, c->ret, c->mean_std, 1,
                       stats_out, stream);
+}
+
+// ------------------------------------------------------------------ NEXT-1 pre-fetching
+extern "C" srl_status srl_batch_upload(srl_ctx* c, int slot, int T, int B, const float* rewards,
+                                       const float* values, const uint8_t* dones,
+                                       const uint16_t* obs, const int32_t* actions,
+                                       const float* logp_old) {
+  if (!c || slot < 0 || slot > 1) FAIL(SRL_EINVAL, "srl_batch_upload: bad ctx/slot");
+  if (T < 1 || B < 1 || (int64_t)T * B > c->max_n) FAIL(SRL_EINVAL, "srl_batch_upload: need 1 <= T*B <= max_local_n");
+  if (!rewards || !values || !dones || !obs || !actions || !logp_old)
+    FAIL(SRL_EINVAL, "srl_batch_upload: null pointer");
+  CK(cudaSetDevice(c->device));
+  auto& sl = c->slot[slot];
+  const int64_t n = c->max_n;
+  if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!sl.obs) {
+    srl_status st;
+    if ((st = dalloc(c, &sl.rewards, sizeof(float) * n))) return st;
+    if ((st = dalloc(c, &sl.values, sizeof(float) * 2 * n))) return st;   // (T+1)B <= 2TB
+    if ((st = dalloc(c, &sl.dones, n))) return st;
+    if ((st = dalloc(c, &sl.obs, sizeof(__half) * n * c->cfg.ld_obs))) return st;
+    if ((st = dalloc(c, &sl.actions, sizeof(int32_t) * n * c->heads.size()))) return st;
+    if ((st = dalloc(c, &sl.logp_old, sizeof(float) * n))) return st;
+    CK(cudaEventCreateWithFlags(&sl.uploaded, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sl.released, cudaEventDisableTiming));
+    CK(cudaEventRecord(sl.released, c->copy_stream));
+  }
+  const int64_t m = (int64_t)T * B;
+  cudaStream_t cs = c->copy_stream;
+  CK(cudaStreamWaitEvent(cs, sl.released, 0));      // the last step on this slot is done with it
+  CK(cudaMemcpyAsync(sl.rewards, rewards, sizeof(float) * m, cudaMemcpyHostToDevice, cs));
+  CK(cudaMemcpyAsync(sl.values, values, sizeof(float) * (m + B), cudaMemcpyHostToDevice, cs));
+  CK(cudaMemcpyAsync(sl.dones, dones, m, cudaMemcpyHostToDevice, cs));
+  CK(cudaMemcpyAsync(sl.obs, obs, sizeof(__half) * m * c->cfg.ld_obs, cudaMemcpyHostToDevice, cs));
+  CK(cudaMemcpyAsync(sl.actions, actions, sizeof(int32_t) * m * c->heads.size(), cudaMemcpyHostToDevice, cs));
+  CK(cudaMemcpyAsync(sl.logp_old, logp_old, sizeof(float) * m, cudaMemcpyHostToDevice, cs));
+  CK(cudaEventRecord(sl.uploaded, cs));
+  sl.T = T;
+  sl.B = B;
+  sl.ready = true;
+  return SRL_OK;
+}
+
+extern "C" srl_status srl_ppo_train_step_slot(srl_ctx* c, int slot, int64_t n_global,
+                                              srl_ppo_stats* stats_out, srl_stream_t stream) {
+  if (!c || slot < 0 || slot > 1) FAIL(SRL_EINVAL, "srl_ppo_train_step_slot: bad ctx/slot");
+  auto& sl = c->slot[slot];
+  if (!sl.ready) FAIL(SRL_ESTATE, "srl_ppo_train_step_slot: slot has no uploaded batch");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaStreamWaitEvent(s, sl.uploaded, 0));
+  srl_status st = srl_ppo_train_step(c, sl.T, sl.B, n_global, sl.rewards, sl.values, sl.dones,
+                                     reinterpret_cast<const uint16_t*>(sl.obs), sl.actions,
+                                     sl.logp_old, stats_out, stream);
+  CK(cudaEventRecord(sl.released, s));
+  sl.ready = false;
+  return st;
 }
 
 // ------------------------------------------------------------------ profiling

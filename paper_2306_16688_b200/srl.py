@@ -18,7 +18,8 @@ SRL_OK, SRL_EINVAL, SRL_ECUDA, SRL_ENCCL, SRL_ENOMEM, SRL_EUNSUPPORTED, SRL_ESTA
 # every symbol include/srl.h declares (checked by tests/test_abi.py)
 EXPORTS = ("srl_last_error", "srl_abi_version", "srl_gae", "srl_adv_norm", "srl_nccl_unique_id",
            "srl_ppo_create", "srl_ppo_destroy", "srl_ppo_params", "srl_ppo_adam_state",
-           "srl_ppo_load_params", "srl_ppo_step", "srl_ppo_train_step", "srl_allreduce_grads", "srl_prof_enable",
+           "srl_ppo_load_params", "srl_ppo_step", "srl_ppo_train_step", "srl_batch_upload",
+           "srl_ppo_train_step_slot", "srl_allreduce_grads", "srl_prof_enable",
            "srl_prof_reset", "srl_prof_count", "srl_prof_read", "srl_debug_gemm")
 
 
@@ -72,6 +73,8 @@ def lib():
     L.srl_ppo_load_params.argtypes = [vp, vp, vp]
     L.srl_ppo_step.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
     L.srl_ppo_train_step.argtypes = [vp, C.c_int, C.c_int, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.srl_batch_upload.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]
+    L.srl_ppo_train_step_slot.argtypes = [vp, C.c_int, i64, vp, vp]
     L.srl_allreduce_grads.argtypes = [vp, vp, i64, C.c_int, vp]
     L.srl_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
                                  C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
@@ -282,6 +285,22 @@ class PPOContext:
         _check(lib().srl_ppo_train_step(self.handle, T, B, int(n_global), _ptr(rewards),
                                         _ptr(values), _ptr(dones), _ptr(obs), _ptr(actions),
                                         _ptr(logp_old), _ptr(stats), _stream(stream)))
+        return stats
+
+    def upload(self, slot, rewards, values, dones, obs, actions, logp_old):
+        """NEXT-1: async H2D of a host batch (pinned CPU tensors) into device slot 0/1."""
+        for t in (rewards, values, dones, obs, actions, logp_old):
+            if t.is_cuda or not t.is_contiguous():
+                raise SrlError("upload: need contiguous host tensors")
+        T, B = rewards.shape
+        _check(lib().srl_batch_upload(self.handle, slot, T, B, _ptr(rewards), _ptr(values),
+                                      _ptr(dones), _ptr(obs), _ptr(actions), _ptr(logp_old)))
+
+    def train_step_slot(self, slot, n_global, stats=None, stream=None):
+        if stats is None:
+            stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=f"cuda:{self.device}")
+        _check(lib().srl_ppo_train_step_slot(self.handle, slot, int(n_global), _ptr(stats),
+                                             _stream(stream)))
         return stats
 
     def allreduce_grads(self, buf: torch.Tensor, op: int = 0, stream=None):

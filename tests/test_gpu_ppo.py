@@ -155,3 +155,30 @@ def test_train_step_equals_composed_calls(name):
     _check_grads(cfg, G2[:cfg.n_params], o["grad"])
     assert abs(st["adv_mean"] - o["mean"]) <= 1e-6 * o["std"]
     assert abs(st["adv_std"] - o["std"]) <= 1e-6 * o["std"]
+
+
+def test_prefetch_slots_equal_device_path():
+    """NEXT-1 (§4.1): host batches uploaded into alternating device slots on the
+    context's copy stream give bit-identical results to steps on device-resident inputs."""
+    import paper_2306_16688_b200 as P
+    cfg = synth.get_config("gfootball").with_(B=16)
+    params, b = make_inputs(cfg, seed=8)
+    keys = ("rewards", "values", "dones", "obs", "actions", "logp_old")
+    host = [torch.from_numpy(np.ascontiguousarray(b[k])).pin_memory() for k in keys]
+    dev = [h.cuda() for h in host]
+    spec = P.NetSpec.from_config(cfg)
+    a = P.PPOContext(spec, max_local_n=b["n"])
+    c = P.PPOContext(spec, max_local_n=b["n"])
+    for ctx in (a, c):
+        ctx.load_params(torch.from_numpy(params).cuda())
+    c.upload(0, *host)
+    for k in range(3):
+        a.train_step(b["n"], *dev)
+        if k + 1 < 3:
+            c.upload((k + 1) % 2, *host)
+        st = P.decode_stats(c.train_step_slot(k % 2, b["n"]))
+    torch.cuda.synchronize()
+    assert st["step"] == 3
+    assert torch.equal(a.params(), c.params()) and torch.equal(a.grads(), c.grads())
+    with pytest.raises(P.SrlError):
+        c.train_step_slot(0, b["n"])          # consumed: nothing uploaded into slot 0 since
