@@ -19,6 +19,12 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
 // SRL_TANH=accurate: rational tanh (rel. err ~2e-7) instead of MUFU.TANH (~5e-4)
+static bool ar_overlap() {
+  static int on = -1;
+  if (on < 0) { const char* e = getenv("SRL_AR_OVERLAP"); on = (e && e[0] == '1') ? 1 : 0; }
+  return on == 1;
+}
+
 static bool tanh_accurate() {
   static int on = -1;
   if (on < 0) {
@@ -152,6 +158,10 @@ struct srl_ctx {
     cudaEvent_t uploaded = nullptr, released = nullptr;
   } slot[2];
   cudaStream_t copy_stream = nullptr;
+  // a6 overlap (world > 1): bucket allreduce of the upper layers runs on comm_stream while the
+  // rest of the backward computes
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_early = nullptr, ev_late = nullptr, ev_comm = nullptr;
   double *gae_part = nullptr, *gae_stats = nullptr, *mean_std = nullptr;
   unsigned int* gae_counter = nullptr;
   int gae_part_cap = 0;
@@ -229,6 +239,9 @@ static void free_ctx(srl_ctx* c) {
     if (sl.released) cudaEventDestroy(sl.released);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  for (cudaEvent_t e : {c->ev_early, c->ev_late, c->ev_comm})
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);
@@ -380,6 +393,16 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if ((st = dalloc(c, &c->G16, sizeof(__half) * (size_t)n * kHeadCols))) return bail(st);
   for (int k = 0; k < 2; ++k)
     if ((st = dalloc(c, &c->dZ[k], sizeof(__half) * (size_t)n * max_h))) return bail(st);
+  if (world > 1) {
+    if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_early, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_late, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) != cudaSuccess) {
+      set_error("srl_ppo_create: stream/event creation failed");
+      free_ctx(c);
+      return SRL_ECUDA;
+    }
+  }
   if ((st = dalloc(c, &c->adv, sizeof(float) * n))) return bail(st);
   if ((st = dalloc(c, &c->ret, sizeof(float) * n))) return bail(st);
   c->gae_part_cap = (int)((n + 31) / 32) + 1;
@@ -629,7 +652,36 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     colsum_parts[l - 1] = grid;
     return st;
   };
+  // finalise (1/N-scaled split/column-sum reduction into the bucket) layers [lo, hi]
+  auto finalize_layers = [&](int lo, int hi) -> srl_status {
+    SegTable all = make_segs(c, splits, colsum_parts), t{};
+    double rd = 0;
+    for (int l = lo; l <= hi; ++l) {
+      t.s[t.n++] = all.s[2 * l];
+      t.s[t.n++] = all.s[2 * l + 1];
+      rd += 4.0 * splits[l] * c->lay[l].out * c->lay[l].in + 4.0 * colsum_parts[l] * c->lay[l].colsum_ld;
+    }
+    ProfScope ps(c, s, "grad_finalize", 0.0, rd);
+    CK(launch_finalize_grads(t, c->P, inv_n, c->grads, c->counters, s));
+    return SRL_OK;
+  };
+  // a6 overlap: once dW of layer 1 is done, layers 1..L (a contiguous bucket tail) are final;
+  // their allreduce runs on comm_stream during layer 0's dX/dW.
+  // Opt-in (SRL_AR_OVERLAP=1): measured slower on 2-4 B200 for the Atari-shaped step, because
+  // NCCL's kernel takes SMs from the persistent one-CTA-per-SM GEMMs running beside it.
+  const bool overlap = apply && c->world > 1 && ar_overlap();
+  const int64_t split_off = c->lay[1].w_off;          // bucket [split_off, P) = layers 1..L
+  auto early_reduce = [&]() -> srl_status {
+    if (srl_status st = finalize_layers(1, L)) return st;
+    CK(cudaEventRecord(c->ev_early, s));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_early, 0));
+    ProfScope ps(c, c->comm_stream, "allreduce", 0.0, 4.0 * (c->P - split_off));
+    CKN(ncclAllReduce(c->grads + split_off, c->grads + split_off, (size_t)(c->P - split_off),
+                      ncclFloat, ncclSum, c->comm, c->comm_stream));
+    return SRL_OK;
+  };
   if (srl_status st = dW(L, c->Y[L - 1], hd.in, c->G16, kHeadCols)) return st;
+  if (overlap && L == 1) if (srl_status st = early_reduce()) return st;
   int cur = 0;
   if (srl_status st = dX(L, c->G16, kHeadCols, c->dZ[cur])) return st;
   for (int l = L - 1; l >= 0; --l) {
@@ -637,23 +689,32 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     const __half* Xl = l == 0 ? X0 : c->Y[l - 1];
     const int ldx = l == 0 ? ld_obs : y.in;
     if (srl_status st = dW(l, c->dZ[cur], y.out, Xl, ldx)) return st;
+    if (overlap && l == 1) if (srl_status st = early_reduce()) return st;
     if (l > 0) {
       if (srl_status st = dX(l, c->dZ[cur], y.out, c->dZ[cur ^ 1])) return st;
       cur ^= 1;
     }
   }
   SegTable segs = make_segs(c, splits, colsum_parts);
-  {
-    double rd = 0;
-    for (int l = 0; l <= L; ++l) rd += 4.0 * splits[l] * c->lay[l].out * c->lay[l].in +
-                                       4.0 * colsum_parts[l] * c->lay[l].colsum_ld;
-    ProfScope ps(c, s, "grad_finalize", 0.0, rd + 4.0 * c->P);
-    CK(launch_finalize_grads(segs, c->P, inv_n, c->grads, c->counters, s));
-    CK(launch_extras(c->P, inv_n, c->stats_part, grid_loss, c->counters, c->grads, s));
-  }
+  if (srl_status st = overlap ? finalize_layers(0, 0) : finalize_layers(0, L)) return st;
+  CK(launch_extras(c->P, inv_n, c->stats_part, grid_loss, c->counters, c->grads, s));
   if (apply) {
     // ---------------- a6: gradient allreduce (bucket already scaled by 1/N_global)
-    if (c->world > 1) {
+    if (overlap) {
+      // layer 0 + the 8 statistics, on the same comm stream (NCCL calls stay in one order)
+      CK(cudaEventRecord(c->ev_late, s));
+      CK(cudaStreamWaitEvent(c->comm_stream, c->ev_late, 0));
+      {
+        ProfScope ps(c, c->comm_stream, "allreduce", 0.0, 4.0 * (split_off + 8));
+        CKN(ncclGroupStart());
+        CKN(ncclAllReduce(c->grads, c->grads, (size_t)split_off, ncclFloat, ncclSum, c->comm, c->comm_stream));
+        CKN(ncclAllReduce(c->grads + c->P, c->grads + c->P, 8, ncclFloat, ncclSum, c->comm, c->comm_stream));
+        CKN(ncclGroupEnd());
+      }
+      CK(cudaEventRecord(c->ev_comm, c->comm_stream));
+      CK(cudaStreamWaitEvent(s, c->ev_comm, 0));
+    }
+    else if (c->world > 1) {
       ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8));
       CKN(ncclAllReduce(c->grads, c->grads, (size_t)(c->P + 8), ncclFloat, ncclSum, c->comm, s));
     }
