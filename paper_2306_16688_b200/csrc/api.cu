@@ -405,7 +405,7 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   }
   if ((st = dalloc(c, &c->adv, sizeof(float) * n))) return bail(st);
   if ((st = dalloc(c, &c->ret, sizeof(float) * n))) return bail(st);
-  c->gae_part_cap = (int)((n + 31) / 32) + 1;
+  c->gae_part_cap = (int)((n + 7) / 8) + 1;   // >= gae_num_blocks(B) for any B <= n
   if ((st = dalloc(c, &c->gae_part, sizeof(double) * 3 * c->gae_part_cap))) return bail(st);
   if ((st = dalloc(c, &c->gae_stats, sizeof(double) * 4))) return bail(st);
   if ((st = dalloc(c, &c->mean_std, sizeof(double) * 2))) return bail(st);

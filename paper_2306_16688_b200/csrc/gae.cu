@@ -68,7 +68,7 @@ __device__ void warp0_merge_parts(const double* part, int count, double* out, do
   }
 }
 
-template <int TC>
+template <int TC, int CB>
 __global__ void __launch_bounds__(TC <= 8 ? 1024 : 512)
 gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __restrict__ v,
            const uint8_t* __restrict__ d, float gamma, float gl, float* __restrict__ adv,
@@ -76,13 +76,19 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
            double* stats_out, double* mean_std_out, int unbiased) {
   griddep_wait();
   griddep_launch();
-  __shared__ float s_a[32][33];
-  __shared__ float s_p[32][33];
-  __shared__ float s_carry[32];
+  // A block owns CB consecutive columns; a warp covers CB columns x (32 / CB) row chunks, so
+  // small-B batches still spread over many SMs (CB = 8: 32-byte row segments per chunk).
+  constexpr int SUB = 32 / CB;
+  __shared__ float s_a[32 * SUB][CB + 1];
+  __shared__ float s_p[32 * SUB][CB + 1];
+  __shared__ float s_carry[CB];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
-  const int b = blockIdx.x * 32 + lane;
+  const int col = lane % CB;
+  const int ch = w * SUB + lane / CB;      // my row chunk inside a super-chunk
+  const int NCHK = W * SUB;
+  const int b = blockIdx.x * CB + col;
   const bool col_ok = b < B;
-  const int SC = W * TC;
+  const int SC = NCHK * TC;
   const int nsc = (T + SC - 1) / SC;
   float carry = 0.f;                       // A at the first row after this super-chunk
   double sh = 0.0, s1 = 0.0, s2 = 0.0;     // shifted sums of my adv values
@@ -90,7 +96,7 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
   bool have_shift = false;
 
   for (int sc = nsc - 1; sc >= 0; --sc) {
-    const int t0 = sc * SC + w * TC;
+    const int t0 = sc * SC + ch * TC;
     float delta[TC], c[TC], vt[TC];
 #pragma unroll
     for (int i = 0; i < TC; ++i) {
@@ -116,11 +122,11 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
       a = delta[i] + c[i] * a;
       P *= c[i];
     }
-    s_a[w][lane] = a;
-    s_p[w][lane] = P;
+    s_a[ch][col] = a;
+    s_p[ch][col] = P;
     __syncthreads();
     float Ain = carry;
-    for (int w2 = W - 1; w2 > w; --w2) Ain = s_a[w2][lane] + s_p[w2][lane] * Ain;
+    for (int c2 = NCHK - 1; c2 > ch; --c2) Ain = s_a[c2][col] + s_p[c2][col] * Ain;
     // pass 2: exact recurrence from the true A_end
     a = Ain;
 #pragma unroll
@@ -137,9 +143,9 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
         ++cnt_all;
       }
     }
-    if (w == 0) s_carry[lane] = a;         // A at row sc*SC
+    if (ch == 0) s_carry[col] = a;         // A at row sc*SC
     __syncthreads();
-    carry = s_carry[lane];
+    carry = s_carry[col];
   }
   if (!part) return;
   // moments: shifted sums (n, shift c, S1 = sum(a - c), S2 = sum(a - c)^2) re-centred to a
@@ -191,24 +197,45 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
   if (threadIdx.x == 0) *counter = 0;   // ready for the next launch
 }
 
-int gae_num_blocks(int B) { return (B + 31) / 32; }
+// columns per block: enough blocks for the 148 SMs when B is small
+static int gae_cols_per_block(int B) { return B >= 32 * 148 ? 32 : (B >= 16 * 148 ? 16 : 8); }
+int gae_num_blocks(int B) {
+  const int cb = gae_cols_per_block(B);
+  return (B + cb - 1) / cb;
+}
+
+template <int TC, int CB>
+static cudaError_t launch_gae_t(int T, int B, int ld, const float* r, const float* v,
+                                const uint8_t* d, float gamma, float gl, float* adv, float* ret,
+                                double* part, cudaStream_t s, unsigned int* counter,
+                                double* stats_out, double* mean_std_out, int unbiased) {
+  constexpr int SUB = 32 / CB;
+  const int maxw = TC <= 8 ? 32 : 16;
+  const int chunks = (T + TC - 1) / TC;
+  const int W = std::max(1, std::min(maxw, (chunks + SUB - 1) / SUB));
+  return launch_k(gae_kernel<TC, CB>, dim3(gae_num_blocks(B)), dim3(32 * W), 0, s, 1, T, B, ld, r,
+                  v, d, gamma, gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased);
+}
 
 cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
                        float gamma, float lambda, float* adv, float* ret, double* part,
                        cudaStream_t s, unsigned int* counter, double* stats_out,
                        double* mean_std_out, int unbiased) {
-  const int blocks = gae_num_blocks(B);
   const float gl = gamma * lambda;
-  if (T <= 32 * 8) {            // <= 32 warps of 8 rows, one pass
-    const int W = (T + 7) / 8;
-    return launch_k(gae_kernel<8>, dim3(blocks), dim3(32 * W), 0, s, 1, T, B, ld, r, v, d, gamma,
-                    gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased);
-  } else {                       // <= 16 warps of 16 rows per super-chunk of 256 rows
-    const int W = std::min(16, (T + 15) / 16);
-    return launch_k(gae_kernel<16>, dim3(blocks), dim3(32 * W), 0, s, 1, T, B, ld, r, v, d, gamma,
-                    gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased);
+  const int cb = gae_cols_per_block(B);
+  const bool short_t = T <= 32 * 8;        // one super-chunk of 8-row chunks
+#define SRL_GAE(TC, CB) \
+  return launch_gae_t<TC, CB>(T, B, ld, r, v, d, gamma, gl, adv, ret, part, s, counter, stats_out, mean_std_out, unbiased)
+  if (short_t) {
+    if (cb == 8) SRL_GAE(8, 8);
+    if (cb == 16) SRL_GAE(8, 16);
+    SRL_GAE(8, 32);
+  } else {
+    if (cb == 8) SRL_GAE(16, 8);
+    if (cb == 16) SRL_GAE(16, 16);
+    SRL_GAE(16, 32);
   }
-  return cudaGetLastError();
+#undef SRL_GAE
 }
 
 // ---------------------------------------------------------------- a2: moments of a vector
