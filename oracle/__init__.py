@@ -46,7 +46,9 @@ def lib():
         _lib.oracle_forward.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, d]
         _lib.oracle_loss_and_grad.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, i32,
                                               d, d, d, C.c_double, C.c_double, C.c_double,
-                                              C.c_double, d, d, d]
+                                              C.c_double, d, d, d, d, C.c_double]
+        _lib.oracle_clip_grad_norm.argtypes = [i64, d, C.c_double]
+        _lib.oracle_clip_grad_norm.restype = C.c_double
         _lib.oracle_adam.argtypes = [i64, d, d, d, d, i64, C.c_double, C.c_double, C.c_double,
                                      C.c_double]
     return _lib
@@ -110,7 +112,7 @@ def forward(obs_dim, hidden, heads, params, obs):
 
 def loss_and_grad(obs_dim, hidden, heads, params, obs, actions, logp_old, adv_hat, ret,
                   clip_eps=0.2, value_coef=0.5, entropy_coef=0.01, grad_scale=None,
-                  grad=None, sums=None, want_per_sample=False):
+                  grad=None, sums=None, want_per_sample=False, v_old=None, value_clip=0.0):
     p = np.ascontiguousarray(params, dtype=np.float64)
     x = np.ascontiguousarray(np.asarray(obs, dtype=np.float64)[:, :obs_dim])
     n = x.shape[0]
@@ -125,13 +127,22 @@ def loss_and_grad(obs_dim, hidden, heads, params, obs, actions, logp_old, adv_ha
     if grad_scale is None:
         grad_scale = 1.0 / n
     ps = np.empty(n, np.float64) if want_per_sample else None
+    vo = None if v_old is None else np.ascontiguousarray(v_old, dtype=np.float64).reshape(-1)
     lib().oracle_loss_and_grad(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads),
                                _p(p, C.c_double), n, _p(x, C.c_double), _p(act, C.c_int32),
                                _p(lo, C.c_double), _p(ah, C.c_double), _p(rt, C.c_double),
                                clip_eps, value_coef, entropy_coef, grad_scale,
                                _p(grad, C.c_double), _p(sums, C.c_double),
-                               _p(ps, C.c_double) if ps is not None else None)
+                               _p(ps, C.c_double) if ps is not None else None,
+                               _p(vo, C.c_double) if vo is not None else None, float(value_clip))
     return grad, sums, ps
+
+
+# ------------------------------------------------------------------ NEXT-3
+def clip_grad_norm(g, max_norm):
+    """In place on a float64 contiguous array; returns the pre-clip global norm."""
+    assert g.dtype == np.float64 and g.flags.c_contiguous
+    return lib().oracle_clip_grad_norm(g.size, _p(g, C.c_double), float(max_norm))
 
 
 # ------------------------------------------------------------------ C-6
@@ -159,11 +170,25 @@ def log_pi(cfg, params, obs, actions):
     return out
 
 
+def minibatch_bounds(n, M):
+    """NEXT-3 reading R-M: local minibatch k of M covers sample rows [k*n//M, (k+1)*n//M)
+    of the time-major flattened shard (contiguous, no shuffle)."""
+    return [(k * n // M, (k + 1) * n // M) for k in range(M)]
+
+
 def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, t=1,
-             apply=True):
+             apply=True, value_clip=0.0, max_grad_norm=0.0, epochs=1, minibatches=1):
     """One trainer step of the oracle over K shards (list of dicts from synth.make_batch
     with a ``logp_old`` entry).  Returns a dict with adv/ret per shard, mean/std, grad,
-    loss sums and (if apply) the updated params/m/v."""
+    loss sums and (if apply) the updated params/m/v.
+
+    NEXT-3: value_clip > 0 clips the value loss around v_old = the
+    rollout values (rows 0..T-1 of each shard's ``values``); max_grad_norm > 0 clips the
+    global gradient (after the rank-order sum, before Adam); epochs x minibatches runs
+    E*M Adam updates, minibatch k being the union over ranks of each shard's local rows
+    ``minibatch_bounds(n_local, M)[k]``.  Normalisation statistics are taken once over the
+    whole batch.  With E*M > 1 the per-update gradients are returned in ``grads`` and
+    ``grad``/``sums`` are those of the last update."""
     advs, rets = [], []
     for sh in shards:
         a, r = gae(sh["rewards"], sh["values"], sh["dones"], cfg.gamma, cfg.lam)
@@ -173,18 +198,38 @@ def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, 
     N = allA.size
     _, mu, sd = adv_norm(allA, eps=eps, unbiased=unbiased)
     p64 = np.asarray(params, dtype=np.float64).copy()
-    grad = np.zeros(p64.size)
-    sums = np.zeros(5)
-    for sh, a, r in zip(shards, advs, rets):                 # rank order (C-5)
-        ahat = (a - mu) / (sd + eps)
-        loss_and_grad(cfg.obs_dim, cfg.hidden, cfg.heads, p64, sh["obs"], sh["actions"],
-                      sh["logp_old"], ahat, r, cfg.clip_eps, cfg.value_coef, cfg.entropy_coef,
-                      grad_scale=1.0 / N, grad=grad, sums=sums)
-    out = dict(adv=advs, ret=rets, mean=mu, std=sd, grad=grad, sums=sums, N=N)
+    if adam_state is None:
+        adam_state = (np.zeros_like(p64), np.zeros_like(p64))
+    m, v = adam_state
+    vold = [np.asarray(sh["values"], np.float64)[:-1].reshape(-1) for sh in shards]
+    out = dict(adv=advs, ret=rets, mean=mu, std=sd, N=N, grads=[], norms=[], sums_all=[])
+    for _ in range(epochs):
+        for k in range(minibatches):
+            grad = np.zeros(p64.size)
+            sums = np.zeros(5)
+            parts = []
+            for sh, a, r, vo in zip(shards, advs, rets, vold):
+                lo, hi = minibatch_bounds(a.size, minibatches)[k]
+                parts.append((sh, a, r, vo, lo, hi))
+            Nmb = sum(hi - lo for *_, lo, hi in parts)
+            for sh, a, r, vo, lo, hi in parts:            # rank order (C-5)
+                ahat = (a[lo:hi] - mu) / (sd + eps)
+                loss_and_grad(cfg.obs_dim, cfg.hidden, cfg.heads, p64,
+                              np.asarray(sh["obs"])[lo:hi], np.asarray(sh["actions"])[lo:hi],
+                              np.asarray(sh["logp_old"])[lo:hi], ahat, r[lo:hi],
+                              cfg.clip_eps, cfg.value_coef, cfg.entropy_coef,
+                              grad_scale=1.0 / Nmb, grad=grad, sums=sums,
+                              v_old=vo[lo:hi] if value_clip > 0 else None,
+                              value_clip=value_clip)
+            norm = clip_grad_norm(grad, max_grad_norm) if max_grad_norm > 0 else float(
+                np.sqrt(np.sum(grad * grad)))
+            out["grads"].append(grad)
+            out["norms"].append(norm)
+            out["sums_all"].append(sums)
+            if apply:
+                adam(p64, m, v, grad, t, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps)
+                t += 1
+    out.update(grad=grad, sums=sums, grad_norm=out["norms"][-1])
     if apply:
-        if adam_state is None:
-            adam_state = (np.zeros_like(p64), np.zeros_like(p64))
-        m, v = adam_state
-        adam(p64, m, v, grad, t, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps)
         out.update(params=p64, m=m, v=v)
     return out

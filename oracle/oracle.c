@@ -116,7 +116,8 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
                           const int32_t* actions, const double* logp_old,
                           const double* adv_hat, const double* ret,
                           double clip_eps, double value_coef, double entropy_coef,
-                          double grad_scale, double* grad, double* sums, double* per_sample) {
+                          double grad_scale, double* grad, double* sums, double* per_sample,
+                          const double* v_old, double value_clip) {
   int d[64];
   layer_dims(obs_dim, L, hidden, H, heads, d);
   const int A = d[L + 1] - 1;
@@ -164,7 +165,17 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
     const double s1 = rho * Ah, s2 = rho_c * Ah;
     const double l_pg = -(s1 < s2 ? s1 : s2);
     const double V = z[A];
-    const double l_v = (V - ret[i]) * (V - ret[i]);
+    double l_v = (V - ret[i]) * (V - ret[i]);
+    double dV = 2.0 * (V - ret[i]);                               /* d l_v / dV */
+    if (value_clip > 0.0 && v_old) {                              /* NEXT-3 value clipping */
+      const double dlt = V - v_old[i];
+      const double Vc = v_old[i] + (dlt < -value_clip ? -value_clip : (dlt > value_clip ? value_clip : dlt));
+      const double l_c = (Vc - ret[i]) * (Vc - ret[i]);
+      if (l_c > l_v) {
+        l_v = l_c;
+        dV = (fabs(dlt) <= value_clip) ? 2.0 * (Vc - ret[i]) : 0.0;
+      }
+    }
     const double loss_i = l_pg + value_coef * l_v - entropy_coef * ent;
     if (per_sample) per_sample[i] = loss_i;
     sums[0] += l_pg;
@@ -186,7 +197,7 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
       }
       s += heads[h];
     }
-    delta[A] = grad_scale * 2.0 * value_coef * (V - ret[i]);
+    delta[A] = grad_scale * value_coef * dV;
 
     /* backprop through the layers, l = L (head) down to 0 */
     for (int l = L; l >= 0; --l) {
@@ -208,6 +219,19 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
     }
   }
   free(ys); free(z); free(lsm); free(p); free(Hh); free(delta); free(dy);
+}
+
+/* ---------------------------------------------------------------- NEXT-3 grad-norm clip */
+double oracle_clip_grad_norm(int64_t P, double* g, double max_norm) {
+  long double ss = 0.0L;
+  for (int64_t i = 0; i < P; ++i) ss += (long double)g[i] * g[i];
+  const double norm = sqrt((double)ss);
+  if (max_norm > 0.0) {
+    const double coef = max_norm / (norm + 1e-6);
+    if (coef < 1.0)
+      for (int64_t i = 0; i < P; ++i) g[i] *= coef;
+  }
+  return norm;
 }
 
 /* ---------------------------------------------------------------- C-6 Adam */

@@ -57,13 +57,23 @@ void oracle_forward(int obs_dim, int L, const int* hidden, int H, const int* hea
  *   d/dz^h_j = -mask*A*rho*(1[j=a_h] - p^h_j) + c_e p^h_j (l^h_j + H^h),
  *   mask = (A >= 0 ? rho <= 1+eps : rho >= 1-eps) (inclusive, C-A6);  d/dV = 2 c_v (V - R).
  * sums[5] += { sum loss_pg, sum (V-R)^2, sum H, sum 1[|rho-1| > eps], sum (logp_old - logpi) }.
- * adv_hat: advantages already normalised.  per_sample (nullable): [n] loss_i. */
+ * adv_hat: advantages already normalised.  per_sample (nullable): [n] loss_i.
+ * NEXT-3 value clipping (DESIGN.md §3.5 reading R-V; value_clip > 0 and v_old non-null):
+ *   V_c = v_old + clip(V - v_old, -value_clip, +value_clip);
+ *   l_v = max((V - R)^2, (V_c - R)^2);  dl_v/dV = 2 (V - R) if (V - R)^2 >= (V_c - R)^2, else
+ *   2 (V_c - R) * 1[|V - v_old| <= value_clip].  value_clip <= 0 or v_old NULL: l_v = (V - R)^2. */
 void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const int* heads,
                           const double* params, int64_t n, const double* obs,
                           const int32_t* actions, const double* logp_old,
                           const double* adv_hat, const double* ret,
                           double clip_eps, double value_coef, double entropy_coef,
-                          double grad_scale, double* grad, double* sums, double* per_sample);
+                          double grad_scale, double* grad, double* sums, double* per_sample,
+                          const double* v_old, double value_clip);
+
+/* NEXT-3 global gradient-norm clipping (PyTorch clip_grad_norm_ semantics, C-A5 extension):
+ *   norm = sqrt(sum g_i^2);  if max_norm / (norm + 1e-6) < 1: g *= max_norm / (norm + 1e-6).
+ * Returns the pre-clip norm.  max_norm <= 0: no-op (norm still returned). */
+double oracle_clip_grad_norm(int64_t P, double* g, double max_norm);
 
 /* C-6  Adam (C-A13), PyTorch semantics, step t >= 1:
  *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
