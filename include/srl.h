@@ -45,7 +45,7 @@ typedef enum srl_status {
 } srl_status;
 
 const char* srl_last_error(void);
-int srl_abi_version(void);                    /* 1 */
+int srl_abi_version(void);                    /* 2 (1 + NEXT-3 fields) */
 
 /* ---------------------------------------------------------------- a1: GAE
  * Generalised advantage estimation over time-major columns (SPEC.md S:L593-601,
@@ -99,6 +99,17 @@ typedef struct srl_ppo_config {
   int adv_unbiased;         /* 0: population sigma (default, C-A4); 1: N-1 */
   int64_t max_local_n;      /* workspace sizing: largest n_local passed to srl_ppo_step */
   int precision;            /* srl_precision */
+  /* NEXT-3 PPO variants (SURVEY.md C-A5 names them as the next extension):
+   *   value_clip > 0: value loss max((V-R)^2, (V_c-R)^2), V_c = v_old + clip(V - v_old, +-value_clip)
+   *     (reading R-V; srl_ppo_step then needs v_old).  0: plain (V-R)^2.
+   *   max_grad_norm > 0: after the allreduce, g *= min(1, max_norm / (||g||_2 + 1e-6)) before
+   *     Adam (reading R-G, PyTorch clip_grad_norm_).  0: off.
+   *   epochs, minibatches (<= 0 read as 1): srl_ppo_train_step runs epochs x minibatches Adam
+   *     updates; local minibatch k = sample rows [k*n/M, (k+1)*n/M) (reading R-M), every rank
+   *     must then hold the same T*B.  Normalisation statistics are taken once per batch. */
+  float value_clip;
+  float max_grad_norm;
+  int epochs, minibatches;
 } srl_ppo_config;
 
 /* Device-resident statistics written by srl_ppo_step (global means over n_global). */
@@ -114,6 +125,7 @@ typedef struct srl_ppo_stats {
   int64_t nonfinite;        /* non-finite per-sample losses + gradient entries (all ranks) */
   int64_t fp16_saturated;   /* fp16 stores clamped to +-65504 (all ranks) */
   int64_t step;             /* Adam step t after this call = policy version (Code 1 inc_version) */
+  double grad_norm;         /* NEXT-3: global gradient norm before clipping (0 if max_grad_norm == 0) */
 } srl_ppo_stats;
 
 /* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller. */
@@ -144,6 +156,8 @@ srl_status srl_ppo_load_params(srl_ctx* ctx, const float* params_dev, srl_stream
  *   obs       device f16 bits [n_local][ld_obs]      actions device i32 [n_local][H]
  *   logp_old  device f32 [n_local]                     adv device f32 [n_local] (raw A)
  *   ret       device f32 [n_local] (R = A + v)
+ *   v_old     device f32 [n_local]: the rollout values V_old (NEXT-3 value clipping); required
+ *             iff cfg.value_clip > 0, ignored otherwise (may be NULL)
  *   adv_mean_std device f64 [2] {mu, sigma} from srl_adv_norm (advantages normalised inside
  *             the loss kernel), or NULL if adv is already normalised.
  *   apply     1: full update.  0: stop after the backward pass: grads_dev holds this rank's
@@ -153,12 +167,15 @@ srl_status srl_ppo_load_params(srl_ctx* ctx, const float* params_dev, srl_stream
  * n_local <= max_local_n, n_local >= 1, n_global >= n_local. */
 srl_status srl_ppo_step(srl_ctx* ctx, int64_t n_local, int64_t n_global,
                         const uint16_t* obs, const int32_t* actions, const float* logp_old,
-                        const float* adv, const float* ret, const double* adv_mean_std,
-                        int apply, srl_ppo_stats* stats_out, srl_stream_t stream);
+                        const float* adv, const float* ret, const float* v_old,
+                        const double* adv_mean_std, int apply, srl_ppo_stats* stats_out,
+                        srl_stream_t stream);
 
 /* One whole trainer step on this rank's shard of a time-major batch (rows a1 -> a7):
  * srl_gae into context-owned adv/ret (cfg gamma, gae_lambda), global normalisation moments
- * (NCCL all-gather of {n, mean, M2} when world > 1), then srl_ppo_step(apply = 1).
+ * (NCCL all-gather of {n, mean, M2} when world > 1), then srl_ppo_step(apply = 1) once per
+ * minibatch per epoch (cfg.epochs x cfg.minibatches, NEXT-3), v_old = values rows 0..T-1.
+ * stats_out holds the last update's statistics.
  * This is Algorithm.step(sample) (PAPER.md Code 1, L649-654) for PPO.
  *   rewards f32 [T][B], values f32 [T+1][B], dones u8 [T][B] (dense, ld = B)
  *   obs f16 bits [T*B][ld_obs], actions i32 [T*B][H], logp_old f32 [T*B] (sample i = t*B + b)

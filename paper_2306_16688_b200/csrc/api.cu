@@ -83,7 +83,7 @@ static srl_status require_device() {
 }
 
 extern "C" const char* srl_last_error(void) { return g_err.c_str(); }
-extern "C" int srl_abi_version(void) { return 1; }
+extern "C" int srl_abi_version(void) { return 2; }
 
 // ------------------------------------------------------------------ a1
 extern "C" srl_status srl_gae(int T, int B, int ld, const float* rewards, const float* values,
@@ -165,6 +165,11 @@ struct srl_ctx {
   double *gae_part = nullptr, *gae_stats = nullptr, *mean_std = nullptr;
   unsigned int* gae_counter = nullptr;
   int gae_part_cap = 0;
+  // NEXT-3 global-norm clipping: [kGradNormBlocks] partials, norm, coef (float in a double slot)
+  double* gn = nullptr;
+  unsigned int* gn_counter = nullptr;
+  double* gn_norm() const { return gn + kGradNormBlocks; }
+  float* gn_coef() const { return reinterpret_cast<float*>(gn + kGradNormBlocks + 1); }
 };
 
 static bool get_tmap(srl_ctx* c, CUtensorMap* out, const void* base, uint64_t inner,
@@ -312,6 +317,10 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if (cfg->max_local_n < 1 || cfg->max_local_n > (int64_t)1 << 31)
     FAIL(SRL_EINVAL, "srl_ppo_create: need 1 <= max_local_n <= 2^31");
   if (cfg->precision != SRL_PREC_F16_SCALED) FAIL(SRL_EUNSUPPORTED, "srl_ppo_create: precision");
+  if (!(cfg->value_clip >= 0.f) || !(cfg->max_grad_norm >= 0.f) || cfg->epochs > 1000 ||
+      cfg->minibatches > 4096)
+    FAIL(SRL_EINVAL, "srl_ppo_create: need value_clip >= 0, max_grad_norm >= 0, epochs <= 1000, "
+                     "minibatches <= 4096");
   if (srl_status st = require_device()) return st;
   CK(cudaSetDevice(device));
   if (!tmap_init()) FAIL(SRL_ECUDA, "cuTensorMapEncodeTiled unavailable");
@@ -321,6 +330,8 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   c->rank = rank;
   c->world = world;
   c->cfg = *cfg;
+  if (c->cfg.epochs < 1) c->cfg.epochs = 1;
+  if (c->cfg.minibatches < 1) c->cfg.minibatches = 1;
   c->hidden.assign(cfg->hidden, cfg->hidden + cfg->n_hidden);
   c->heads.assign(cfg->head_sizes, cfg->head_sizes + cfg->n_heads);
   c->cfg.hidden = c->hidden.data();
@@ -410,6 +421,8 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if ((st = dalloc(c, &c->gae_stats, sizeof(double) * 4))) return bail(st);
   if ((st = dalloc(c, &c->mean_std, sizeof(double) * 2))) return bail(st);
   if ((st = dalloc(c, &c->gae_counter, sizeof(unsigned int) * 4))) return bail(st);
+  if ((st = dalloc(c, &c->gn, sizeof(double) * (kGradNormBlocks + 2)))) return bail(st);
+  if ((st = dalloc(c, &c->gn_counter, sizeof(unsigned int) * 4))) return bail(st);
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(id.internal, nccl_id, 128);
@@ -540,12 +553,14 @@ static srl_status gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUte
 extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global,
                                    const uint16_t* obs, const int32_t* actions,
                                    const float* logp_old, const float* adv, const float* ret,
-                                   const double* adv_mean_std, int apply,
+                                   const float* v_old, const double* adv_mean_std, int apply,
                                    srl_ppo_stats* stats_out, srl_stream_t stream) {
   if (!c) FAIL(SRL_EINVAL, "srl_ppo_step: null ctx");
   if (n_local < 1 || n_local > c->max_n || n_global < n_local)
     FAIL(SRL_EINVAL, "srl_ppo_step: need 1 <= n_local <= max_local_n, n_global >= n_local");
   if (!obs || !actions || !logp_old || !adv || !ret) FAIL(SRL_EINVAL, "srl_ppo_step: null input");
+  const bool vclip = c->cfg.value_clip > 0.f;
+  if (vclip && !v_old) FAIL(SRL_EINVAL, "srl_ppo_step: value_clip > 0 needs v_old");
   if ((reinterpret_cast<uintptr_t>(obs) & 15) != 0) FAIL(SRL_EINVAL, "srl_ppo_step: obs must be 16-byte aligned");
   CK(cudaSetDevice(c->device));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -599,6 +614,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     for (int h = 0; h < g.n_heads; ++h) g.head_size[h] = c->heads[h];
     g.clip_eps = c->cfg.clip_eps; g.value_coef = c->cfg.value_coef;
     g.entropy_coef = c->cfg.entropy_coef; g.adv_eps = c->cfg.adv_eps;
+    g.v_old = vclip ? v_old : nullptr; g.value_clip = c->cfg.value_clip;
     ProfScope ps(c, s, "head_loss", 2.0 * n * hd.in * hd.out,
                  2.0 * n * hd.in + 2.0 * n * kHeadCols + (16.0 + 4.0 * g.n_heads) * n);
     if (srl_status st = gemm(64, false, false, EPI_LOSS, 1, ta, tb, to, to, g, sms, s, &grid_loss)) return st;
@@ -718,13 +734,21 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
       ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8));
       CKN(ncclAllReduce(c->grads, c->grads, (size_t)(c->P + 8), ncclFloat, ncclSum, c->comm, s));
     }
+    // ---------------- NEXT-3: global gradient-norm clipping of the reduced bucket
+    const bool gclip = c->cfg.max_grad_norm > 0.f;
+    if (gclip) {
+      ProfScope ps(c, s, "grad_norm", 0.0, 4.0 * c->P);
+      CK(launch_gradnorm(c->grads, c->P, c->gn, c->gn_counter, c->cfg.max_grad_norm,
+                         c->gn_norm(), c->gn_coef(), s));
+    }
     // ---------------- a7: Adam + fp16 shadow refresh
     ProfScope ps(c, s, "adam", 0.0, 30.0 * c->P);
     CK(launch_adam(segs, c->P, c->params, c->m, c->v, c->grads, c->t_dev, c->cfg.lr,
-                   c->cfg.beta1, c->cfg.beta2, c->cfg.adam_eps, s));
+                   c->cfg.beta1, c->cfg.beta2, c->cfg.adam_eps, s, gclip ? c->gn_coef() : nullptr));
   }
   CK(launch_stats(c->grads, c->P, adv_mean_std, n_global, c->cfg.value_coef, c->cfg.entropy_coef,
-                  c->t_dev, apply, stats_out, s, c->counters));
+                  c->t_dev, apply, stats_out, s, c->counters,
+                  (apply && c->cfg.max_grad_norm > 0.f) ? c->gn_norm() : nullptr));
   return SRL_OK;
 }
 
@@ -757,8 +781,28 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
     CKN(ncclAllGather(c->gae_stats, gathered, 3, ncclDouble, c->comm, s));
     CK(launch_merge_moments(gathered, c->world, nullptr, c->mean_std, c->cfg.adv_unbiased, s));
   }
-  return srl_ppo_step(c, n, n_global, obs, actions, logp_old, c->adv, c->ret, c->mean_std, 1,
-                      stats_out, stream);
+  // a3..a7 once per minibatch per epoch (NEXT-3, reading R-M); E = M = 1 is one update
+  const int E = c->cfg.epochs, M = c->cfg.minibatches;
+  const float* v_old = c->cfg.value_clip > 0.f ? values : nullptr;   // rows 0..T-1 = V_old
+  if (E == 1 && M == 1)
+    return srl_ppo_step(c, n, n_global, obs, actions, logp_old, c->adv, c->ret, v_old,
+                        c->mean_std, 1, stats_out, stream);
+  if (M > 1 && n_global != (int64_t)c->world * n)
+    FAIL(SRL_EINVAL, "srl_ppo_train_step: minibatches > 1 needs the same T*B on every rank");
+  if (M > n) FAIL(SRL_EINVAL, "srl_ppo_train_step: minibatches > T*B");
+  const int H = (int)c->heads.size();
+  const int64_t ld = c->cfg.ld_obs;
+  for (int e = 0; e < E; ++e)
+    for (int k = 0; k < M; ++k) {
+      const int64_t lo = k * n / M, hi = (k + 1) * n / M;
+      const int64_t nk = hi - lo;
+      if (srl_status st = srl_ppo_step(c, nk, M == 1 ? n_global : (int64_t)c->world * nk, obs + lo * ld,
+                                       actions + lo * H, logp_old + lo, c->adv + lo, c->ret + lo,
+                                       v_old ? v_old + lo : nullptr, c->mean_std, 1, stats_out,
+                                       stream))
+        return st;
+    }
+  return SRL_OK;
 }
 
 // ------------------------------------------------------------------ NEXT-1 pre-fetching

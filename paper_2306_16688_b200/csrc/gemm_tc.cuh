@@ -51,6 +51,7 @@ struct GemmArgs {
   int n_heads, A;
   int head_size[kMaxHeads];
   float clip_eps, value_coef, entropy_coef, adv_eps;
+  const float* v_old; float value_clip;           // NEXT-3 value clipping (v_old null: off)
 };
 
 // Shared-memory layout (identical on host and device):
@@ -199,8 +200,8 @@ __device__ __forceinline__ void count_warp(unsigned long long* ctr, uint32_t n) 
 // Compact runtime loops over the A+1 real columns only (no 64-wide unrolling).
 // Formulas: DESIGN.md §3.1 (SURVEY C-4).
 __device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, const int* act,
-                                              float Ahat, float lp_old, float R, bool rvalid,
-                                              double (&st)[5], uint32_t& nonfinite) {
+                                              float Ahat, float lp_old, float R, float vo,
+                                              bool rvalid, double (&st)[5], uint32_t& nonfinite) {
   const uint32_t lane = lane_id();
   float* z = zb + lane;                       // z[j * kZPitch]: this row's column j
   float logpi = 0.f, ent = 0.f;
@@ -232,8 +233,18 @@ __device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, cons
   const float lo = 1.f - a.clip_eps, hi = 1.f + a.clip_eps;
   const float rc = fminf(fmaxf(rho, lo), hi);
   const float lpg = -fminf(rho * Ahat, rc * Ahat);
-  const float dv = z[a.A * kZPitch] - R;
-  const float lv = dv * dv;
+  const float V = z[a.A * kZPitch];
+  const float dv = V - R;
+  float lv = dv * dv;
+  float gv = 2.f * dv;                       // d lv / dV
+  if (a.v_old) {                             // NEXT-3 value clipping (reading R-V)
+    const float d = V - vo;
+    const float dc = vo + fminf(fmaxf(d, -a.value_clip), a.value_clip) - R;
+    if (dc * dc > lv) {
+      lv = dc * dc;
+      gv = fabsf(d) <= a.value_clip ? 2.f * dc : 0.f;
+    }
+  }
   const float mask = (Ahat >= 0.f) ? (rho <= hi ? 1.f : 0.f) : (rho >= lo ? 1.f : 0.f);
   const float pol = -mask * Ahat * rho;      // coefficient of (onehot - p)
   const float li = lpg + a.value_coef * lv - a.entropy_coef * ent;
@@ -253,7 +264,7 @@ __device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, cons
     }
     off += sz;
   }
-  z[a.A * kZPitch] = ok ? 2.f * a.value_coef * dv : 0.f;
+  z[a.A * kZPitch] = ok ? a.value_coef * gv : 0.f;
   if (!rvalid) return;
   if (!ok) {
     ++nonfinite;
@@ -573,13 +584,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
       } else {  // EPI_LOSS
         int act[kMaxHeads];
-        float Ahat = 0.f, lp = 0.f, R = 0.f;
+        float Ahat = 0.f, lp = 0.f, R = 0.f, vo = 0.f;
         for (int h = 0; h < args.n_heads; ++h) act[h] = 0;
         if (rvalid) {   // per-row inputs: coalesced across lanes, issued before the TMEM wait
           for (int h = 0; h < args.n_heads; ++h) act[h] = __ldg(args.actions + (int64_t)row * args.n_heads + h);
           Ahat = __ldg(args.adv + row);
           lp = __ldg(args.logp_old + row);
           R = __ldg(args.ret + row);
+          if (args.v_old) vo = __ldg(args.v_old + row);
         }
         float* zb = reinterpret_cast<float*>(smem + SL.zbuf) + ew * 64 * kZPitch;
         {
@@ -595,7 +607,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const double mu = args.mean_std[0], sd = args.mean_std[1];
           Ahat = (float)(((double)Ahat - mu) / (sd + (double)args.adv_eps));
         }
-        ppo_rows_smem(args, zb, act, Ahat, lp, R, rvalid, st, nonfinite);
+        ppo_rows_smem(args, zb, act, Ahat, lp, R, vo, rvalid, st, nonfinite);
         __syncwarp();
         // per-CTA bias-gradient partials: lane j sums column j over the warp's 32 rows
         for (int j = lane; j <= args.A; j += 32) {

@@ -108,11 +108,14 @@ cudaError_t launch_extras(int64_t P, float inv_n, const double* stats_part, int 
                           const unsigned long long* counters, float* bucket, cudaStream_t s);
 cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float* v,
                         const float* bucket, const int64_t* t_dev, float lr, float b1,
-                        float b2, float eps, cudaStream_t s);
+                        float b2, float eps, cudaStream_t s, const float* coef = nullptr);
+constexpr int kGradNormBlocks = 296;   // 2 x 148 SMs
+cudaError_t launch_gradnorm(const float* bucket, int64_t P, double* part, unsigned int* counter,
+                            float max_norm, double* norm_out, float* coef_out, cudaStream_t s);
 cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s);
 cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,
                          int64_t n_global, float value_coef, float entropy_coef,
                          int64_t* t_dev, int apply, void* stats_out, cudaStream_t s,
-                         unsigned long long* counters = nullptr);
+                         unsigned long long* counters = nullptr, const double* gnorm = nullptr);
 
 }  // namespace srl

@@ -169,10 +169,12 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
                                                    float* __restrict__ v,
                                                    const float* __restrict__ g,
                                                    const int64_t* __restrict__ t_dev, float lr,
-                                                   float b1, float b2, float eps) {
+                                                   float b1, float b2, float eps,
+                                                   const float* __restrict__ coef) {
   griddep_wait();
   griddep_launch();
   if (g[P + 5] > 0.f) return;
+  const float cf = coef ? *coef : 1.f;           // NEXT-3 global-norm clip coefficient
   const Segment& s = t.s[blockIdx.y];            // one segment per grid row
   const int cnt = s.rows * s.cols;
   const int nq = (cnt + 3) >> 2;
@@ -190,7 +192,8 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
       float4 pp = *reinterpret_cast<const float4*>(p + i0);
       float4 mm = *reinterpret_cast<const float4*>(m + i0);
       float4 vv = *reinterpret_cast<const float4*>(v + i0);
-      const float4 gg = *reinterpret_cast<const float4*>(g + i0);
+      float4 gg = *reinterpret_cast<const float4*>(g + i0);
+      gg.x *= cf; gg.y *= cf; gg.z *= cf; gg.w *= cf;
       adam_one(pp.x, mm.x, vv.x, gg.x, b1, b2, step_size, bc2_sqrt, eps);
       adam_one(pp.y, mm.y, vv.y, gg.y, b1, b2, step_size, bc2_sqrt, eps);
       adam_one(pp.z, mm.z, vv.z, gg.z, b1, b2, step_size, bc2_sqrt, eps);
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
       for (int e = e0; e < cnt; ++e) {
         const int64_t i = s.off + e;
         float pi = p[i], mi = m[i], vi = v[i];
-        adam_one(pi, mi, vi, g[i], b1, b2, step_size, bc2_sqrt, eps);
+        adam_one(pi, mi, vi, g[i] * cf, b1, b2, step_size, bc2_sqrt, eps);
         p[i] = pi; m[i] = mi; v[i] = vi;
         if (!s.is_bias) {
           const int r = e / s.cols, c = e - r * s.cols;
@@ -229,13 +232,67 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
 
 cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float* v,
                         const float* bucket, const int64_t* t_dev, float lr, float b1, float b2,
-                        float eps, cudaStream_t s) {
+                        float eps, cudaStream_t s, const float* coef) {
   int64_t maxq = 1;
   for (int i = 0; i < t.n; ++i) maxq = std::max<int64_t>(maxq, ((int64_t)t.s[i].rows * t.s[i].cols + 3) / 4);
   int64_t bx = (maxq + 255) / 256;
   if (bx > 4 * num_sms()) bx = 4 * num_sms();
   return launch_k(adam_kernel, dim3((unsigned)bx, (unsigned)t.n), dim3(256), 0, s, 1, t, P, p, m,
-                  v, bucket, t_dev, lr, b1, b2, eps);
+                  v, bucket, t_dev, lr, b1, b2, eps, coef);
+}
+
+// NEXT-3 global gradient-norm clipping (reading R-G, PyTorch clip_grad_norm_ semantics):
+// norm = ||g[0..P)||_2 of the (allreduced) bucket in double, coef = min(1, max_norm /
+// (norm + 1e-6)); Adam scales g by coef.  Fixed grid and fixed reduction order: the last
+// block to finish sums the block partials in index order (deterministic, like the GAE merge).
+__global__ void __launch_bounds__(256) gradnorm_kernel(const float* __restrict__ g, int64_t P,
+                                                       double* __restrict__ part,
+                                                       unsigned int* counter, float max_norm,
+                                                       double* norm_out, float* coef_out) {
+  griddep_wait();
+  griddep_launch();
+  double acc = 0.0;
+  const int64_t nq = P >> 2;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int64_t q = blockIdx.x * 256 + threadIdx.x; q < nq; q += (int64_t)gridDim.x * 256) {
+    const float4 x = g4[q];
+    acc += (double)x.x * x.x + (double)x.y * x.y + (double)x.z * x.z + (double)x.w * x.w;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = 4 * nq + threadIdx.x; i < P; i += 256) acc += (double)g[i] * g[i];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[8];
+  __shared__ bool s_last;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < 8; ++w) b += red[w];
+    part[blockIdx.x] = b;
+    __threadfence();
+    s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x >= 32) return;
+  __threadfence();
+  double x = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) x += __ldcg(part + b);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (threadIdx.x == 0) {
+    const double norm = sqrt(x);
+    const double cf = (double)max_norm / (norm + 1e-6);
+    *norm_out = norm;
+    *coef_out = cf < 1.0 ? (float)cf : 1.f;
+    *counter = 0;                                 // ready for the next launch
+  }
+}
+
+cudaError_t launch_gradnorm(const float* bucket, int64_t P, double* part, unsigned int* counter,
+                            float max_norm, double* norm_out, float* coef_out, cudaStream_t s) {
+  return launch_k(gradnorm_kernel, dim3(kGradNormBlocks), dim3(256), 0, s, 1, bucket, P, part,
+                  counter, max_norm, norm_out, coef_out);
 }
 
 __global__ void shadow_kernel(const SegTable t, const float* __restrict__ p) {
@@ -260,7 +317,7 @@ cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s) {
 __global__ void stats_kernel(const float* __restrict__ bucket, int64_t P,
                              const double* __restrict__ mean_std, int64_t n_global, float cv,
                              float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
-                             unsigned long long* counters) {
+                             unsigned long long* counters, const double* gnorm) {
   griddep_wait();
   griddep_launch();
   const float* ex = bucket + P;
@@ -279,14 +336,16 @@ __global__ void stats_kernel(const float* __restrict__ bucket, int64_t P,
   out->nonfinite = (int64_t)ex[5];
   out->fp16_saturated = (int64_t)ex[6];
   out->step = t_dev[0];
+  out->grad_norm = gnorm ? *gnorm : 0.0;
 }
 
 cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,
                          int64_t n_global, float value_coef, float entropy_coef, int64_t* t_dev,
-                         int apply, void* stats_out, cudaStream_t s, unsigned long long* counters) {
+                         int apply, void* stats_out, cudaStream_t s, unsigned long long* counters,
+                         const double* gnorm) {
   return launch_k(stats_kernel, dim3(1), dim3(1), 0, s, 1, bucket, P, mean_std, n_global,
                   value_coef, entropy_coef, t_dev, apply, static_cast<srl_ppo_stats*>(stats_out),
-                  counters);
+                  counters, gnorm);
 }
 
 }  // namespace srl

@@ -35,13 +35,17 @@ class PPOConfigC(C.Structure):
                 ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
                 ("adam_eps", C.c_float), ("adv_eps", C.c_float),
                 ("gamma", C.c_float), ("gae_lambda", C.c_float), ("adv_unbiased", C.c_int),
-                ("max_local_n", C.c_int64), ("precision", C.c_int)]
+                ("max_local_n", C.c_int64), ("precision", C.c_int),
+                # NEXT-3 PPO variants
+                ("value_clip", C.c_float), ("max_grad_norm", C.c_float),
+                ("epochs", C.c_int), ("minibatches", C.c_int)]
 
 
 class PPOStatsC(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("policy_loss", "value_loss", "entropy", "clip_fraction",
                                           "approx_kl", "loss", "adv_mean", "adv_std")] + \
-               [(k, C.c_int64) for k in ("n_global", "nonfinite", "fp16_saturated", "step")]
+               [(k, C.c_int64) for k in ("n_global", "nonfinite", "fp16_saturated", "step")] + \
+               [("grad_norm", C.c_double)]
 
 
 STATS_BYTES = C.sizeof(PPOStatsC)
@@ -71,7 +75,7 @@ def lib():
     L.srl_ppo_params.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64), C.POINTER(C.c_uint64)]
     L.srl_ppo_adam_state.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64)]
     L.srl_ppo_load_params.argtypes = [vp, vp, vp]
-    L.srl_ppo_step.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
+    L.srl_ppo_step.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
     L.srl_ppo_train_step.argtypes = [vp, C.c_int, C.c_int, i64, vp, vp, vp, vp, vp, vp, vp, vp]
     L.srl_batch_upload.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]
     L.srl_ppo_train_step_slot.argtypes = [vp, C.c_int, i64, vp, vp]
@@ -179,6 +183,10 @@ class NetSpec:
     gamma: float = 0.99
     gae_lambda: float = 0.95
     adv_unbiased: int = 0
+    value_clip: float = 0.0       # NEXT-3
+    max_grad_norm: float = 0.0
+    epochs: int = 1
+    minibatches: int = 1
 
     @classmethod
     def from_config(cls, cfg):
@@ -202,7 +210,8 @@ class PPOContext:
                               self._heads, spec.clip_eps, spec.value_coef, spec.entropy_coef,
                               spec.lr, spec.beta1, spec.beta2, spec.adam_eps, spec.adv_eps,
                               spec.gamma, spec.gae_lambda, int(spec.adv_unbiased),
-                              int(max_local_n), 0)
+                              int(max_local_n), 0, spec.value_clip, spec.max_grad_norm,
+                              int(spec.epochs), int(spec.minibatches))
         h = C.c_void_p()
         _check(lib().srl_ppo_create(C.byref(self.cfg), rank, world, nccl_id, self.device,
                                     C.byref(h)))
@@ -246,17 +255,20 @@ class PPOContext:
         return self._read(self.m_ptr, self.P, stream), self._read(self.v_ptr, self.P, stream)
 
     def step(self, n_global, obs, actions, logp_old, adv, ret, adv_mean_std=None, apply=True,
-             stats=None, stream=None):
+             stats=None, stream=None, v_old=None):
         """srl_ppo_step; returns the device stats buffer (uint8 [sizeof srl_ppo_stats])."""
         _cuda(obs, torch.float16, "obs")
         _cuda(actions, torch.int32, "actions")
         for t, nm in ((logp_old, "logp_old"), (adv, "adv"), (ret, "ret")):
             _cuda(t, torch.float32, nm)
+        if v_old is not None:
+            _cuda(v_old, torch.float32, "v_old")
         n_local = logp_old.numel()
         if stats is None:
             stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
         _check(lib().srl_ppo_step(self.handle, n_local, int(n_global), _ptr(obs), _ptr(actions),
-                                  _ptr(logp_old), _ptr(adv), _ptr(ret), _ptr(adv_mean_std),
+                                  _ptr(logp_old), _ptr(adv), _ptr(ret), _ptr(v_old),
+                                  _ptr(adv_mean_std),
                                   int(apply), _ptr(stats), _stream(stream)))
         return stats
 

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.srl_abi_version() == 1
+    assert L.srl_abi_version() == 2
 
 
 def test_sass_is_sm100a_tcgen05():
@@ -53,7 +53,7 @@ def test_validation_without_gpu(L):
     assert L.srl_gae(0, 4, 4, None, None, None, 0.99, 0.95, None, None, None, None) == 1
     assert L.srl_gae(8, 4, 4, None, None, None, 0.99, 0.95, None, None, None, None) == 1
     assert b"srl_gae" in L.srl_last_error()
-    assert L.srl_ppo_step(None, 1, 1, None, None, None, None, None, None, 1, None, None) == 1
+    assert L.srl_ppo_step(None, 1, 1, None, None, None, None, None, None, None, 1, None, None) == 1
     assert L.srl_allreduce_grads(None, None, 0, 0, None) == 1
 
 
@@ -62,7 +62,7 @@ def test_create_rejects_bad_config(L):
     hid = (C.c_int * 1)(100)      # not a multiple of 64
     heads = (C.c_int * 1)(2)
     cfg = S.PPOConfigC(4, 8, 1, hid, 1, heads, 0.2, 0.5, 0.01, 3e-4, 0.9, 0.999, 1e-8, 1e-8,
-                       0.99, 0.95, 0, 32, 0)
+                       0.99, 0.95, 0, 32, 0, 0.0, 0.0, 1, 1)
     h = C.c_void_p()
     assert L.srl_ppo_create(C.byref(cfg), 0, 1, None, 0, C.byref(h)) == 1
     assert b"hidden" in L.srl_last_error()
