@@ -49,6 +49,11 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps (capped at 100)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    # NEXT-3 PPO variants (defaults = the BASELINE workload: one update per batch, no clipping)
+    ap.add_argument("--epochs", type=int, default=1)
+    ap.add_argument("--minibatches", type=int, default=1)
+    ap.add_argument("--value-clip", type=float, default=0.0)
+    ap.add_argument("--max-grad-norm", type=float, default=0.0)
     return ap.parse_args()
 
 
@@ -154,12 +159,13 @@ def reference_arm(args, world, rank):
     c = cfg.with_(B=Bp * cfg.agents)
     b = synth.make_batch(c, seed=0)
     b["logp_old"] = synth.logp_old_uniform_policy(c, b["xi"])
-    st = None
+    nx = dict(epochs=max(1, args.epochs), minibatches=max(1, args.minibatches),
+              value_clip=args.value_clip, max_grad_norm=args.max_grad_norm)
     for _ in range(args.warmup):
-        oracle.ppo_step(c, params, [b], apply=True)
+        oracle.ppo_step(c, params, [b], apply=True, **nx)
     t0 = time.perf_counter()
     for k in range(args.steps):
-        oracle.ppo_step(c, params, [b], apply=True, t=k + 1)
+        oracle.ppo_step(c, params, [b], apply=True, t=k + 1, **nx)
     dt = time.perf_counter() - t0
     value = b["n"] * args.steps / dt
     sample = (f"{cfg.name}-shaped T={cfg.T}, B'={Bp * cfg.agents} columns ({b['n']} samples) per "
@@ -167,7 +173,7 @@ def reference_arm(args, world, rank):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": cfg.name, "T": cfg.T, "B_per_step": Bp * cfg.agents},
+           "data": "synthetic", "config": {"workload": cfg.name, "T": cfg.T, "B_per_step": Bp * cfg.agents, **nx},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
@@ -203,8 +209,11 @@ def main_ours(args, world, rank, local):
     if world > 1:
         from paper_2306_16688_b200.dist import broadcast_unique_id
         nccl_id = broadcast_unique_id(device=dev)
-    ctx = P.PPOContext(P.NetSpec.from_config(cfg), max_local_n=n, rank=rank, world=world,
-                       nccl_id=nccl_id, device=local)
+    import dataclasses
+    spec = dataclasses.replace(P.NetSpec.from_config(cfg), epochs=args.epochs,
+                               minibatches=args.minibatches, value_clip=args.value_clip,
+                               max_grad_norm=args.max_grad_norm)
+    ctx = P.PPOContext(spec, max_local_n=n, rank=rank, world=world, nccl_id=nccl_id, device=local)
     ctx.load_params(params)
     T, Bk = b["rewards"].shape
     stats = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8, device=dev)
@@ -354,7 +363,10 @@ def main_ours(args, world, rank, local):
     # + moments merge when world > 1, the 3L+2 GEMMs, finalize_w + finalize_b + extras, adam,
     # stats (NCCL's kernels are not counted)
     L = len(cfg.hidden)
-    per_step = 1 + (1 if world > 1 else 0) + (L + 1 + (L + 1) + L) + 3 + 1 + 1
+    # per update; epochs x minibatches updates per step (NEXT-3), + grad_norm when clipping
+    per_update = (L + 1 + (L + 1) + L) + 3 + 1 + 1 + (1 if args.max_grad_norm > 0 else 0)
+    updates = max(1, args.epochs) * max(1, args.minibatches)
+    per_step = 1 + (1 if world > 1 else 0) + per_update * updates
     cpu = None
     if not args.no_cpu_baseline:
         v, cn, Bp, secs = time_oracle(cfg, args.cpu_seconds)
@@ -370,11 +382,14 @@ def main_ours(args, world, rank, local):
         "config": {"workload": cfg.name, "T": cfg.T, "B_per_rank": cfg.B, "obs_dim": cfg.obs_dim,
                    "hidden": list(cfg.hidden), "heads": list(cfg.heads), "samples_per_step": N,
                    "frames_per_step": N * cfg.frame_skip, "parallelism": f"dp{world}",
+                   "epochs": max(1, args.epochs), "minibatches": max(1, args.minibatches),
+                   "value_clip": args.value_clip, "max_grad_norm": args.max_grad_norm,
                    "l2": "no flush: per-step working set > L2 (obs %.0f MB + activations %.0f MB + "
                          "dZ %.0f MB per rank vs 126 MB L2)" % (
                              n * cfg.ld_obs * 2 / 1e6, n * sum(cfg.hidden) * 2 / 1e6,
                              n * max(cfg.hidden) * 4 / 1e6)},
         "frames_per_s": N * cfg.frame_skip * K / (ms_total * 1e-3),
+        "sample_updates_per_s": N * updates * K / (ms_total * 1e-3),
         "host_submit_ms_per_step": host_ms,
         "profiled_ms_per_step": prof_ms,
         "e2e": {"value": N * Ke / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes * world,

@@ -38,7 +38,8 @@ def lib():
         d, i64, i32, u8 = C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_uint8)
         f = C.POINTER(C.c_float)
         ip = C.POINTER(C.c_int)
-        _lib.oracle_gae.argtypes = [C.c_int, C.c_int, C.c_int, f, f, u8, C.c_double, C.c_double, d, d]
+        _lib.oracle_gae.argtypes = [C.c_int, C.c_int, C.c_int, f, f, u8, f, C.c_double, C.c_double,
+                                    d, d]
         _lib.oracle_moments.argtypes = [d, i64, d, d]
         _lib.oracle_adv_norm.argtypes = [d, i64, C.c_double, C.c_int, d, d, d]
         _lib.oracle_param_count.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip]
@@ -64,16 +65,20 @@ def _ints(xs):
 
 
 # ------------------------------------------------------------------ C-1
-def gae(rewards, values, dones, gamma, lam):
-    """rewards/dones [T][ld], values [T+1][ld] -> (adv, ret) float64 [T][B=ld]."""
+def gae(rewards, values, dones, gamma, lam, trunc_values=None):
+    """rewards/dones [T][ld], values [T+1][ld] -> (adv, ret) float64 [T][B=ld].
+    trunc_values [T][ld] (NEXT-3 R-T): flags with bit 1 set and bit 0 clear bootstrap from it."""
     r = np.ascontiguousarray(rewards, dtype=np.float32)
     v = np.ascontiguousarray(values, dtype=np.float32)
     dd = np.ascontiguousarray(dones, dtype=np.uint8)
     T, ld = r.shape
     assert v.shape == (T + 1, ld) and dd.shape == (T, ld)
+    tv = None if trunc_values is None else np.ascontiguousarray(trunc_values, dtype=np.float32)
+    assert tv is None or tv.shape == (T, ld)
     adv = np.empty((T, ld), np.float64)
     ret = np.empty((T, ld), np.float64)
     lib().oracle_gae(T, ld, ld, _p(r, C.c_float), _p(v, C.c_float), _p(dd, C.c_uint8),
+                     _p(tv, C.c_float) if tv is not None else None,
                      gamma, lam, _p(adv, C.c_double), _p(ret, C.c_double))
     return adv, ret
 
@@ -188,13 +193,20 @@ def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, 
     E*M Adam updates, minibatch k being the union over ranks of each shard's local rows
     ``minibatch_bounds(n_local, M)[k]``.  Normalisation statistics are taken once over the
     whole batch.  With E*M > 1 the per-update gradients are returned in ``grads`` and
-    ``grad``/``sums`` are those of the last update."""
-    advs, rets = [], []
+    ``grad``/``sums`` are those of the last update.
+
+    Optional shard keys (NEXT-3): ``trunc_values`` [T][Bk] (reading R-T, time-limit
+    bootstrap in GAE) and ``valid`` [T][Bk] u8 (reading R-P: padding samples, valid = 0,
+    are left out of the normalisation moments, the loss and N)."""
+    advs, rets, vms = [], [], []
     for sh in shards:
-        a, r = gae(sh["rewards"], sh["values"], sh["dones"], cfg.gamma, cfg.lam)
+        a, r = gae(sh["rewards"], sh["values"], sh["dones"], cfg.gamma, cfg.lam,
+                   trunc_values=sh.get("trunc_values"))
         advs.append(a.reshape(-1))
         rets.append(r.reshape(-1))
-    allA = np.concatenate(advs)
+        vm = sh.get("valid")
+        vms.append(np.ones(a.size, bool) if vm is None else np.asarray(vm).reshape(-1) != 0)
+    allA = np.concatenate([a[vm] for a, vm in zip(advs, vms)])
     N = allA.size
     _, mu, sd = adv_norm(allA, eps=eps, unbiased=unbiased)
     p64 = np.asarray(params, dtype=np.float64).copy()
@@ -208,18 +220,21 @@ def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, 
             grad = np.zeros(p64.size)
             sums = np.zeros(5)
             parts = []
-            for sh, a, r, vo in zip(shards, advs, rets, vold):
+            for sh, a, r, vo, vm in zip(shards, advs, rets, vold, vms):
                 lo, hi = minibatch_bounds(a.size, minibatches)[k]
-                parts.append((sh, a, r, vo, lo, hi))
-            Nmb = sum(hi - lo for *_, lo, hi in parts)
-            for sh, a, r, vo, lo, hi in parts:            # rank order (C-5)
-                ahat = (a[lo:hi] - mu) / (sd + eps)
+                rows = lo + np.nonzero(vm[lo:hi])[0]      # the valid rows of the range
+                parts.append((sh, a, r, vo, rows))
+            Nmb = sum(rows.size for *_, rows in parts)
+            for sh, a, r, vo, rows in parts:               # rank order (C-5)
+                if rows.size == 0:
+                    continue
+                ahat = (a[rows] - mu) / (sd + eps)
                 loss_and_grad(cfg.obs_dim, cfg.hidden, cfg.heads, p64,
-                              np.asarray(sh["obs"])[lo:hi], np.asarray(sh["actions"])[lo:hi],
-                              np.asarray(sh["logp_old"])[lo:hi], ahat, r[lo:hi],
+                              np.asarray(sh["obs"])[rows], np.asarray(sh["actions"])[rows],
+                              np.asarray(sh["logp_old"])[rows], ahat, r[rows],
                               cfg.clip_eps, cfg.value_coef, cfg.entropy_coef,
                               grad_scale=1.0 / Nmb, grad=grad, sums=sums,
-                              v_old=vo[lo:hi] if value_clip > 0 else None,
+                              v_old=vo[rows] if value_clip > 0 else None,
                               value_clip=value_clip)
             norm = clip_grad_norm(grad, max_grad_norm) if max_grad_norm > 0 else float(
                 np.sqrt(np.sum(grad * grad)))

@@ -14,15 +14,19 @@
 
 /* ---------------------------------------------------------------- C-1 GAE */
 void oracle_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
-                double gamma, double lambda, double* adv, double* ret) {
+                const float* trunc_values, double gamma, double lambda, double* adv, double* ret) {
   for (int b = 0; b < B; ++b) {
     double A_next = 0.0;                         /* A_T = 0 */
     for (int t = T - 1; t >= 0; --t) {
-      double m = 1.0 - (double)(d[(int64_t)t * ld + b] != 0);       /* m_t = 1 - d_t */
+      const uint8_t f = d[(int64_t)t * ld + b];
+      double m = 1.0 - (double)(f != 0);                           /* m_t = 1 - d_t */
       double r_t = r[(int64_t)t * ld + b];
       double v_t = v[(int64_t)t * ld + b];
       double v_n = v[(int64_t)(t + 1) * ld + b];
-      double delta = r_t + gamma * v_n * m - v_t;                  /* delta_t */
+      double boot = v_n * m;                                       /* v_{t+1} m_t */
+      if (trunc_values && f != 0 && !(f & 1))                      /* NEXT-3 R-T: time limit */
+        boot = trunc_values[(int64_t)t * ld + b];
+      double delta = r_t + gamma * boot - v_t;                     /* delta_t */
       double A = delta + gamma * lambda * m * A_next;              /* A_t */
       adv[(int64_t)t * B + b] = A;
       ret[(int64_t)t * B + b] = A + v_t;                           /* R_t = A_t + v_t */

@@ -26,9 +26,14 @@ extern "C" {
 /* C-1  GAE by the backward recursion (BASELINE.json north_star):
  *   m_t = 1 - d_t;  delta_t = r_t + gamma * v_{t+1} * m_t - v_t;
  *   A_t = delta_t + gamma * lambda * m_t * A_{t+1},  A_T = 0;   R_t = A_t + v_t  (C-A1, C-A3).
- * r, d: [T][ld], v: [T+1][ld] (row T = bootstrap value).  adv, ret: dense [T][B]. */
+ * r, d: [T][ld], v: [T+1][ld] (row T = bootstrap value).  adv, ret: dense [T][B].
+ * d is a flag byte: nonzero ends the episode at t (m_t = 0).  NEXT-3 reading R-T (SURVEY C-A2):
+ * with trunc_values [T][ld] non-null, a flag with bit 0 clear and bit 1 set is a time-limit
+ * truncation: the recursion is still cut, but delta_t bootstraps from the truncated state,
+ *   delta_t = r_t + gamma * trunc_values_t - v_t.
+ * trunc_values NULL: every nonzero flag is terminal (the core's reading). */
 void oracle_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
-                double gamma, double lambda, double* adv, double* ret);
+                const float* trunc_values, double gamma, double lambda, double* adv, double* ret);
 
 /* C-2  batch moments, two-pass in long double: mean, and M2 = sum (a - mean)^2. */
 void oracle_moments(const double* a, int64_t n, double* mean, double* m2);

@@ -165,3 +165,89 @@ def test_grad_norm_clip_in_step_and_adam_count():
     b2 = oracle.ppo_step(cfg, b1["params"], sh, adam_state=(b1["m"], b1["v"]), t=2)
     assert np.array_equal(a["params"], b2["params"])
     assert not math.isclose(float(np.abs(a["params"] - b1["params"]).max()), 0.0)
+
+
+# ------------------------------------------------------------------ R-T: time-limit truncation
+def test_truncation_hand_case():
+    """One column, gamma = 0.5, lambda = 1, flags [0, 2, 0] (bit 1 = time limit at t = 1),
+    trunc value 7 at t = 1:  t=2: delta = 3 + 0.5*2 - 1.5 = 2.5 = A_2;  t=1: delta = 2 +
+    0.5*7 - 1 = 4.5 and the chain is cut: A_1 = 4.5;  t=0: delta = 1 + 0.5*1 - 0.5 = 1,
+    A_0 = 1 + 0.5*4.5 = 3.25.  Without trunc_values the flag is terminal: A_1 = 2 - 1 = 1."""
+    r = np.array([[1.0], [2.0], [3.0]], np.float32)
+    v = np.array([[0.5], [1.0], [1.5], [2.0]], np.float32)
+    f = np.array([[0], [2], [0]], np.uint8)
+    tv = np.array([[0.0], [7.0], [0.0]], np.float32)
+    a, ret = oracle.gae(r, v, f, 0.5, 1.0, trunc_values=tv)
+    assert a[:, 0].tolist() == [3.25, 4.5, 2.5]
+    assert ret[:, 0].tolist() == [3.75, 5.5, 4.0]
+    a0, _ = oracle.gae(r, v, f, 0.5, 1.0)
+    assert a0[:, 0].tolist() == [1.0 + 0.5 * 1.0, 1.0, 2.5]
+    # a terminal flag (bit 0) wins over a truncation bit
+    a3, _ = oracle.gae(r, v, np.array([[0], [3], [0]], np.uint8), 0.5, 1.0, trunc_values=tv)
+    assert a3[1, 0] == 1.0
+
+
+def test_truncation_equals_split_column_with_bootstrap():
+    """A column truncated at t equals, on rows 0..t, the un-flagged prefix column whose
+    bootstrap row is the truncated state's value (bit-exact: same double operations)."""
+    rng = np.random.default_rng(5)
+    T = 12
+    r = rng.normal(size=(T, 1)).astype(np.float32)
+    v = rng.normal(size=(T + 1, 1)).astype(np.float32)
+    f = np.zeros((T, 1), np.uint8)
+    t = 6
+    f[t, 0] = 2
+    tv = rng.normal(size=(T, 1)).astype(np.float32)
+    a, _ = oracle.gae(r, v, f, 0.99, 0.95, trunc_values=tv)
+    vp = np.concatenate([v[:t + 1], tv[t:t + 1]])
+    ap, _ = oracle.gae(r[:t + 1], vp, np.zeros((t + 1, 1), np.uint8), 0.99, 0.95)
+    assert np.array_equal(a[:t + 1], ap)
+    # and the rows after the cut are the GAE of the suffix on its own
+    As, _ = oracle.gae(r[t + 1:], v[t + 1:], f[t + 1:], 0.99, 0.95)
+    assert np.array_equal(a[t + 1:], As)
+
+
+# ------------------------------------------------------------------ R-P: padding mask
+def _padded_shard(cfg, params, seed):
+    b = synth.make_batch(cfg, seed=seed)
+    b["logp_old"] = oracle.log_pi(cfg, params, b["obs"], b["actions"]) - b["xi"]
+    rng = np.random.default_rng(seed)
+    valid = (rng.random((cfg.T, b["Bk"])) < 0.7).astype(np.uint8)
+    valid[0, 0] = 1
+    b["valid"] = valid
+    return b
+
+
+def test_valid_mask_moments_and_all_ones():
+    cfg = synth.get_config("tiny").with_(B=8)
+    params = synth.make_params(cfg, 2)
+    b = _padded_shard(cfg, params, 6)
+    o = oracle.ppo_step(cfg, params, [b], apply=False)
+    a = o["adv"][0][b["valid"].reshape(-1) != 0]
+    assert o["N"] == int(b["valid"].sum())
+    assert abs(o["mean"] - a.mean()) <= 1e-14 * max(1.0, abs(a.mean()))     # numpy moments
+    assert abs(o["std"] - a.std()) <= 1e-13 * a.std()
+    ones = dict(b, valid=np.ones_like(b["valid"]))
+    plain = {k: v for k, v in b.items() if k != "valid"}
+    o1, o2 = oracle.ppo_step(cfg, params, [ones], apply=False), oracle.ppo_step(cfg, params, [plain], apply=False)
+    assert np.array_equal(o1["grad"], o2["grad"]) and o1["N"] == o2["N"]
+
+
+def test_valid_mask_padding_never_leaks():
+    """Garbage (NaN observations, out-of-range log-probs, other actions) in padding rows
+    leaves every output unchanged."""
+    cfg = synth.get_config("tiny").with_(B=8)
+    params = synth.make_params(cfg, 3)
+    b = _padded_shard(cfg, params, 7)
+    o = oracle.ppo_step(cfg, params, [b], apply=True)
+    pad = b["valid"].reshape(-1) == 0
+    g = dict(b)
+    g["obs"] = b["obs"].copy()
+    g["obs"][pad] = np.float16(np.nan)
+    g["logp_old"] = b["logp_old"].copy()
+    g["logp_old"][pad] = 1e6
+    g["actions"] = b["actions"].copy()
+    g["actions"][pad] = 0
+    og = oracle.ppo_step(cfg, params, [g], apply=True)
+    assert np.array_equal(o["grad"], og["grad"]) and np.array_equal(o["params"], og["params"])
+    assert np.array_equal(o["sums"], og["sums"])
