@@ -50,6 +50,11 @@ def lib():
                                               C.c_double, d, d, d, d, C.c_double]
         _lib.oracle_clip_grad_norm.argtypes = [i64, d, C.c_double]
         _lib.oracle_clip_grad_norm.restype = C.c_double
+        u64 = C.POINTER(C.c_uint64)
+        _lib.oracle_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_int]
+        _lib.oracle_uniform.restype = C.c_double
+        _lib.oracle_rollout.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, u64,
+                                        C.c_uint64, C.c_int, i32, d, d, d]
         _lib.oracle_adam.argtypes = [i64, d, d, d, d, i64, C.c_double, C.c_double, C.c_double,
                                      C.c_double]
     return _lib
@@ -148,6 +153,27 @@ def clip_grad_norm(g, max_norm):
     """In place on a float64 contiguous array; returns the pre-clip global norm."""
     assert g.dtype == np.float64 and g.flags.c_contiguous
     return lib().oracle_clip_grad_norm(g.size, _p(g, C.c_double), float(max_norm))
+
+
+# ------------------------------------------------------------------ NEXT-2
+def uniform(seed, key, h):
+    return lib().oracle_uniform(int(seed), int(key), int(h))
+
+
+def rollout(obs_dim, hidden, heads, params, obs, seed=0, keys=None, deterministic=False):
+    """Policy-worker inference: (actions i32 [n][H], logp [n], value [n], margin [n][H])."""
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    x = np.ascontiguousarray(np.asarray(obs, dtype=np.float64)[:, :obs_dim])
+    n = x.shape[0]
+    H = len(heads)
+    k = None if keys is None else np.ascontiguousarray(keys, dtype=np.uint64)
+    act = np.empty((n, H), np.int32)
+    lp, val, mg = np.empty(n), np.empty(n), np.empty((n, H))
+    lib().oracle_rollout(obs_dim, len(hidden), _ints(hidden), H, _ints(heads), _p(p, C.c_double),
+                         n, _p(x, C.c_double), _p(k, C.c_uint64) if k is not None else None,
+                         int(seed), int(bool(deterministic)), _p(act, C.c_int32),
+                         _p(lp, C.c_double), _p(val, C.c_double), _p(mg, C.c_double))
+    return act, lp, val, mg
 
 
 # ------------------------------------------------------------------ C-6

@@ -225,6 +225,68 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
   free(ys); free(z); free(lsm); free(p); free(Hh); free(delta); free(dy);
 }
 
+/* ---------------------------------------------------------------- NEXT-2 rollout */
+static uint64_t sm64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+double oracle_uniform(uint64_t seed, uint64_t key, int h) {
+  return (double)(sm64(sm64(seed ^ key) + (uint64_t)h) >> 40) * (1.0 / 16777216.0);
+}
+
+void oracle_rollout(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                    const double* params, int64_t n, const double* obs, const uint64_t* keys,
+                    uint64_t seed, int deterministic, int32_t* actions, double* logp,
+                    double* value, double* margin) {
+  int d[64];
+  layer_dims(obs_dim, L, hidden, H, heads, d);
+  const int A = d[L + 1] - 1;
+  double* z = (double*)malloc(sizeof(double) * (size_t)(A + 1));
+  double* out = (double*)malloc(sizeof(double) * (size_t)(A + 1));
+  for (int64_t i = 0; i < n; ++i) {
+    oracle_forward(obs_dim, L, hidden, H, heads, params, 1, obs + i * obs_dim, z);
+    const uint64_t key = keys ? keys[i] : (uint64_t)i;
+    double lp = 0.0;
+    int s = 0;
+    for (int h = 0; h < H; ++h) {
+      const int a_n = heads[h];
+      double mx = z[s];
+      for (int j = 1; j < a_n; ++j) mx = z[s + j] > mx ? z[s + j] : mx;
+      double se = 0.0;
+      for (int j = 0; j < a_n; ++j) se += exp(z[s + j] - mx);
+      const double lse = mx + log(se);
+      for (int j = 0; j < a_n; ++j) out[j] = z[s + j] - lse;     /* log-softmax */
+      int a = a_n - 1;
+      double mg = 1.0;
+      if (deterministic) {
+        a = 0;
+        for (int j = 1; j < a_n; ++j) if (z[s + j] > z[s + a]) a = j;
+        for (int j = 0; j < a_n; ++j)
+          if (j != a && z[s + a] - z[s + j] < mg) mg = z[s + a] - z[s + j];
+      } else {
+        const double u = oracle_uniform(seed, key, h);
+        double cdf = 0.0;
+        for (int j = 0; j < a_n; ++j) {         /* inverse CDF: first j with u < cdf_j */
+          cdf += exp(out[j]);
+          if (j < a_n - 1 && fabs(u - cdf) < mg) mg = fabs(u - cdf);
+          if (u < cdf) { a = j; break; }
+        }
+      }
+      actions[i * H + h] = a;
+      lp += out[a];
+      if (margin) margin[i * H + h] = mg;
+      s += a_n;
+    }
+    logp[i] = lp;
+    value[i] = z[A];
+  }
+  free(z);
+  free(out);
+}
+
 /* ---------------------------------------------------------------- NEXT-3 grad-norm clip */
 double oracle_clip_grad_norm(int64_t P, double* g, double max_norm) {
   long double ss = 0.0L;

@@ -80,6 +80,23 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
  * Returns the pre-clip norm.  max_norm <= 0: no-op (norm still returned). */
 double oracle_clip_grad_norm(int64_t P, double* g, double max_norm);
 
+/* NEXT-2 policy-worker inference (§3.2.1; SPEC.md policy worker S:L443:
+ * "actions sampled from the policy distribution using a per-worker counter-based RNG keyed by
+ * (seed, client_id, request_id)"; DESIGN.md §3.6 reading R-S).
+ * Counter RNG: sm64(x) = SplitMix64 finaliser of x + 0x9E3779B97F4A7C15;
+ *   u(seed, key, h) = (sm64(sm64(seed ^ key) + h) >> 40) * 2^-24   in [0, 1), exact in f32.
+ * Per request i (key = keys[i], or i if keys is NULL) and head h: forward, log-softmax l^h,
+ * p^h = exp(l^h); sampled action a_h = min { j : u < sum_{k<=j} p^h_k } (A_h - 1 if rounding
+ * leaves none); deterministic != 0: a_h = argmax_j z^h_j (lowest index on ties).
+ * Outputs: actions [n][H], logp [n] = sum_h l^h[a_h], value [n] = V.
+ * margin (nullable) [n][H]: distance of u from the nearest CDF boundary (sampling) or the gap
+ * between the two largest logits (deterministic) -- for the tests' decision-margin filter. */
+double oracle_uniform(uint64_t seed, uint64_t key, int h);
+void oracle_rollout(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                    const double* params, int64_t n, const double* obs, const uint64_t* keys,
+                    uint64_t seed, int deterministic, int32_t* actions, double* logp,
+                    double* value, double* margin);
+
 /* C-6  Adam (C-A13), PyTorch semantics, step t >= 1:
  *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
  *   p -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps). */
