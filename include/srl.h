@@ -56,14 +56,22 @@ int srl_abi_version(void);                    /* 2 (1 + NEXT-3 fields) */
  * d_t = 1 means the episode ended AT transition t: it cuts v_{t+1} and A_{t+1}.
  *   rewards  device f32 [T][ld]          values device f32 [T+1][ld] (row T = bootstrap)
  *   dones    device u8  [T][ld] (0/1)    adv_out device f32 [T][ld]   ret_out f32 [T][ld] or NULL
+ *   trunc_values device f32 [T][ld] or NULL (NEXT-3, DESIGN.md §3.5 reading R-T, SURVEY C-A2):
+ *             a dones byte with bit 0 clear and bit 1 set marks a time-limit truncation at t:
+ *             the recursion is still cut but delta_t = r_t + gamma * trunc_values_t - v_t.
+ *             NULL: every nonzero dones byte is terminal.
+ *   valid    device u8 [T][ld] or NULL (NEXT-3 reading R-P, SURVEY C-A17): entries with 0 are
+ *             padding and are left out of stats_out (adv/ret are still written).  The caller
+ *             cuts each padded column's chain with a dones flag on its last real step.
  *   stats_out device f64 [3] or NULL: {n, mean, M2} of adv over the T*B entries (M2 = sum of
  *             squared deviations), the input srl_adv_norm takes as local_stats.
  * Layout: element (t, b) at t*ld + b; ld >= B.  With ld == B the outputs are the dense
  * sample-major vectors srl_ppo_step consumes (sample i = t*B + b).  T >= 1, B >= 1.
  * Columns are independent: a rank passes its own block of columns. */
 srl_status srl_gae(int T, int B, int ld, const float* rewards, const float* values,
-                   const uint8_t* dones, float gamma, float lambda,
-                   float* adv_out, float* ret_out, double* stats_out, srl_stream_t stream);
+                   const uint8_t* dones, const float* trunc_values, const uint8_t* valid,
+                   float gamma, float lambda, float* adv_out, float* ret_out,
+                   double* stats_out, srl_stream_t stream);
 
 /* ---------------------------------------------------------------- a2: normalisation
  * Batch-wide advantage normalisation (C-A4):
@@ -158,6 +166,9 @@ srl_status srl_ppo_load_params(srl_ctx* ctx, const float* params_dev, srl_stream
  *   ret       device f32 [n_local] (R = A + v)
  *   v_old     device f32 [n_local]: the rollout values V_old (NEXT-3 value clipping); required
  *             iff cfg.value_clip > 0, ignored otherwise (may be NULL)
+ *   valid     device u8 [n_local] or NULL (NEXT-3 R-P): rows with 0 are padding -- zero
+ *             gradient, no statistics; n_global then counts the valid rows of all ranks.
+ *             Padding rows must still hold finite observations (0 * inf in the dW GEMM).
  *   adv_mean_std device f64 [2] {mu, sigma} from srl_adv_norm (advantages normalised inside
  *             the loss kernel), or NULL if adv is already normalised.
  *   apply     1: full update.  0: stop after the backward pass: grads_dev holds this rank's
@@ -168,8 +179,8 @@ srl_status srl_ppo_load_params(srl_ctx* ctx, const float* params_dev, srl_stream
 srl_status srl_ppo_step(srl_ctx* ctx, int64_t n_local, int64_t n_global,
                         const uint16_t* obs, const int32_t* actions, const float* logp_old,
                         const float* adv, const float* ret, const float* v_old,
-                        const double* adv_mean_std, int apply, srl_ppo_stats* stats_out,
-                        srl_stream_t stream);
+                        const uint8_t* valid, const double* adv_mean_std, int apply,
+                        srl_ppo_stats* stats_out, srl_stream_t stream);
 
 /* One whole trainer step on this rank's shard of a time-major batch (rows a1 -> a7):
  * srl_gae into context-owned adv/ret (cfg gamma, gae_lambda), global normalisation moments
@@ -178,12 +189,31 @@ srl_status srl_ppo_step(srl_ctx* ctx, int64_t n_local, int64_t n_global,
  * stats_out holds the last update's statistics.
  * This is Algorithm.step(sample) (PAPER.md Code 1, L649-654) for PPO.
  *   rewards f32 [T][B], values f32 [T+1][B], dones u8 [T][B] (dense, ld = B)
+ *   trunc_values f32 [T][B] or NULL, valid u8 [T][B] or NULL: as srl_gae (NEXT-3); with valid,
+ *   n_global = the number of valid samples of all ranks, and minibatches must be 1
+ *   (SRL_EUNSUPPORTED otherwise).
  *   obs f16 bits [T*B][ld_obs], actions i32 [T*B][H], logp_old f32 [T*B] (sample i = t*B + b)
  *   n_global = sum over ranks of T*B.  T*B <= max_local_n. */
 srl_status srl_ppo_train_step(srl_ctx* ctx, int T, int B, int64_t n_global,
                               const float* rewards, const float* values, const uint8_t* dones,
+                              const float* trunc_values, const uint8_t* valid,
                               const uint16_t* obs, const int32_t* actions, const float* logp_old,
                               srl_ppo_stats* stats_out, srl_stream_t stream);
+
+/* NEXT-2: policy-worker batched inference (§3.2.1: policy workers "flush
+ * requests, run a batched forward and respond"; SPEC.md S:L443 counter-based RNG keyed by
+ * (seed, client_id, request_id); DESIGN.md §3.6 reading R-S).  With the context's current
+ * parameters: forward (a3's kernels), then the head GEMM with a sampling epilogue:
+ *   u(h) = top 24 bits of sm64(sm64(seed ^ key) + h) / 2^24, sm64 = SplitMix64 finaliser;
+ *   a_h = min { j : u(h) < sum_{k<=j} softmax(z^h)_k }  (deterministic != 0: argmax, lowest
+ *   index on ties);  logp = sum_h log softmax(z^h)[a_h];  value = V.
+ *   obs       device f16 bits [n][ld_obs] (16-byte aligned)
+ *   keys      device u64 [n] request keys (e.g. client_id << 32 | request_id), NULL: key = row
+ *   actions_out device i32 [n][H]; logp_out, value_out device f32 [n].
+ * 1 <= n <= max_local_n.  Overwrites the context's activation workspace (not the gradients). */
+srl_status srl_policy_rollout(srl_ctx* ctx, int64_t n, const uint16_t* obs, const uint64_t* keys,
+                              uint64_t seed, int deterministic, int32_t* actions_out,
+                              float* logp_out, float* value_out, srl_stream_t stream);
 
 /* NEXT-1: trainer data pre-fetching (§4.1: "we reserve GPU memory for two
  * batches of training samples ... while the GPU computes the gradient on this sample batch,
@@ -192,12 +222,14 @@ srl_status srl_ppo_train_step(srl_ctx* ctx, int T, int B, int64_t n_global,
  *   srl_batch_upload copies one host batch (same layouts as srl_ppo_train_step; pinned host
  *   memory makes the copies asynchronous) into slot 0 or 1 on the context's own copy stream,
  *   after the last step that read that slot has finished with it.  It returns immediately.
+ *   trunc_values / valid: optional host arrays (NULL: none for this batch), NEXT-3.
  *   srl_ppo_train_step_slot makes `stream` wait for that upload, runs srl_ppo_train_step on the
  *   slot, and releases the slot for the next upload.
  * Alternating slots overlaps the H2D copy of batch k+1 with the step on batch k. */
 srl_status srl_batch_upload(srl_ctx* ctx, int slot, int T, int B, const float* rewards,
                             const float* values, const uint8_t* dones, const uint16_t* obs,
-                            const int32_t* actions, const float* logp_old);
+                            const int32_t* actions, const float* logp_old,
+                            const float* trunc_values, const uint8_t* valid);
 srl_status srl_ppo_train_step_slot(srl_ctx* ctx, int slot, int64_t n_global,
                                    srl_ppo_stats* stats_out, srl_stream_t stream);
 

@@ -87,7 +87,8 @@ extern "C" int srl_abi_version(void) { return 2; }
 
 // ------------------------------------------------------------------ a1
 extern "C" srl_status srl_gae(int T, int B, int ld, const float* rewards, const float* values,
-                              const uint8_t* dones, float gamma, float lambda, float* adv_out,
+                              const uint8_t* dones, const float* trunc_values,
+                              const uint8_t* valid, float gamma, float lambda, float* adv_out,
                               float* ret_out, double* stats_out, srl_stream_t stream) {
   if (T < 1 || B < 1 || ld < B) FAIL(SRL_EINVAL, "srl_gae: need T >= 1, B >= 1, ld >= B");
   if (!rewards || !values || !dones || !adv_out) FAIL(SRL_EINVAL, "srl_gae: null pointer");
@@ -96,7 +97,8 @@ extern "C" srl_status srl_gae(int T, int B, int ld, const float* rewards, const 
   double* part = nullptr;
   const int nb = gae_num_blocks(B);
   if (stats_out) CK(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * 3 * nb, s));
-  CK(launch_gae(T, B, ld, rewards, values, dones, gamma, lambda, adv_out, ret_out, part, s));
+  CK(launch_gae(T, B, ld, rewards, values, dones, trunc_values, valid, gamma, lambda, adv_out,
+                ret_out, part, s));
   if (stats_out) {
     CK(launch_merge_moments(part, nb, stats_out, nullptr, 0, s));
     CK(cudaFreeAsync(part, s));
@@ -153,6 +155,9 @@ struct srl_ctx {
     uint8_t* dones = nullptr;
     __half* obs = nullptr;
     int32_t* actions = nullptr;
+    float* trunc_values = nullptr;   // NEXT-3, allocated on first use
+    uint8_t* valid = nullptr;
+    bool has_tv = false, has_valid = false;
     int T = 0, B = 0;
     bool ready = false;
     cudaEvent_t uploaded = nullptr, released = nullptr;
@@ -550,29 +555,11 @@ static srl_status gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUte
     if (!get_tmap(c, &(map), __VA_ARGS__)) FAIL(SRL_ECUDA, "tensor map encode failed"); \
   } while (0)
 
-extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global,
-                                   const uint16_t* obs, const int32_t* actions,
-                                   const float* logp_old, const float* adv, const float* ret,
-                                   const float* v_old, const double* adv_mean_std, int apply,
-                                   srl_ppo_stats* stats_out, srl_stream_t stream) {
-  if (!c) FAIL(SRL_EINVAL, "srl_ppo_step: null ctx");
-  if (n_local < 1 || n_local > c->max_n || n_global < n_local)
-    FAIL(SRL_EINVAL, "srl_ppo_step: need 1 <= n_local <= max_local_n, n_global >= n_local");
-  if (!obs || !actions || !logp_old || !adv || !ret) FAIL(SRL_EINVAL, "srl_ppo_step: null input");
-  const bool vclip = c->cfg.value_clip > 0.f;
-  if (vclip && !v_old) FAIL(SRL_EINVAL, "srl_ppo_step: value_clip > 0 needs v_old");
-  if ((reinterpret_cast<uintptr_t>(obs) & 15) != 0) FAIL(SRL_EINVAL, "srl_ppo_step: obs must be 16-byte aligned");
-  CK(cudaSetDevice(c->device));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int n = (int)n_local;
+// a3: the hidden layers of the forward pass, Y_l = tanh(Y_{l-1} W_l^T + b_l), into c->Y
+static srl_status forward_hidden(srl_ctx* c, int n, const __half* X0, cudaStream_t s) {
   const int L = c->L;
   const int sms = c->sms;
-  const float inv_n = (float)(1.0 / (double)n_global);
-  const __half* X0 = reinterpret_cast<const __half*>(obs);
   const int ld_obs = c->cfg.ld_obs;
-  // c->counters are zero here: zeroed at create, re-zeroed by the stats kernel of every step
-
-  // ---------------- a3: forward hidden layers Y_l = tanh(Y_{l-1} W_l^T + b_l)
   for (int l = 0; l < L; ++l) {
     const Lay& y = c->lay[l];
     CUtensorMap ta, tb;
@@ -592,6 +579,35 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     if (srl_status st = gemm(y.bn_fwd, false, false, tanh_accurate() ? EPI_TANH_ACC : EPI_TANH, y.cg_fwd,
                              ta, tb, to, to, g, sms, s)) return st;
   }
+  return SRL_OK;
+}
+
+extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global,
+                                   const uint16_t* obs, const int32_t* actions,
+                                   const float* logp_old, const float* adv, const float* ret,
+                                   const float* v_old, const uint8_t* valid,
+                                   const double* adv_mean_std, int apply,
+                                   srl_ppo_stats* stats_out, srl_stream_t stream) {
+  if (!c) FAIL(SRL_EINVAL, "srl_ppo_step: null ctx");
+  if (n_local < 1 || n_local > c->max_n || n_global < (valid ? 1 : n_local))
+    FAIL(SRL_EINVAL, "srl_ppo_step: need 1 <= n_local <= max_local_n, n_global >= n_local "
+                     "(>= 1 with a valid mask)");
+  if (!obs || !actions || !logp_old || !adv || !ret) FAIL(SRL_EINVAL, "srl_ppo_step: null input");
+  const bool vclip = c->cfg.value_clip > 0.f;
+  if (vclip && !v_old) FAIL(SRL_EINVAL, "srl_ppo_step: value_clip > 0 needs v_old");
+  if ((reinterpret_cast<uintptr_t>(obs) & 15) != 0) FAIL(SRL_EINVAL, "srl_ppo_step: obs must be 16-byte aligned");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int n = (int)n_local;
+  const int L = c->L;
+  const int sms = c->sms;
+  const float inv_n = (float)(1.0 / (double)n_global);
+  const __half* X0 = reinterpret_cast<const __half*>(obs);
+  const int ld_obs = c->cfg.ld_obs;
+  // c->counters are zero here: zeroed at create, re-zeroed by the stats kernel of every step
+
+  // ---------------- a3: forward hidden layers Y_l = tanh(Y_{l-1} W_l^T + b_l)
+  if (srl_status st = forward_hidden(c, n, X0, s)) return st;
   // ---------------- a4: head GEMM + fused PPO loss -> per-sample dlogits G16
   const Lay& hd = c->lay[L];
   int grid_loss = 0;
@@ -615,6 +631,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     g.clip_eps = c->cfg.clip_eps; g.value_coef = c->cfg.value_coef;
     g.entropy_coef = c->cfg.entropy_coef; g.adv_eps = c->cfg.adv_eps;
     g.v_old = vclip ? v_old : nullptr; g.value_clip = c->cfg.value_clip;
+    g.valid = valid;
     ProfScope ps(c, s, "head_loss", 2.0 * n * hd.in * hd.out,
                  2.0 * n * hd.in + 2.0 * n * kHeadCols + (16.0 + 4.0 * g.n_heads) * n);
     if (srl_status st = gemm(64, false, false, EPI_LOSS, 1, ta, tb, to, to, g, sms, s, &grid_loss)) return st;
@@ -755,12 +772,14 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
 // ------------------------------------------------------------------ a1..a7 in one call
 extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_global,
                                          const float* rewards, const float* values,
-                                         const uint8_t* dones, const uint16_t* obs,
+                                         const uint8_t* dones, const float* trunc_values,
+                                         const uint8_t* valid, const uint16_t* obs,
                                          const int32_t* actions, const float* logp_old,
                                          srl_ppo_stats* stats_out, srl_stream_t stream) {
   if (!c) FAIL(SRL_EINVAL, "srl_ppo_train_step: null ctx");
-  if (T < 1 || B < 1 || (int64_t)T * B > c->max_n || n_global < (int64_t)T * B)
-    FAIL(SRL_EINVAL, "srl_ppo_train_step: need 1 <= T*B <= max_local_n <= n_global");
+  if (T < 1 || B < 1 || (int64_t)T * B > c->max_n || n_global < (valid ? 1 : (int64_t)T * B))
+    FAIL(SRL_EINVAL, "srl_ppo_train_step: need 1 <= T*B <= max_local_n, T*B <= n_global "
+                     "(n_global >= 1 with a valid mask)");
   if (!rewards || !values || !dones) FAIL(SRL_EINVAL, "srl_ppo_train_step: null trajectory input");
   const int nb = gae_num_blocks(B);
   if (nb > c->gae_part_cap) FAIL(SRL_EINVAL, "srl_ppo_train_step: B too large");
@@ -770,7 +789,8 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
   {
     // a1 + a2 (local): the scan's last block merges the moments (world 1: straight to mean/std)
     ProfScope ps(c, s, "gae_scan", 0.0, 17.0 * n);
-    CK(launch_gae(T, B, B, rewards, values, dones, c->cfg.gamma, c->cfg.gae_lambda, c->adv,
+    CK(launch_gae(T, B, B, rewards, values, dones, trunc_values, valid, c->cfg.gamma,
+                  c->cfg.gae_lambda, c->adv,
                   c->ret, c->gae_part, s, c->gae_counter, c->gae_stats,
                   c->world == 1 ? c->mean_std : nullptr, c->cfg.adv_unbiased));
   }
@@ -785,11 +805,13 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
   const int E = c->cfg.epochs, M = c->cfg.minibatches;
   const float* v_old = c->cfg.value_clip > 0.f ? values : nullptr;   // rows 0..T-1 = V_old
   if (E == 1 && M == 1)
-    return srl_ppo_step(c, n, n_global, obs, actions, logp_old, c->adv, c->ret, v_old,
+    return srl_ppo_step(c, n, n_global, obs, actions, logp_old, c->adv, c->ret, v_old, valid,
                         c->mean_std, 1, stats_out, stream);
   if (M > 1 && n_global != (int64_t)c->world * n)
     FAIL(SRL_EINVAL, "srl_ppo_train_step: minibatches > 1 needs the same T*B on every rank");
   if (M > n) FAIL(SRL_EINVAL, "srl_ppo_train_step: minibatches > T*B");
+  if (M > 1 && valid)   // N_k would be the valid count of each global minibatch: not on the host
+    FAIL(SRL_EUNSUPPORTED, "srl_ppo_train_step: minibatches > 1 with a valid mask");
   const int H = (int)c->heads.size();
   const int64_t ld = c->cfg.ld_obs;
   for (int e = 0; e < E; ++e)
@@ -798,18 +820,51 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
       const int64_t nk = hi - lo;
       if (srl_status st = srl_ppo_step(c, nk, M == 1 ? n_global : (int64_t)c->world * nk, obs + lo * ld,
                                        actions + lo * H, logp_old + lo, c->adv + lo, c->ret + lo,
-                                       v_old ? v_old + lo : nullptr, c->mean_std, 1, stats_out,
-                                       stream))
+                                       v_old ? v_old + lo : nullptr, valid ? valid + lo : nullptr,
+                                       c->mean_std, 1, stats_out, stream))
         return st;
     }
   return SRL_OK;
+}
+
+// ------------------------------------------------------------------ NEXT-2 policy inference
+extern "C" srl_status srl_policy_rollout(srl_ctx* c, int64_t n, const uint16_t* obs,
+                                         const uint64_t* keys, uint64_t seed, int deterministic,
+                                         int32_t* actions_out, float* logp_out, float* value_out,
+                                         srl_stream_t stream) {
+  if (!c) FAIL(SRL_EINVAL, "srl_policy_rollout: null ctx");
+  if (n < 1 || n > c->max_n) FAIL(SRL_EINVAL, "srl_policy_rollout: need 1 <= n <= max_local_n");
+  if (!obs || !actions_out || !logp_out || !value_out) FAIL(SRL_EINVAL, "srl_policy_rollout: null pointer");
+  if ((reinterpret_cast<uintptr_t>(obs) & 15) != 0) FAIL(SRL_EINVAL, "srl_policy_rollout: obs must be 16-byte aligned");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nn = (int)n;
+  if (srl_status st = forward_hidden(c, nn, reinterpret_cast<const __half*>(obs), s)) return st;
+  const Lay& hd = c->lay[c->L];
+  CUtensorMap ta, tb;
+  TMC(ta, c->Y[c->L - 1], hd.in, nn, (uint64_t)hd.in * 2, 64, 128);
+  TMC(tb, hd.w16, hd.in, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
+  GemmArgs g{};
+  g.M = nn; g.N = kHeadCols;
+  g.m_tiles = (nn + 127) / 128; g.n_tiles = 1; g.k_splits = 1;
+  g.kb_total = (hd.in + 63) / 64; g.kb_per_split = g.kb_total;
+  g.bias = c->params + hd.b_off;
+  g.n_heads = (int)c->heads.size(); g.A = c->A;
+  for (int h = 0; h < g.n_heads; ++h) g.head_size[h] = c->heads[h];
+  g.seed = seed; g.keys = reinterpret_cast<const unsigned long long*>(keys);
+  g.deterministic = deterministic;
+  g.act_out = actions_out; g.logp_out = logp_out; g.value_out = value_out;
+  ProfScope ps(c, s, "head_sample", 2.0 * nn * hd.in * hd.out,
+               2.0 * nn * hd.in + (8.0 + 4.0 * g.n_heads) * nn);
+  return gemm(64, false, false, EPI_SAMPLE, 1, ta, tb, ta, ta, g, c->sms, s);
 }
 
 // ------------------------------------------------------------------ NEXT-1 pre-fetching
 extern "C" srl_status srl_batch_upload(srl_ctx* c, int slot, int T, int B, const float* rewards,
                                        const float* values, const uint8_t* dones,
                                        const uint16_t* obs, const int32_t* actions,
-                                       const float* logp_old) {
+                                       const float* logp_old, const float* trunc_values,
+                                       const uint8_t* valid) {
   if (!c || slot < 0 || slot > 1) FAIL(SRL_EINVAL, "srl_batch_upload: bad ctx/slot");
   if (T < 1 || B < 1 || (int64_t)T * B > c->max_n) FAIL(SRL_EINVAL, "srl_batch_upload: need 1 <= T*B <= max_local_n");
   if (!rewards || !values || !dones || !obs || !actions || !logp_old)
@@ -830,6 +885,10 @@ extern "C" srl_status srl_batch_upload(srl_ctx* c, int slot, int T, int B, const
     CK(cudaEventCreateWithFlags(&sl.released, cudaEventDisableTiming));
     CK(cudaEventRecord(sl.released, c->copy_stream));
   }
+  if (trunc_values && !sl.trunc_values)
+    if (srl_status st = dalloc(c, &sl.trunc_values, sizeof(float) * n)) return st;
+  if (valid && !sl.valid)
+    if (srl_status st = dalloc(c, &sl.valid, n)) return st;
   const int64_t m = (int64_t)T * B;
   cudaStream_t cs = c->copy_stream;
   CK(cudaStreamWaitEvent(cs, sl.released, 0));      // the last step on this slot is done with it
@@ -839,6 +898,11 @@ extern "C" srl_status srl_batch_upload(srl_ctx* c, int slot, int T, int B, const
   CK(cudaMemcpyAsync(sl.obs, obs, sizeof(__half) * m * c->cfg.ld_obs, cudaMemcpyHostToDevice, cs));
   CK(cudaMemcpyAsync(sl.actions, actions, sizeof(int32_t) * m * c->heads.size(), cudaMemcpyHostToDevice, cs));
   CK(cudaMemcpyAsync(sl.logp_old, logp_old, sizeof(float) * m, cudaMemcpyHostToDevice, cs));
+  if (trunc_values)
+    CK(cudaMemcpyAsync(sl.trunc_values, trunc_values, sizeof(float) * m, cudaMemcpyHostToDevice, cs));
+  if (valid) CK(cudaMemcpyAsync(sl.valid, valid, m, cudaMemcpyHostToDevice, cs));
+  sl.has_tv = trunc_values != nullptr;
+  sl.has_valid = valid != nullptr;
   CK(cudaEventRecord(sl.uploaded, cs));
   sl.T = T;
   sl.B = B;
@@ -855,6 +919,8 @@ extern "C" srl_status srl_ppo_train_step_slot(srl_ctx* c, int slot, int64_t n_gl
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaStreamWaitEvent(s, sl.uploaded, 0));
   srl_status st = srl_ppo_train_step(c, sl.T, sl.B, n_global, sl.rewards, sl.values, sl.dones,
+                                     sl.has_tv ? sl.trunc_values : nullptr,
+                                     sl.has_valid ? sl.valid : nullptr,
                                      reinterpret_cast<const uint16_t*>(sl.obs), sl.actions,
                                      sl.logp_old, stats_out, stream);
   CK(cudaEventRecord(sl.released, s));

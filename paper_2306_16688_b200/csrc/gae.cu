@@ -10,7 +10,10 @@
 //   pass 2: every warp re-runs the exact recurrence from the true A_end (values are
 //   register-resident), writes adv/ret and accumulates moments.
 // Integer inputs with gamma = lambda = 1 stay exact, so the result is bit-identical to the
-// sequential recursion (C-B1).  Moments per block are {n, mean, M2} in double, merged in a
+// sequential recursion (C-B1).
+// NEXT-3: a flag byte with bit 0 clear and bit 1 set is a time-limit truncation (reading R-T):
+// with trunc values the cut step bootstraps from them; a valid mask (reading R-P) leaves
+// padding entries out of the moments (adv/ret are still written for every entry).  Moments per block are {n, mean, M2} in double, merged in a
 // fixed order (deterministic), shifted sums inside a thread.
 #include <math.h>
 
@@ -71,7 +74,8 @@ __device__ void warp0_merge_parts(const double* part, int count, double* out, do
 template <int TC, int CB>
 __global__ void __launch_bounds__(TC <= 8 ? 1024 : 512)
 gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __restrict__ v,
-           const uint8_t* __restrict__ d, float gamma, float gl, float* __restrict__ adv,
+           const uint8_t* __restrict__ d, const float* __restrict__ tv,
+           const uint8_t* __restrict__ vmask, float gamma, float gl, float* __restrict__ adv,
            float* __restrict__ ret, double* __restrict__ part, unsigned int* counter,
            double* stats_out, double* mean_std_out, int unbiased) {
   griddep_wait();
@@ -98,17 +102,21 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
   for (int sc = nsc - 1; sc >= 0; --sc) {
     const int t0 = sc * SC + ch * TC;
     float delta[TC], c[TC], vt[TC];
+    uint32_t vbits = 0;                      // bit i: entry t0 + i enters the moments
 #pragma unroll
     for (int i = 0; i < TC; ++i) {
       const int t = t0 + i;
       if (col_ok && t < T) {
-        const float rr = __ldg(r + (int64_t)t * ld + b);
-        const float v0 = __ldg(v + (int64_t)t * ld + b);
-        const float v1 = __ldg(v + (int64_t)(t + 1) * ld + b);
-        const float m = __ldg(d + (int64_t)t * ld + b) ? 0.f : 1.f;
-        delta[i] = rr + gamma * v1 * m - v0;
-        c[i] = gl * m;
+        const int64_t e = (int64_t)t * ld + b;
+        const float rr = __ldg(r + e);
+        const float v0 = __ldg(v + e);
+        const uint8_t f = __ldg(d + e);
+        float boot = __ldg(v + e + ld);      // v_{t+1}
+        if (f) boot = (tv && !(f & 1)) ? __ldg(tv + e) : 0.f;
+        delta[i] = rr + gamma * boot - v0;
+        c[i] = f ? 0.f : gl;
         vt[i] = v0;
+        if (!vmask || __ldg(vmask + e)) vbits |= 1u << i;
       } else {
         delta[i] = 0.f;   // rows past T: identity step
         c[i] = 1.f;
@@ -136,6 +144,7 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
       if (col_ok && t < T) {
         adv[(int64_t)t * ld + b] = a;
         if (ret) ret[(int64_t)t * ld + b] = a + vt[i];
+        if (!((vbits >> i) & 1u)) continue;
         if (!have_shift) { sh = a; have_shift = true; }
         const double e = (double)a - sh;
         s1 += e;
@@ -206,26 +215,27 @@ int gae_num_blocks(int B) {
 
 template <int TC, int CB>
 static cudaError_t launch_gae_t(int T, int B, int ld, const float* r, const float* v,
-                                const uint8_t* d, float gamma, float gl, float* adv, float* ret,
-                                double* part, cudaStream_t s, unsigned int* counter,
+                                const uint8_t* d, const float* tv, const uint8_t* vm, float gamma,
+                                float gl, float* adv, float* ret, double* part, cudaStream_t s,
+                                unsigned int* counter,
                                 double* stats_out, double* mean_std_out, int unbiased) {
   constexpr int SUB = 32 / CB;
   const int maxw = TC <= 8 ? 32 : 16;
   const int chunks = (T + TC - 1) / TC;
   const int W = std::max(1, std::min(maxw, (chunks + SUB - 1) / SUB));
   return launch_k(gae_kernel<TC, CB>, dim3(gae_num_blocks(B)), dim3(32 * W), 0, s, 1, T, B, ld, r,
-                  v, d, gamma, gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased);
+                  v, d, tv, vm, gamma, gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased);
 }
 
 cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
-                       float gamma, float lambda, float* adv, float* ret, double* part,
+                       const float* tv, const uint8_t* vm, float gamma, float lambda, float* adv, float* ret, double* part,
                        cudaStream_t s, unsigned int* counter, double* stats_out,
                        double* mean_std_out, int unbiased) {
   const float gl = gamma * lambda;
   const int cb = gae_cols_per_block(B);
   const bool short_t = T <= 32 * 8;        // one super-chunk of 8-row chunks
 #define SRL_GAE(TC, CB) \
-  return launch_gae_t<TC, CB>(T, B, ld, r, v, d, gamma, gl, adv, ret, part, s, counter, stats_out, mean_std_out, unbiased)
+  return launch_gae_t<TC, CB>(T, B, ld, r, v, d, tv, vm, gamma, gl, adv, ret, part, s, counter, stats_out, mean_std_out, unbiased)
   if (short_t) {
     if (cb == 8) SRL_GAE(8, 8);
     if (cb == 16) SRL_GAE(8, 16);

@@ -30,7 +30,7 @@
 
 namespace srl {
 
-enum { EPI_TANH = 0, EPI_DTANH = 1, EPI_PART = 2, EPI_LOSS = 3, EPI_TANH_ACC = 4 };
+enum { EPI_TANH = 0, EPI_DTANH = 1, EPI_PART = 2, EPI_LOSS = 3, EPI_TANH_ACC = 4, EPI_SAMPLE = 5 };
 
 constexpr int kMaxHeads = 8;
 constexpr int kHeadCols = 64;   // padded head width G (logits + value + zero pad)
@@ -52,6 +52,10 @@ struct GemmArgs {
   int head_size[kMaxHeads];
   float clip_eps, value_coef, entropy_coef, adv_eps;
   const float* v_old; float value_clip;           // NEXT-3 value clipping (v_old null: off)
+  const uint8_t* valid;                           // NEXT-3 padding mask [M] (null: all valid)
+  // NEXT-2 policy inference (EPI_SAMPLE): counter-RNG sampling or argmax per head
+  unsigned long long seed; const unsigned long long* keys; int deterministic;
+  int32_t* act_out; float* logp_out; float* value_out;
 };
 
 // Shared-memory layout (identical on host and device):
@@ -74,15 +78,15 @@ __host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, i
   const uint32_t stage_bytes = (uint32_t)(128 + bn / cg) * 64 * 2;
   L.ring = 0;
   L.ostage = stages * stage_bytes;
-  const uint32_t ost = (epi == EPI_PART) ? 0 : kEpiWarps * kOutSlots * kStageTile;
+  const uint32_t ost = (epi == EPI_PART || epi == EPI_SAMPLE) ? 0 : kEpiWarps * kOutSlots * kStageTile;
   L.ystage = L.ostage + ost;
   const uint32_t yst = (epi == EPI_DTANH) ? kEpiWarps * kYSlots * kStageTile : 0;
   L.colsum = L.ystage + yst;
   const uint32_t cs = (epi == EPI_DTANH || epi == EPI_LOSS) ? kEpiWarps * colsum_ld * 4 : 0;
   L.bias = L.colsum + cs;
-  const uint32_t bs = (epi == EPI_TANH || epi == EPI_LOSS) ? 4096 : 0;
+  const uint32_t bs = (epi == EPI_TANH || epi == EPI_LOSS || epi == EPI_SAMPLE) ? 4096 : 0;
   L.zbuf = L.bias + bs;
-  const uint32_t zs = (epi == EPI_LOSS) ? kEpiWarps * 64 * kZPitch * 4 : 0;
+  const uint32_t zs = (epi == EPI_LOSS || epi == EPI_SAMPLE) ? kEpiWarps * 64 * kZPitch * 4 : 0;
   L.bars = L.zbuf + zs;
   L.total = L.bars + kBarBytes;
   return L;
@@ -277,6 +281,52 @@ __device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, cons
   st[4] += lp_old - logpi;
 }
 
+// NEXT-2 (DESIGN.md §3.6 reading R-S): SplitMix64 finaliser of x + golden gamma; the uniform
+// of (seed, key, head) is the top 24 bits of sm64(sm64(seed ^ key) + head), exact in fp32.
+__device__ __forceinline__ unsigned long long sm64(unsigned long long x) {
+  unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// One row of head outputs (lane = row, column j at zb[j * kZPitch + lane]): per head
+// log-softmax, then inverse-CDF sampling with the counter RNG (or argmax), logp and value.
+__device__ __forceinline__ void sample_row(const GemmArgs& a, const float* zb, int row) {
+  const float* z = zb + lane_id();
+  const unsigned long long base = sm64(a.seed ^ (a.keys ? __ldg(a.keys + row) : (unsigned long long)row));
+  float lp = 0.f;
+  int off = 0;
+#pragma unroll 1
+  for (int h = 0; h < a.n_heads; ++h) {
+    const int sz = a.head_size[h];
+    float mx = -INFINITY;
+    int am = 0;
+    for (int j = 0; j < sz; ++j) {
+      const float v = z[(off + j) * kZPitch];
+      if (v > mx) { mx = v; am = j; }          // first maximum
+    }
+    float se = 0.f;
+    for (int j = 0; j < sz; ++j) se += __expf(z[(off + j) * kZPitch] - mx);
+    const float lse = mx + __logf(se);
+    int act = am;
+    if (!a.deterministic) {
+      const float u = (float)(sm64(base + (unsigned long long)h) >> 40) * (1.f / 16777216.f);
+      float cdf = 0.f;
+      act = sz - 1;
+      for (int j = 0; j < sz; ++j) {
+        cdf += __expf(z[(off + j) * kZPitch] - lse);
+        if (u < cdf) { act = j; break; }
+      }
+    }
+    lp += z[(off + act) * kZPitch] - lse;
+    a.act_out[(int64_t)row * a.n_heads + h] = act;
+    off += sz;
+  }
+  a.logp_out[row] = lp;
+  a.value_out[row] = z[a.A * kZPitch];
+}
+
 // Per-warp output staging: kOutSlots 32x32 tiles, a tile is reused once the TMA store issued
 // kOutSlots tiles ago has read it (the TMA unit also serves the operand loads, so stores can
 // queue for a while).
@@ -312,11 +362,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   // SPLIT: both epilogue warpgroups drain every tile, each half of its 32-column chunks, which
   // halves the per-tile epilogue latency the MMA waits on (only 512/BN accumulators exist).
   // The loss epilogue needs whole rows: its groups take alternate tiles instead.
-  constexpr bool SPLIT = EPI != EPI_LOSS && BN >= 64;
+  constexpr bool ROWEPI = EPI == EPI_LOSS || EPI == EPI_SAMPLE;   // whole head rows per lane
+  constexpr bool SPLIT = !ROWEPI && BN >= 64;
   constexpr int NCH_ALL = BN / 32;
   constexpr int NCH = SPLIT ? NCH_ALL / 2 : NCH_ALL;     // chunks per warp per tile
   using Cfg = GemmCfg<BN, CG>;
-  static_assert(EPI != EPI_LOSS || BN == kHeadCols, "loss epilogue works on the 64-col head");
+  static_assert(!ROWEPI || BN == kHeadCols, "loss/sample epilogues work on the 64-col head");
   static_assert(CG == 1 || (BN / CG) % 64 == 0 || !B_MN, "MN-major B halves must be 64-wide");
   const int STAGES = args.stages;
   const SmemLayout SL = smem_layout(BN, EPI, STAGES, args.colsum_ld, CG);
@@ -454,8 +505,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int i = lane; i < args.colsum_ld; i += 32) my_colsum[i] = 0.f;
       __syncwarp();
     }
-    if (EPI == EPI_TANH || EPI == EPI_LOSS) {
-      const int nb = (EPI == EPI_LOSS) ? args.A + 1 : args.N;
+    if (EPI == EPI_TANH || ROWEPI) {
+      const int nb = ROWEPI ? args.A + 1 : args.N;
       for (int i = ew * 32 + lane; i < 1024; i += 256) bias_s[i] = i < nb ? __ldg(args.bias + i) : 0.f;
       named_bar_sync(1, 256);
     }
@@ -582,11 +633,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           }
         }
+      } else if constexpr (EPI == EPI_SAMPLE) {
+        float* zb = reinterpret_cast<float*>(smem + SL.zbuf) + ew * 64 * kZPitch;
+        float z[64];
+        tmem_ld32(taddr, z);
+        tmem_ld32(taddr + 32, z + 32);
+        tc_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (j <= args.A) zb[j * kZPitch + lane] = z[j] + bias_s[j];
+        if (rvalid) sample_row(args, zb, row);   // each lane reads only its own zb column
+        __syncwarp();
       } else {  // EPI_LOSS
         int act[kMaxHeads];
         float Ahat = 0.f, lp = 0.f, R = 0.f, vo = 0.f;
         for (int h = 0; h < args.n_heads; ++h) act[h] = 0;
-        if (rvalid) {   // per-row inputs: coalesced across lanes, issued before the TMEM wait
+        // padding rows (valid == 0) take no part: zero dlogits, no statistics
+        const bool lvalid = rvalid && (!args.valid || __ldg(args.valid + row) != 0);
+        if (lvalid) {   // per-row inputs: coalesced across lanes, issued before the TMEM wait
           for (int h = 0; h < args.n_heads; ++h) act[h] = __ldg(args.actions + (int64_t)row * args.n_heads + h);
           Ahat = __ldg(args.adv + row);
           lp = __ldg(args.logp_old + row);
@@ -607,7 +671,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const double mu = args.mean_std[0], sd = args.mean_std[1];
           Ahat = (float)(((double)Ahat - mu) / (sd + (double)args.adv_eps));
         }
-        ppo_rows_smem(args, zb, act, Ahat, lp, R, vo, rvalid, st, nonfinite);
+        ppo_rows_smem(args, zb, act, Ahat, lp, R, vo, lvalid, st, nonfinite);
         __syncwarp();
         // per-CTA bias-gradient partials: lane j sums column j over the warp's 32 rows
         for (int j = lane; j <= args.A; j += 32) {

@@ -54,6 +54,7 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 // counter != null: the last block merges the partials into stats_out {n, mean, M2} and
 // mean_std_out {mean, sigma} (either may be null) and resets *counter to 0.
 cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
+                       const float* tv /* nullable */, const uint8_t* vm /* nullable */,
                        float gamma, float lambda, float* adv, float* ret,
                        double* part /* [gae_num_blocks(B)][3] or null */, cudaStream_t s,
                        unsigned int* counter = nullptr, double* stats_out = nullptr,

@@ -90,6 +90,10 @@ cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUt
       if (!a_mn && !b_mn && bn == 64 && cg == 1)
         return launch_one<64, false, false, EPI_LOSS, 1>(ta, tb, to, ty, args, grid, s);
       break;
+    case EPI_SAMPLE:
+      if (!a_mn && !b_mn && bn == 64 && cg == 1)
+        return launch_one<64, false, false, EPI_SAMPLE, 1>(ta, tb, to, ty, args, grid, s);
+      break;
     case EPI_PART:
       if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_PART, cg) }
       if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_PART, cg) }

@@ -19,7 +19,7 @@ SRL_OK, SRL_EINVAL, SRL_ECUDA, SRL_ENCCL, SRL_ENOMEM, SRL_EUNSUPPORTED, SRL_ESTA
 EXPORTS = ("srl_last_error", "srl_abi_version", "srl_gae", "srl_adv_norm", "srl_nccl_unique_id",
            "srl_ppo_create", "srl_ppo_destroy", "srl_ppo_params", "srl_ppo_adam_state",
            "srl_ppo_load_params", "srl_ppo_step", "srl_ppo_train_step", "srl_batch_upload",
-           "srl_ppo_train_step_slot", "srl_allreduce_grads", "srl_prof_enable",
+           "srl_ppo_train_step_slot", "srl_policy_rollout", "srl_allreduce_grads", "srl_prof_enable",
            "srl_prof_reset", "srl_prof_count", "srl_prof_read", "srl_debug_gemm")
 
 
@@ -66,7 +66,8 @@ def lib():
     vp, i64, st = C.c_void_p, C.c_int64, C.c_int
     L.srl_last_error.restype = C.c_char_p
     L.srl_abi_version.restype = C.c_int
-    L.srl_gae.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_float, C.c_float, vp, vp, vp, vp]
+    L.srl_gae.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_float,
+                          vp, vp, vp, vp]
     L.srl_adv_norm.argtypes = [vp, vp, i64, vp, C.c_float, C.c_int, C.c_int, vp, vp]
     L.srl_nccl_unique_id.argtypes = [C.c_char_p]
     L.srl_ppo_create.argtypes = [C.POINTER(PPOConfigC), C.c_int, C.c_int, C.c_char_p, C.c_int,
@@ -75,10 +76,12 @@ def lib():
     L.srl_ppo_params.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64), C.POINTER(C.c_uint64)]
     L.srl_ppo_adam_state.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64)]
     L.srl_ppo_load_params.argtypes = [vp, vp, vp]
-    L.srl_ppo_step.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
-    L.srl_ppo_train_step.argtypes = [vp, C.c_int, C.c_int, i64, vp, vp, vp, vp, vp, vp, vp, vp]
-    L.srl_batch_upload.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]
+    L.srl_ppo_step.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
+    L.srl_ppo_train_step.argtypes = [vp, C.c_int, C.c_int, i64, vp, vp, vp, vp, vp, vp, vp, vp,
+                                     vp, vp]
+    L.srl_batch_upload.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp]
     L.srl_ppo_train_step_slot.argtypes = [vp, C.c_int, i64, vp, vp]
+    L.srl_policy_rollout.argtypes = [vp, i64, vp, vp, C.c_uint64, C.c_int, vp, vp, vp, vp]
     L.srl_allreduce_grads.argtypes = [vp, vp, i64, C.c_int, vp]
     L.srl_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
                                  C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
@@ -114,11 +117,16 @@ def _cuda(t, dtype, name):
 
 
 # ------------------------------------------------------------------ a1
-def gae(rewards, values, dones, gamma, lam, adv=None, ret=None, stats=None, ld=None, stream=None):
+def gae(rewards, values, dones, gamma, lam, adv=None, ret=None, stats=None, ld=None, stream=None,
+        trunc_values=None, valid=None):
     """srl_gae on [T][ld] tensors; returns (adv, ret, stats{n, mean, M2} f64[3])."""
     _cuda(rewards, torch.float32, "rewards")
     _cuda(values, torch.float32, "values")
     _cuda(dones, torch.uint8, "dones")
+    if trunc_values is not None:
+        _cuda(trunc_values, torch.float32, "trunc_values")
+    if valid is not None:
+        _cuda(valid, torch.uint8, "valid")
     T, ldr = rewards.shape
     B = ldr if ld is None else ld
     if adv is None:
@@ -127,7 +135,8 @@ def gae(rewards, values, dones, gamma, lam, adv=None, ret=None, stats=None, ld=N
         ret = torch.empty_like(rewards)
     if stats is None:
         stats = torch.empty(3, dtype=torch.float64, device=rewards.device)
-    _check(lib().srl_gae(T, B, ldr, _ptr(rewards), _ptr(values), _ptr(dones), gamma, lam,
+    _check(lib().srl_gae(T, B, ldr, _ptr(rewards), _ptr(values), _ptr(dones), _ptr(trunc_values),
+                         _ptr(valid), gamma, lam,
                          _ptr(adv), _ptr(ret), _ptr(stats), _stream(stream)))
     return adv, ret, stats
 
@@ -255,7 +264,7 @@ class PPOContext:
         return self._read(self.m_ptr, self.P, stream), self._read(self.v_ptr, self.P, stream)
 
     def step(self, n_global, obs, actions, logp_old, adv, ret, adv_mean_std=None, apply=True,
-             stats=None, stream=None, v_old=None):
+             stats=None, stream=None, v_old=None, valid=None):
         """srl_ppo_step; returns the device stats buffer (uint8 [sizeof srl_ppo_stats])."""
         _cuda(obs, torch.float16, "obs")
         _cuda(actions, torch.int32, "actions")
@@ -263,11 +272,13 @@ class PPOContext:
             _cuda(t, torch.float32, nm)
         if v_old is not None:
             _cuda(v_old, torch.float32, "v_old")
+        if valid is not None:
+            _cuda(valid, torch.uint8, "valid")
         n_local = logp_old.numel()
         if stats is None:
             stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
         _check(lib().srl_ppo_step(self.handle, n_local, int(n_global), _ptr(obs), _ptr(actions),
-                                  _ptr(logp_old), _ptr(adv), _ptr(ret), _ptr(v_old),
+                                  _ptr(logp_old), _ptr(adv), _ptr(ret), _ptr(v_old), _ptr(valid),
                                   _ptr(adv_mean_std),
                                   int(apply), _ptr(stats), _stream(stream)))
         return stats
@@ -289,24 +300,27 @@ class PPOContext:
         return out
 
     def train_step(self, n_global, rewards, values, dones, obs, actions, logp_old, stats=None,
-                   stream=None):
+                   stream=None, trunc_values=None, valid=None):
         """srl_ppo_train_step: GAE -> normalisation -> update in one call (device inputs)."""
         T, B = rewards.shape
         if stats is None:
             stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
         _check(lib().srl_ppo_train_step(self.handle, T, B, int(n_global), _ptr(rewards),
-                                        _ptr(values), _ptr(dones), _ptr(obs), _ptr(actions),
+                                        _ptr(values), _ptr(dones), _ptr(trunc_values),
+                                        _ptr(valid), _ptr(obs), _ptr(actions),
                                         _ptr(logp_old), _ptr(stats), _stream(stream)))
         return stats
 
-    def upload(self, slot, rewards, values, dones, obs, actions, logp_old):
+    def upload(self, slot, rewards, values, dones, obs, actions, logp_old, trunc_values=None,
+               valid=None):
         """NEXT-1: async H2D of a host batch (pinned CPU tensors) into device slot 0/1."""
-        for t in (rewards, values, dones, obs, actions, logp_old):
-            if t.is_cuda or not t.is_contiguous():
+        for t in (rewards, values, dones, obs, actions, logp_old, trunc_values, valid):
+            if t is not None and (t.is_cuda or not t.is_contiguous()):
                 raise SrlError("upload: need contiguous host tensors")
         T, B = rewards.shape
         _check(lib().srl_batch_upload(self.handle, slot, T, B, _ptr(rewards), _ptr(values),
-                                      _ptr(dones), _ptr(obs), _ptr(actions), _ptr(logp_old)))
+                                      _ptr(dones), _ptr(obs), _ptr(actions), _ptr(logp_old),
+                                      _ptr(trunc_values), _ptr(valid)))
 
     def train_step_slot(self, slot, n_global, stats=None, stream=None):
         if stats is None:
@@ -314,6 +328,25 @@ class PPOContext:
         _check(lib().srl_ppo_train_step_slot(self.handle, slot, int(n_global), _ptr(stats),
                                              _stream(stream)))
         return stats
+
+    def rollout(self, obs, keys=None, seed=0, deterministic=False, actions=None, logp=None,
+                value=None, stream=None):
+        """NEXT-2 srl_policy_rollout: batched policy inference -> (actions i32 [n][H], logp, value)."""
+        _cuda(obs, torch.float16, "obs")
+        n = obs.shape[0]
+        if keys is not None:
+            _cuda(keys, torch.int64, "keys")
+        dev = obs.device
+        if actions is None:
+            actions = torch.empty((n, len(self.spec.heads)), dtype=torch.int32, device=dev)
+        if logp is None:
+            logp = torch.empty(n, dtype=torch.float32, device=dev)
+        if value is None:
+            value = torch.empty(n, dtype=torch.float32, device=dev)
+        _check(lib().srl_policy_rollout(self.handle, n, _ptr(obs), _ptr(keys), int(seed) & ((1 << 64) - 1),
+                                        int(bool(deterministic)), _ptr(actions), _ptr(logp),
+                                        _ptr(value), _stream(stream)))
+        return actions, logp, value
 
     def allreduce_grads(self, buf: torch.Tensor, op: int = 0, stream=None):
         _cuda(buf, torch.float32, "buf")

@@ -50,10 +50,10 @@ def test_sass_is_sm100a_tcgen05():
 
 def test_validation_without_gpu(L):
     # null pointers / bad shapes are rejected on the host before any launch
-    assert L.srl_gae(0, 4, 4, None, None, None, 0.99, 0.95, None, None, None, None) == 1
-    assert L.srl_gae(8, 4, 4, None, None, None, 0.99, 0.95, None, None, None, None) == 1
+    assert L.srl_gae(0, 4, 4, None, None, None, None, None, 0.99, 0.95, None, None, None, None) == 1
+    assert L.srl_gae(8, 4, 4, None, None, None, None, None, 0.99, 0.95, None, None, None, None) == 1
     assert b"srl_gae" in L.srl_last_error()
-    assert L.srl_ppo_step(None, 1, 1, None, None, None, None, None, None, None, 1, None, None) == 1
+    assert L.srl_ppo_step(None, 1, 1, None, None, None, None, None, None, None, None, 1, None, None) == 1
     assert L.srl_allreduce_grads(None, None, 0, 0, None) == 1
 
 

@@ -184,3 +184,109 @@ def test_minibatches_reject_bad_sizes():
     with pytest.raises(P.SrlError):              # unequal shards would need N_k per rank
         ctx2.train_step(2 * b["n"], dv["rewards"], dv["values"], dv["dones"], dv["obs"],
                         dv["actions"], dv["logp_old"])
+
+
+# ------------------------------------------------------------------ R-T / R-P in the GAE scan
+def _flags_tv_valid(rng, T, B):
+    u = rng.random((T, B))
+    f = np.where(u < 0.03, 1, np.where(u < 0.06, 2, np.where(u < 0.07, 3, 0))).astype(np.uint8)
+    valid = (rng.random((T, B)) < 0.8).astype(np.uint8)
+    return f, valid
+
+
+@pytest.mark.parametrize("T,B", [(7, 33), (128, 96), (400, 50)])
+def test_gae_truncation_valid_integer_bit_exact(T, B):
+    """gamma = lambda = 1 and small integers (C-B1 style): the truncated bootstrap is exact, so
+    adv/ret equal the oracle bit for bit; the masked moments count only valid entries."""
+    import paper_2306_16688_b200 as P
+    rng = np.random.default_rng(T + B)
+    r = rng.integers(-3, 4, (T, B)).astype(np.float32)
+    v = rng.integers(-5, 6, (T + 1, B)).astype(np.float32)
+    tv = rng.integers(-5, 6, (T, B)).astype(np.float32)
+    f, valid = _flags_tv_valid(rng, T, B)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    adv, ret, st = P.gae(dev(r), dev(v), dev(f), 1.0, 1.0, trunc_values=dev(tv), valid=dev(valid))
+    ra, rr = oracle.gae(r, v, f, 1.0, 1.0, trunc_values=tv)
+    assert np.array_equal(adv.cpu().numpy(), ra.astype(np.float32))
+    assert np.array_equal(ret.cpu().numpy(), rr.astype(np.float32))
+    st = st.cpu().numpy()
+    sel = ra[valid != 0]
+    mu, m2 = oracle.moments(sel)
+    assert st[0] == sel.size and abs(st[1] - mu) <= 1e-12 * max(1, abs(mu))
+    assert abs(st[2] - m2) <= 1e-9 * m2
+    # without trunc values a truncation flag is terminal (the core's reading)
+    a0, _, _ = P.gae(dev(r), dev(v), dev(f), 1.0, 1.0)
+    assert np.array_equal(a0.cpu().numpy(), oracle.gae(r, v, f, 1.0, 1.0)[0].astype(np.float32))
+
+
+def _padded_inputs(cfg, seed):
+    params, b = make_inputs(cfg, seed=seed)
+    rng = np.random.default_rng(seed)
+    f, valid = _flags_tv_valid(rng, cfg.T, b["Bk"])
+    b["dones"] = f
+    b["trunc_values"] = rng.normal(size=(cfg.T, b["Bk"])).astype(np.float32)
+    b["valid"] = valid
+    return params, b
+
+
+@pytest.mark.parametrize("name", ["gfootball", "hns"])
+def test_train_step_truncation_and_padding_parity(name):
+    """Whole trainer step with time-limit flags + trunc values and a padding mask: gradient
+    (kink-free fixture), statistics and normalisation against the oracle; padding rows
+    rewritten with other finite garbage give a bit-identical result (no leak)."""
+    import paper_2306_16688_b200 as P
+    cfg = synth.get_config(name).with_(B=REDUCED[name] * synth.get_config(name).agents)
+    params, b = _padded_inputs(cfg, 17)
+    n = b["n"]
+    nv = int(b["valid"].sum())
+    o = oracle.ppo_step(cfg, params, [b], apply=False)
+    assert o["N"] == nv
+
+    def run(bb):
+        ctx = _ctx(cfg, params, n)
+        d = to_dev(bb)
+        tv = torch.from_numpy(bb["trunc_values"]).cuda()
+        vm = torch.from_numpy(bb["valid"]).cuda()
+        st = P.decode_stats(ctx.train_step(nv, d["rewards"], d["values"], d["dones"], d["obs"],
+                                           d["actions"], d["logp_old"], trunc_values=tv, valid=vm))
+        return st, ctx.grads().cpu().numpy().astype(np.float64)
+
+    st, G = run(b)
+    _check_grads(cfg, G[:cfg.n_params], o["grad"])
+    assert st["n_global"] == nv and st["nonfinite"] == 0
+    assert abs(st["adv_mean"] - o["mean"]) <= 1e-6 * o["std"]
+    assert abs(st["adv_std"] - o["std"]) <= 1e-6 * o["std"]
+    assert abs(st["entropy"] - o["sums"][2] / nv) <= TOL * abs(o["sums"][2] / nv)
+    g = dict(b)
+    pad = b["valid"].reshape(-1) == 0
+    g["obs"] = b["obs"].copy()
+    g["obs"][pad] = np.float16(3.0)
+    g["logp_old"] = b["logp_old"].copy()
+    g["logp_old"][pad] = -50.0
+    g["actions"] = b["actions"].copy()
+    g["actions"][pad] = 0
+    st2, G2 = run(g)
+    # the pads' activations differ, but every row they feed is multiplied by a zero dZ row
+    assert np.array_equal(G2, G)
+
+
+def test_prefetch_slots_with_truncation_and_padding():
+    """NEXT-1 slots carry the optional NEXT-3 arrays: bit-identical to the device path."""
+    import paper_2306_16688_b200 as P
+    cfg = synth.get_config("gfootball").with_(B=16)
+    params, b = _padded_inputs(cfg, 19)
+    nv = int(b["valid"].sum())
+    keys = ("rewards", "values", "dones", "obs", "actions", "logp_old", "trunc_values", "valid")
+    host = {k: torch.from_numpy(np.ascontiguousarray(b[k])).pin_memory() for k in keys}
+    dev = {k: h.cuda() for k, h in host.items()}
+    a, c = _ctx(cfg, params, b["n"]), _ctx(cfg, params, b["n"])
+    base = [host[k] for k in keys[:6]]
+    c.upload(0, *base, trunc_values=host["trunc_values"], valid=host["valid"])
+    for k in range(2):
+        a.train_step(nv, *[dev[x] for x in keys[:6]], trunc_values=dev["trunc_values"],
+                     valid=dev["valid"])
+        if k == 0:
+            c.upload(1, *base, trunc_values=host["trunc_values"], valid=host["valid"])
+        c.train_step_slot(k % 2, nv)
+    torch.cuda.synchronize()
+    assert torch.equal(a.params(), c.params()) and torch.equal(a.grads(), c.grads())
