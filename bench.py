@@ -298,6 +298,21 @@ def main_ours(args, world, rank, local):
     x1.record()
     barrier()
     e2e_ms = max_over_ranks(x0.elapsed_time(x1))
+    # ---------------- NEXT-2: policy-worker batched inference on the same batch of observations
+    # (forward + counter-RNG sampling epilogue), device-timed like `value`
+    Ki = min(K, 100)
+    inf_out = (torch.empty((n, len(cfg.heads)), dtype=torch.int32, device=dev),
+               torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.float32, device=dev))
+    for j in range(3):
+        ctx.rollout(d["obs"], seed=j, actions=inf_out[0], logp=inf_out[1], value=inf_out[2])
+    barrier()
+    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    i0.record()
+    for j in range(Ki):
+        ctx.rollout(d["obs"], seed=j, actions=inf_out[0], logp=inf_out[1], value=inf_out[2])
+    i1.record()
+    barrier()
+    inf_ms = max_over_ranks(i0.elapsed_time(i1)) / Ki
     if sampler:
         time.sleep(0.1)
         sampler.stop()
@@ -395,6 +410,10 @@ def main_ours(args, world, rank, local):
         "e2e": {"value": N * Ke / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes * world,
                 "d2h_bytes_per_step": P.srl.STATS_BYTES * world, "steps": Ke},
         "gpu_launches": per_step * K,
+        "inference": {"what": "NEXT-2 srl_policy_rollout: forward + sampling epilogue over the "
+                              "step's observations (policy-worker batch = the whole batch)",
+                      "value": N / (inf_ms * 1e-3), "unit": "samples/s", "ms_per_call": inf_ms,
+                      "batch_per_rank": n, "calls": Ki, "gpu_launches_per_call": L + 1},
         "roofline": roofline,
         "kernels": kernels,
         "cpu_baseline": cpu,
