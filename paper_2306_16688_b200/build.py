@@ -44,18 +44,21 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> str:
+    """defines: extra -D flags (tools/build_variant.py); out: alternative .so path."""
     inc, lib = nccl_dirs()
-    os.makedirs(BUILD, exist_ok=True)
+    build_dir = BUILD if out is None else os.path.join(os.path.dirname(out), "obj")
+    so = SO if out is None else out
+    os.makedirs(build_dir, exist_ok=True)
     hdr = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "srl.h")]
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-                    "-I", CSRC, "-I", inc, "--expt-relaxed-constexpr"]
+                    "-I", CSRC, "-I", inc, "--expt-relaxed-constexpr"] + [f"-D{d}" for d in defines]
     if verbose:
         flags += ["-Xptxas", "-v"]
 
     def compile_one(src):
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + hdr):
             cmd = [nvcc()] + flags + ["-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
@@ -67,14 +70,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    if force or _stale(SO, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "shared", "-o", SO] + objs + [
+    if force or _stale(so, objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "shared", "-o", so] + objs + [
             "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}",
             "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return SO
+    return so
 
 
 if __name__ == "__main__":

@@ -65,8 +65,14 @@ struct SmemLayout {
 };
 constexpr int kZPitch = 33;                       // loss row buffer [64 cols][33] per warp
 constexpr int kStageTile = 32 * 32 * 2;           // one 32x32 fp16 staging tile
-constexpr int kYSlots = 2;                        // y_prev ring per warp (1 chunk in flight)
-constexpr int kOutSlots = 4;                      // output staging tiles per warp
+#ifndef SRL_Y_SLOTS
+#define SRL_Y_SLOTS 2
+#endif
+#ifndef SRL_OUT_SLOTS
+#define SRL_OUT_SLOTS 2
+#endif
+constexpr int kYSlots = SRL_Y_SLOTS;              // y_prev ring per warp (1 chunk in flight)
+constexpr int kOutSlots = SRL_OUT_SLOTS;          // output staging tiles per warp
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kBarBytes = 640;                    // 64 mbarriers + TMEM slot
@@ -548,15 +554,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                              (SPLIT ? grp * NCH * 32 : 0);
 
       if constexpr (EPI == EPI_TANH) {
-        float nxt[32];
-        tmem_ld32(taddr, nxt);
-#pragma unroll 1
-        for (int c = 0; c < NCH; ++c) {
-          float v[32];
-          tc_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = nxt[j];
-          if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, nxt);   // overlap next TMEM read
+        auto body = [&](int c, float (&v)[32]) {
           const int col0 = n0 + c * 32;
           const float4* b4 = reinterpret_cast<const float4*>(bias_s + col0);
 #pragma unroll
@@ -574,17 +572,27 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               v[4 * q + 3] = tanh_mufu(v[4 * q + 3] + bb.w);
             }
           }
-          {
-            uint8_t* t = ost.acquire();
-            stile_write_row(t, (int)lane, v);
-            ost.release(t, &tmO, col0, row0);      // rows >= M are clipped by TMA
+          uint8_t* t = ost.acquire();
+          stile_write_row(t, (int)lane, v);
+          ost.release(t, &tmO, col0, row0);      // rows >= M are clipped by TMA
+        };
+        // ping-pong register buffers (compile-time after unrolling): the next chunk's TMEM
+        // read is in flight while this one is computed, without a register copy
+        float b0[32], b1[32];
+        tmem_ld32(taddr, b0);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          tc_wait_ld();
+          if (c & 1) {
+            if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, b0);
+            body(c, b1);
+          } else {
+            if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, b1);
+            body(c, b0);
           }
         }
       } else if constexpr (EPI == EPI_DTANH) {
-        float nxt[32];
-        tmem_ld32(taddr, nxt);
-#pragma unroll 1
-        for (int c = 0; c < NCH; ++c) {
+        auto body = [&](int c, float (&v)[32]) {
           const int yb = (ybase + c) % kYSlots;
           if (c + kYSlots - 1 < NCH && lane == 0) {   // keep kYSlots-1 chunks in flight
             const int sl = (ybase + c + kYSlots - 1) % kYSlots;
@@ -592,11 +600,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             mbar_expect_tx(&my_ybar[sl], kStageTile);
             tma_load_2d(ystage + sl * kStageTile, &tmY, &my_ybar[sl], n0 + (c + kYSlots - 1) * 32, row0);
           }
-          float v[32];
-          tc_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = nxt[j];
-          if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, nxt);
           const int col0 = n0 + c * 32;
           wait_bounded(&my_ybar[yb], (yph >> yb) & 1u);
           yph ^= 1u << yb;
@@ -618,6 +621,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           ost.release(t, &tmO, col0, row0);
           const float s = transpose_reduce32(v);
           my_colsum[col0 + lane] += s;
+        };
+        float b0[32], b1[32];
+        tmem_ld32(taddr, b0);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          tc_wait_ld();
+          if (c & 1) {
+            if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, b0);
+            body(c, b1);
+          } else {
+            if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, b1);
+            body(c, b0);
+          }
         }
       } else if constexpr (EPI == EPI_PART) {
 #pragma unroll 1

@@ -11,7 +11,8 @@ from dataclasses import dataclass
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(HERE, "libsrl.so")
+# SRL_LIB: load another build of the same library (tools/build_variant.py experiments)
+SO = os.environ.get("SRL_LIB") or os.path.join(HERE, "libsrl.so")
 
 SRL_OK, SRL_EINVAL, SRL_ECUDA, SRL_ENCCL, SRL_ENOMEM, SRL_EUNSUPPORTED, SRL_ESTATE = range(7)
 
