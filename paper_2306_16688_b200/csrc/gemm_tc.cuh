@@ -78,8 +78,9 @@ constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kBarBytes = 640;                    // 64 mbarriers + TMEM slot
 constexpr uint32_t kSmemLimit = 232448;           // 227 KB per CTA
 
+// zcols: columns of the per-warp row buffer of the loss / sample epilogues (A + 1 + H)
 __host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, int colsum_ld,
-                                                  int cg = 1) {
+                                                  int cg = 1, int zcols = 64 + 8) {
   SmemLayout L;
   const uint32_t stage_bytes = (uint32_t)(128 + bn / cg) * 64 * 2;
   L.ring = 0;
@@ -92,7 +93,7 @@ __host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, i
   L.bias = L.colsum + cs;
   const uint32_t bs = (epi == EPI_TANH || epi == EPI_LOSS || epi == EPI_SAMPLE) ? 4096 : 0;
   L.zbuf = L.bias + bs;
-  const uint32_t zs = (epi == EPI_LOSS || epi == EPI_SAMPLE) ? kEpiWarps * 64 * kZPitch * 4 : 0;
+  const uint32_t zs = (epi == EPI_LOSS || epi == EPI_SAMPLE) ? kEpiWarps * zcols * kZPitch * 4 : 0;
   L.bars = L.zbuf + zs;
   L.total = L.bars + kBarBytes;
   return L;
@@ -100,9 +101,9 @@ __host__ __device__ inline SmemLayout smem_layout(int bn, int epi, int stages, i
 
 // largest ring (<= 8 slots) that fits next to the epilogue buffers; 1 KB alignment slack and
 // 512 B for the kernel's static shared memory
-inline int gemm_stages(int bn, int epi, int colsum_ld, int cg = 1) {
+inline int gemm_stages(int bn, int epi, int colsum_ld, int cg = 1, int zcols = 64 + 8) {
   const uint32_t stage_bytes = (uint32_t)(128 + bn / cg) * 64 * 2;
-  const SmemLayout z = smem_layout(bn, epi, 0, colsum_ld, cg);
+  const SmemLayout z = smem_layout(bn, epi, 0, colsum_ld, cg, zcols);
   const int64_t avail = (int64_t)kSmemLimit - 1024 - 512 - z.total;
   const int st = (int)(avail / stage_bytes);
   return st > 8 ? 8 : st;
@@ -209,13 +210,13 @@ __device__ __forceinline__ void count_warp(unsigned long long* ctr, uint32_t n) 
 // row `lane`; on return it holds dloss_i/dz_j (j <= A), the per-sample logit gradient.
 // Compact runtime loops over the A+1 real columns only (no 64-wide unrolling).
 // Formulas: DESIGN.md §3.1 (SURVEY C-4).
-__device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, const int* act,
+__device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, const int32_t* arow,
                                               float Ahat, float lp_old, float R, float vo,
                                               bool rvalid, double (&st)[5], uint32_t& nonfinite) {
   const uint32_t lane = lane_id();
   float* z = zb + lane;                       // z[j * kZPitch]: this row's column j
   float logpi = 0.f, ent = 0.f;
-  float Hh[kMaxHeads];
+  float* Hh = z + (a.A + 1) * kZPitch;        // per-head entropies, columns A+1 .. A+H
   int off = 0;
 #pragma unroll 1
   for (int h = 0; h < a.n_heads; ++h) {
@@ -234,9 +235,9 @@ __device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, cons
       z[j * kZPitch] = l;
       hh -= __expf(l) * l;
     }
-    Hh[h] = hh;
+    Hh[h * kZPitch] = hh;
     ent += hh;
-    logpi += z[(off + act[h]) * kZPitch];
+    logpi += z[(off + (arow ? __ldg(arow + h) : 0)) * kZPitch];
     off += sz;
   }
   const float rho = expf(logpi - lp_old);
@@ -263,8 +264,8 @@ __device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, cons
 #pragma unroll 1
   for (int h = 0; h < a.n_heads; ++h) {
     const int sz = a.head_size[h];
-    const int ah = off + act[h];
-    const float H = Hh[h];
+    const int ah = off + (arow ? __ldg(arow + h) : 0);
+    const float H = Hh[h * kZPitch];
 #pragma unroll 4
     for (int j = off; j < off + sz; ++j) {
       const float l = z[j * kZPitch];
@@ -376,7 +377,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   static_assert(!ROWEPI || BN == kHeadCols, "loss/sample epilogues work on the 64-col head");
   static_assert(CG == 1 || (BN / CG) % 64 == 0 || !B_MN, "MN-major B halves must be 64-wide");
   const int STAGES = args.stages;
-  const SmemLayout SL = smem_layout(BN, EPI, STAGES, args.colsum_ld, CG);
+  const int zcols = args.A + 1 + args.n_heads;    // row buffer columns (loss / sample only)
+  const SmemLayout SL = smem_layout(BN, EPI, STAGES, args.colsum_ld, CG, zcols);
   const int rank = (CG == 2) ? (int)cluster_ctarank() : 0;   // CTA rank in the pair
   const bool leader = rank == 0;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;      // pair (cluster) index / count
@@ -650,7 +652,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
         }
       } else if constexpr (EPI == EPI_SAMPLE) {
-        float* zb = reinterpret_cast<float*>(smem + SL.zbuf) + ew * 64 * kZPitch;
+        float* zb = reinterpret_cast<float*>(smem + SL.zbuf) + ew * zcols * kZPitch;
         float z[64];
         tmem_ld32(taddr, z);
         tmem_ld32(taddr + 32, z + 32);
@@ -661,19 +663,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (rvalid) sample_row(args, zb, row);   // each lane reads only its own zb column
         __syncwarp();
       } else {  // EPI_LOSS
-        int act[kMaxHeads];
+        const int32_t* arow = nullptr;
         float Ahat = 0.f, lp = 0.f, R = 0.f, vo = 0.f;
-        for (int h = 0; h < args.n_heads; ++h) act[h] = 0;
         // padding rows (valid == 0) take no part: zero dlogits, no statistics
         const bool lvalid = rvalid && (!args.valid || __ldg(args.valid + row) != 0);
         if (lvalid) {   // per-row inputs: coalesced across lanes, issued before the TMEM wait
-          for (int h = 0; h < args.n_heads; ++h) act[h] = __ldg(args.actions + (int64_t)row * args.n_heads + h);
+          arow = args.actions + (int64_t)row * args.n_heads;
           Ahat = __ldg(args.adv + row);
           lp = __ldg(args.logp_old + row);
           R = __ldg(args.ret + row);
           if (args.v_old) vo = __ldg(args.v_old + row);
         }
-        float* zb = reinterpret_cast<float*>(smem + SL.zbuf) + ew * 64 * kZPitch;
+        float* zb = reinterpret_cast<float*>(smem + SL.zbuf) + ew * zcols * kZPitch;
         {
           float z[64];
           tmem_ld32(taddr, z);
@@ -687,7 +688,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const double mu = args.mean_std[0], sd = args.mean_std[1];
           Ahat = (float)(((double)Ahat - mu) / (sd + (double)args.adv_eps));
         }
-        ppo_rows_smem(args, zb, act, Ahat, lp, R, vo, lvalid, st, nonfinite);
+        ppo_rows_smem(args, zb, arow, Ahat, lp, R, vo, lvalid, st, nonfinite);
         __syncwarp();
         // per-CTA bias-gradient partials: lane j sums column j over the warp's 32 rows
         for (int j = lane; j <= args.A; j += 32) {

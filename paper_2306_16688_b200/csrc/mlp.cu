@@ -45,9 +45,10 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
                               const CUtensorMap& ty, GemmArgs a, int grid, cudaStream_t s) {
   auto kern = gemm_tc_kernel<BN, AM, BM, EPI, CG>;
   constexpr int E = EPI == EPI_TANH_ACC ? EPI_TANH : EPI;   // same smem layout
-  if (a.stages <= 0) a.stages = gemm_stages(BN, E, a.colsum_ld, CG);
+  const int zcols = a.A + 1 + a.n_heads;
+  if (a.stages <= 0) a.stages = gemm_stages(BN, E, a.colsum_ld, CG, zcols);
   if (a.stages < 2) return cudaErrorInvalidConfiguration;
-  const size_t smem = 1024 + smem_layout(BN, E, a.stages, a.colsum_ld, CG).total;
+  const size_t smem = 1024 + smem_layout(BN, E, a.stages, a.colsum_ld, CG, zcols).total;
   if (smem + 512 > kSmemLimit) return cudaErrorInvalidConfiguration;
   static size_t configured = 0;
   if (smem > configured) {
