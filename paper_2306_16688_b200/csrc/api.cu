@@ -213,6 +213,11 @@ struct ProfScope {
   }
 };
 
+static bool dw512_enabled() {   // opt-in: measured ~5% slower dW + finalize on the Atari shape
+  const char* e = getenv("SRL_DW512");
+  return e && e[0] == '1';
+}
+
 static int pick_bn(int n) {
   if (n % 256 == 0) return 256;
   if (n <= 64) return 64;
@@ -393,6 +398,9 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
     const int dM = (l == c->L) ? y.in : y.out;
     const int dN = (l == c->L) ? kHeadCols : y.in;
     y.bn_dw = (l == c->L) ? kHeadCols : pick_bn(dN);
+    // 512-wide dW tiles (two N = 256 MMAs sharing the dZ tile): the layer's dZ is read once
+    // per split instead of once per 256 columns (SRL_DW512=1 enables)
+    if (l < c->L && dN % 512 == 0 && dM >= 256 && dw512_enabled()) y.bn_dw = 512;
     y.cg_dw = (l < c->L && dM >= 256 && y.bn_dw >= 128) ? 2 : 1;
     y.dw_m_tiles = (dM + 128 * y.cg_dw - 1) / (128 * y.cg_dw);
     y.dw_n_tiles = (dN + y.bn_dw - 1) / y.bn_dw;
@@ -977,7 +985,9 @@ extern "C" srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int
                                      int cg, float* D, srl_stream_t stream) {
   if (M < 1 || N < 1 || K < 1 || !A || !B || !D || lda % 8 || ldb % 8 || splits < 1)
     FAIL(SRL_EINVAL, "srl_debug_gemm: bad args");
-  if (bn != 64 && bn != 128 && bn != 256) FAIL(SRL_EINVAL, "srl_debug_gemm: bn");
+  if (bn != 64 && bn != 128 && bn != 256 && bn != 512) FAIL(SRL_EINVAL, "srl_debug_gemm: bn");
+  if (bn == 512 && (cg != 2 || !a_mn || !b_mn))
+    FAIL(SRL_EINVAL, "srl_debug_gemm: bn = 512 is the CTA-pair MN-major x MN-major (dW) tile");
   if (cg != 1 && cg != 2) FAIL(SRL_EINVAL, "srl_debug_gemm: cg");
   if (cg == 2 && bn == 64) FAIL(SRL_EINVAL, "srl_debug_gemm: cg = 2 needs bn >= 128");
   if (srl_status st = require_device()) return st;

@@ -119,7 +119,11 @@ struct GemmCfg {
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TX_BYTES = CG * STAGE_BYTES;   // bytes the leader's full barrier expects
-  static constexpr int ACC_STAGES = 512 / BN;     // TMEM accumulators: 2 / 4 / 8
+  static constexpr int ACC_STAGES = 512 / BN;     // TMEM accumulators: 1 / 2 / 4 / 8
+  // BN = 512 (dW only): two N = 256 MMAs per K step share the A tile (A read once per tile)
+  static constexpr int MMA_N = BN > 256 ? 256 : BN;
+  static constexpr int N_HALVES = BN / MMA_N;
+  static constexpr int BOXES_PER_HALF = MMA_N / CG / 64;   // 64-col MN-major B boxes per CTA
   static constexpr int TMEM_COLS = 512;
 };
 
@@ -376,6 +380,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   using Cfg = GemmCfg<BN, CG>;
   static_assert(!ROWEPI || BN == kHeadCols, "loss/sample epilogues work on the 64-col head");
   static_assert(CG == 1 || (BN / CG) % 64 == 0 || !B_MN, "MN-major B halves must be 64-wide");
+  static_assert(BN <= 256 || (B_MN && EPI == EPI_PART), "BN = 512 is the dW (MN-major B, partials) tile");
   const int STAGES = args.stages;
   const int zcols = args.A + 1 + args.n_heads;    // row buffer columns (loss / sample only)
   const SmemLayout SL = smem_layout(BN, EPI, STAGES, args.colsum_ld, CG, zcols);
@@ -454,8 +459,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (!B_MN) {
             load(sb, &tmB, &full[stage], k0, n0);
           } else {
+            // box j of this CTA: MMA half h = j / BOXES_PER_HALF; within it this CTA's
+            // MMA_N / CG columns (the pair splits every N = 256 MMA's columns)
 #pragma unroll
-            for (int j = 0; j < BN / CG / 64; ++j) load(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / CG / 64; ++j) {
+              const int h = j / Cfg::BOXES_PER_HALF, jj = j % Cfg::BOXES_PER_HALF;
+              load(sb + j * 8192, &tmB, &full[stage],
+                   nt * BN + h * Cfg::MMA_N + rank * (Cfg::MMA_N / CG) + 64 * jj, k0);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -463,7 +474,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
   } else if (warp == 1 && leader) {
     // ============================ MMA issuer (the pair's leader CTA only)
-    constexpr uint32_t IDESC = umma_idesc_f16(128 * CG, BN, A_MN, B_MN);
+    constexpr uint32_t IDESC = umma_idesc_f16(128 * CG, Cfg::MMA_N, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -486,9 +497,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = A_MN ? umma_desc_sw128(a_base + k * 2048, 8192, 1024)
                                      : umma_desc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? umma_desc_sw128(b_base + k * 2048, 8192, 1024)
-                                     : umma_desc_sw128(b_base + k * 32, 16, 1024);
-            tc_mma_f16_cg<CG>(d_tmem, ad, bd, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+#pragma unroll
+            for (int h = 0; h < Cfg::N_HALVES; ++h) {
+              const uint32_t bh = b_base + h * Cfg::BOXES_PER_HALF * 8192;
+              const uint64_t bd = B_MN ? umma_desc_sw128(bh + k * 2048, 8192, 1024)
+                                       : umma_desc_sw128(bh + k * 32, 16, 1024);
+              tc_mma_f16_cg<CG>(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
           }
           tc_commit_cg<CG>(&empty[stage]);      // frees the slot in both CTAs
         }

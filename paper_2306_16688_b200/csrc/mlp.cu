@@ -96,6 +96,8 @@ cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUt
         return launch_one<64, false, false, EPI_SAMPLE, 1>(ta, tb, to, ty, args, grid, s);
       break;
     case EPI_PART:
+      if (a_mn && b_mn && bn == 512 && cg == 2)
+        return launch_one<512, true, true, EPI_PART, 2>(ta, tb, to, ty, args, grid, s);
       if (!a_mn && !b_mn) { SRL_DISPATCH_BN(false, false, EPI_PART, cg) }
       if (!a_mn && b_mn) { SRL_DISPATCH_BN(false, true, EPI_PART, cg) }
       if (a_mn && !b_mn) { SRL_DISPATCH_BN(true, false, EPI_PART, cg) }

@@ -57,3 +57,17 @@ def test_gemm_k_not_multiple_of_8_rows_padded():
     ref = A[:, :K].float() @ B[:, :K].float().t()
     torch.cuda.synchronize()
     assert (D - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("M,N,K,splits", [(512, 512, 4096, 7), (256, 1024, 640, 1), (384, 512, 1000, 3)])
+def test_gemm_dw512_pair_tile(M, N, K, splits):
+    """The dW tile: 512 columns per CTA pair as two N = 256 MMAs sharing the A tile (MN-major
+    A and B, split-K partials), ragged M (384 = 1.5 pair tiles) and K."""
+    import paper_2306_16688_b200 as P
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn((K, M), generator=g, device="cuda").half()
+    B = torch.randn((K, N), generator=g, device="cuda").half()
+    D = P.debug_gemm(A, 1, B, 1, M, N, K, bn=512, splits=splits, cg=2)
+    ref = _ref(A, 1, B, 1)
+    torch.cuda.synchronize()
+    assert torch.allclose(D, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
