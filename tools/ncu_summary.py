@@ -27,13 +27,15 @@ def launches(path, rnd, config="atari"):
     os.makedirs(PROF, exist_ok=True)
     shutil.copy(path, os.path.join(PROF, f"{rnd}_launches.csv"))
     txt = open(path).read()
-    rows = list(csv.DictReader(io.StringIO(txt[txt.index('"ID"'):])))
+    body = "\n".join(l for l in txt[txt.index('"ID"'):].splitlines() if l.startswith('"'))
+    rows = list(csv.DictReader(io.StringIO(body)))
     by = collections.OrderedDict()
     for r in rows:
         by.setdefault(int(r["ID"]), {"kernel": r["Kernel Name"]})[r["Metric Name"]] = float(
             r["Metric Value"].replace(",", ""))
     recs = list(by.values())
-    start = next(i for i, r in enumerate(recs) if r["kernel"].startswith("void gae_kernel"))
+    starts = [i for i, r in enumerate(recs) if ("gae_kernel" in r["kernel"])]
+    start = starts[min(3, len(starts) - 1)]          # the first step after 3 warm-up steps
     step = recs[start:start + len(STEP_ORDER)]
     tot = sum(r["gpu__time_duration.sum"] for r in step)
     lines = [f"# {rnd}: ncu launch list, one `srl_ppo_train_step` ({config}-shaped, 1 x B200)", "",
