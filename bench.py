@@ -397,6 +397,7 @@ def main_ours(args, world, rank, local):
         "config": {"workload": cfg.name, "T": cfg.T, "B_per_rank": cfg.B, "obs_dim": cfg.obs_dim,
                    "hidden": list(cfg.hidden), "heads": list(cfg.heads), "samples_per_step": N,
                    "frames_per_step": N * cfg.frame_skip, "parallelism": f"dp{world}",
+                   "grad_allreduce": ctx.comm_path,
                    "epochs": max(1, args.epochs), "minibatches": max(1, args.minibatches),
                    "value_clip": args.value_clip, "max_grad_norm": args.max_grad_norm,
                    "l2": "no flush: per-step working set > L2 (obs %.0f MB + activations %.0f MB + "

@@ -233,6 +233,12 @@ srl_status srl_batch_upload(srl_ctx* ctx, int slot, int T, int B, const float* r
 srl_status srl_ppo_train_step_slot(srl_ctx* ctx, int slot, int64_t n_global,
                                    srl_ppo_stats* stats_out, srl_stream_t stream);
 
+/* How srl_ppo_step reduces the gradient bucket across ranks (a6): 0 = world 1 (none),
+ * 1 = NCCL allreduce, 2 = one-shot allreduce over NVLink peer memory (CUDA IPC-mapped buckets
+ * of all ranks summed in rank order; the default when every rank could map every peer;
+ * SRL_P2P_AR=0 selects NCCL).  -1 on a null ctx. */
+int srl_ppo_comm_path(srl_ctx* ctx);
+
 /* a6: in-place allreduce over the ctx's ranks of a device f32 buffer (SPEC reduce_gradients
  * S:L505-513): op 0 = sum, op 1 = mean.  world == 1: identity (op 1 leaves values as is). */
 srl_status srl_allreduce_grads(srl_ctx* ctx, float* buf, int64_t count, int op,

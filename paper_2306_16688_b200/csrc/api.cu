@@ -25,6 +25,12 @@ static bool ar_overlap() {
   return on == 1;
 }
 
+// SRL_P2P_AR=0: gradient allreduce through NCCL instead of the NVLink peer-memory kernel
+static bool p2p_ar_enabled() {
+  const char* e = getenv("SRL_P2P_AR");
+  return !(e && e[0] == '0');
+}
+
 static bool tanh_accurate() {
   static int on = -1;
   if (on < 0) {
@@ -174,6 +180,14 @@ struct srl_ctx {
   double* gn = nullptr;
   unsigned int* gn_counter = nullptr;
   double* gn_norm() const { return gn + kGradNormBlocks; }
+  // a6 over NVLink peer memory (world > 1): exposed double-buffered bucket + flags, peers' maps
+  bool p2p = false;
+  float* xbuf = nullptr;                       // [2][P + 8]
+  unsigned long long* xflags = nullptr;        // [kMaxPeers]
+  P2PPeers peers{};
+  std::vector<void*> ipc_opened;
+  unsigned long long epoch = 0, mepoch = 0;
+  int64_t xstride() const { return (P + 8 + 63) / 64 * 64; }   // 256-B aligned halves
   float* gn_coef() const { return reinterpret_cast<float*>(gn + kGradNormBlocks + 1); }
 };
 
@@ -258,6 +272,7 @@ static void free_ctx(srl_ctx* c) {
   for (cudaEvent_t e : {c->ev_early, c->ev_late, c->ev_comm})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);
   delete c;
@@ -447,6 +462,43 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
       return SRL_ENCCL;
     }
   }
+  if (world > 1 && world <= kMaxPeers && p2p_ar_enabled()) {
+    // exchange CUDA IPC handles of the exposed bucket and flags (one NCCL all-gather)
+    if ((st = dalloc(c, &c->xbuf, sizeof(float) * 2 * c->xstride()))) return bail(st);
+    if ((st = dalloc(c, &c->xflags, kSyncBytes))) return bail(st);
+    cudaIpcMemHandle_t h[2];
+    bool ok = cudaIpcGetMemHandle(&h[0], c->xbuf) == cudaSuccess &&
+              cudaIpcGetMemHandle(&h[1], c->xflags) == cudaSuccess;
+    uint8_t* dh = nullptr;
+    std::vector<uint8_t> all((size_t)world * sizeof(h));
+    if (ok) ok = cudaMalloc(&dh, all.size() + sizeof(h)) == cudaSuccess;
+    if (ok) ok = cudaMemcpy(dh + all.size(), h, sizeof(h), cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok) ok = ncclAllGather(dh + all.size(), dh, sizeof(h), ncclUint8, c->comm, 0) == ncclSuccess;
+    if (ok) ok = cudaMemcpy(all.data(), dh, all.size(), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (dh) cudaFree(dh);
+    for (int r = 0; ok && r < world; ++r) {
+      if (r == rank) { c->peers.x[r] = c->xbuf; c->peers.flag[r] = c->xflags; continue; }
+      cudaIpcMemHandle_t ph[2];
+      std::memcpy(ph, all.data() + (size_t)r * sizeof(h), sizeof(h));
+      void *px = nullptr, *pf = nullptr;
+      ok = cudaIpcOpenMemHandle(&px, ph[0], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      if (ok) c->ipc_opened.push_back(px);
+      if (ok) ok = cudaIpcOpenMemHandle(&pf, ph[1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      if (ok) c->ipc_opened.push_back(pf);
+      c->peers.x[r] = static_cast<float*>(px);
+      c->peers.flag[r] = static_cast<unsigned long long*>(pf);
+    }
+    // every rank must agree: the peer path is used only if it could be set up everywhere
+    int mine = ok ? 1 : 0, *dflag = nullptr, every = 0;
+    if (cudaMalloc(&dflag, sizeof(int)) == cudaSuccess) {
+      cudaMemcpy(dflag, &mine, sizeof(int), cudaMemcpyHostToDevice);
+      if (ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, c->comm, 0) == ncclSuccess)
+        cudaMemcpy(&every, dflag, sizeof(int), cudaMemcpyDeviceToHost);
+      cudaFree(dflag);
+    }
+    cudaGetLastError();
+    c->p2p = every == 1;
+  }
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     set_error(std::string("srl_ppo_create: ") + cudaGetErrorString(e));
@@ -455,6 +507,12 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   }
   *out = c;
   return SRL_OK;
+}
+
+extern "C" int srl_ppo_comm_path(srl_ctx* c) {
+  if (!c) return -1;
+  if (c->world == 1) return 0;
+  return (c->p2p && !ar_overlap()) ? 2 : 1;
 }
 
 extern "C" srl_status srl_ppo_destroy(srl_ctx* ctx) {
@@ -693,6 +751,13 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     colsum_parts[l - 1] = grid;
     return st;
   };
+  // a6 through NVLink peer memory: finalise and extras write this rank's bucket into its
+  // exposed buffer (parity of the step's epoch) and the allreduce kernel sums all ranks' into
+  // c->grads.  Otherwise they write c->grads directly (NCCL allreduce in place, or world 1).
+  const bool p2p = apply && c->world > 1 && c->p2p && !ar_overlap();
+  const unsigned long long epoch = p2p ? c->epoch + 1 : 0;
+  const int64_t xoff = (int64_t)(epoch & 1ull) * c->xstride();
+  float* bk = p2p ? c->xbuf + xoff : c->grads;
   // finalise (1/N-scaled split/column-sum reduction into the bucket) layers [lo, hi]
   auto finalize_layers = [&](int lo, int hi) -> srl_status {
     SegTable all = make_segs(c, splits, colsum_parts), t{};
@@ -703,7 +768,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
       rd += 4.0 * splits[l] * c->lay[l].out * c->lay[l].in + 4.0 * colsum_parts[l] * c->lay[l].colsum_ld;
     }
     ProfScope ps(c, s, "grad_finalize", 0.0, rd);
-    CK(launch_finalize_grads(t, c->P, inv_n, c->grads, c->counters, s));
+    CK(launch_finalize_grads(t, c->P, inv_n, bk, c->counters, s));
     return SRL_OK;
   };
   // a6 overlap: once dW of layer 1 is done, layers 1..L (a contiguous bucket tail) are final;
@@ -738,7 +803,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   }
   SegTable segs = make_segs(c, splits, colsum_parts);
   if (srl_status st = overlap ? finalize_layers(0, 0) : finalize_layers(0, L)) return st;
-  CK(launch_extras(c->P, inv_n, c->stats_part, grid_loss, c->counters, c->grads, s));
+  CK(launch_extras(c->P, inv_n, c->stats_part, grid_loss, c->counters, bk, s));
   if (apply) {
     // ---------------- a6: gradient allreduce (bucket already scaled by 1/N_global)
     if (overlap) {
@@ -754,6 +819,11 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
       }
       CK(cudaEventRecord(c->ev_comm, c->comm_stream));
       CK(cudaStreamWaitEvent(s, c->ev_comm, 0));
+    }
+    else if (p2p) {
+      ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8) * c->world);
+      c->epoch = epoch;
+      CK(launch_p2p_allreduce(c->peers, c->world, c->rank, xoff, c->P + 8, epoch, c->grads, s));
     }
     else if (c->world > 1) {
       ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8));
@@ -805,9 +875,14 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
   if (c->world > 1) {
     // a2 (global): all-gather the ranks' {n, mean, M2} and merge them in rank order
     ProfScope ps(c, s, "adv_norm", 0.0, 24.0 * c->world);
-    double* gathered = c->norm_scratch;
-    CKN(ncclAllGather(c->gae_stats, gathered, 3, ncclDouble, c->comm, s));
-    CK(launch_merge_moments(gathered, c->world, nullptr, c->mean_std, c->cfg.adv_unbiased, s));
+    if (c->p2p && !ar_overlap()) {
+      CK(launch_p2p_moments(c->peers, c->world, c->rank, ++c->mepoch, c->gae_stats, c->mean_std,
+                            c->cfg.adv_unbiased, s));
+    } else {
+      double* gathered = c->norm_scratch;
+      CKN(ncclAllGather(c->gae_stats, gathered, 3, ncclDouble, c->comm, s));
+      CK(launch_merge_moments(gathered, c->world, nullptr, c->mean_std, c->cfg.adv_unbiased, s));
+    }
   }
   // a3..a7 once per minibatch per epoch (NEXT-3, reading R-M); E = M = 1 is one update
   const int E = c->cfg.epochs, M = c->cfg.minibatches;

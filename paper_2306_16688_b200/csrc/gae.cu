@@ -286,12 +286,10 @@ cudaError_t launch_moments(const float* x, int64_t n, double* part, cudaStream_t
   return launch_k(moments_kernel, dim3(kMomentBlocks), dim3(256), 0, s, 1, x, n, part);
 }
 
-// merge partial triples in index order (contiguous ranges per thread, then a fixed tree)
-__global__ void __launch_bounds__(256) merge_moments_kernel(const double* __restrict__ part,
-                                                            int count, double* out,
-                                                            double* mean_std, int unbiased) {
-  griddep_wait();
-  griddep_launch();
+// merge partial triples in index order (contiguous ranges per thread, then a fixed tree);
+// 256 threads
+__device__ void merge_parts_block(const double* part, int count, double* out, double* mean_std,
+                                  int unbiased) {
   __shared__ double sn[256], sm[256], sq[256];
   const int t = threadIdx.x;
   const int lo = (int)((int64_t)count * t / 256), hi = (int)((int64_t)count * (t + 1) / 256);
@@ -315,6 +313,59 @@ __global__ void __launch_bounds__(256) merge_moments_kernel(const double* __rest
       mean_std[1] = denom > 0 ? sqrt(sq[0] / denom) : 0.0;
     }
   }
+}
+
+__global__ void __launch_bounds__(256) merge_moments_kernel(const double* __restrict__ part,
+                                                            int count, double* out,
+                                                            double* mean_std, int unbiased) {
+  griddep_wait();
+  griddep_launch();
+  merge_parts_block(part, count, out, mean_std, unbiased);
+}
+
+// a2 across ranks over NVLink peer memory (the NCCL all-gather's replacement when the peer
+// buckets are mapped): thread r stores this rank's {n, mean, M2} into rank r's slot for this
+// rank (parity of the epoch), fences, release-stores the epoch into rank r's flag; then waits
+// for every rank's flag here and merges the world triples in rank order with the same
+// merge_parts_block as the NCCL path (identical result on every rank and on both paths).
+__device__ __forceinline__ void st_rel_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(256) p2p_moments_kernel(const P2PPeers pe, int world, int rank,
+                                                          unsigned long long epoch,
+                                                          const double* __restrict__ local,
+                                                          double* mean_std, int unbiased) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ double tri[kMaxPeers * 3];
+  const int t = threadIdx.x;
+  const int par = (int)(epoch & 1ull);
+  if (t < world) {
+    double* dst = p2p_slots(pe.flag[t]) + (par * kMaxPeers + rank) * 4;
+    dst[0] = local[0]; dst[1] = local[1]; dst[2] = local[2];
+    __threadfence_system();
+    st_rel_sys(p2p_mflags(pe.flag[t]) + rank, epoch);
+    const unsigned long long* f = p2p_mflags(pe.flag[rank]) + t;
+    long long t0 = clock64();
+    while (ld_acq_sys(f) < epoch)
+      if (clock64() - t0 > (1ll << 33)) __trap();   // ~4 s: a missing rank is an error
+    const volatile double* src = p2p_slots(pe.flag[rank]) + (par * kMaxPeers + t) * 4;
+    tri[3 * t] = src[0]; tri[3 * t + 1] = src[1]; tri[3 * t + 2] = src[2];
+  }
+  __syncthreads();
+  merge_parts_block(tri, world, nullptr, mean_std, unbiased);
+}
+
+cudaError_t launch_p2p_moments(const P2PPeers& pe, int world, int rank, unsigned long long epoch,
+                               const double* local, double* mean_std, int unbiased, cudaStream_t s) {
+  return launch_k(p2p_moments_kernel, dim3(1), dim3(256), 0, s, 1, pe, world, rank, epoch, local,
+                  mean_std, unbiased);
 }
 
 cudaError_t launch_merge_moments(const double* part, int count, double* out, double* mean_std,

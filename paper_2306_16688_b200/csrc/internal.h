@@ -111,6 +111,25 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
                         const float* bucket, const int64_t* t_dev, float lr, float b1,
                         float b2, float eps, cudaStream_t s, const float* coef = nullptr);
 constexpr int kGradNormBlocks = 296;   // 2 x 148 SMs
+// a6 over NVLink peer memory (world <= 8 on one node): every rank's exposed bucket (double
+// buffered by step parity) and flag array, mapped into this process with CUDA IPC
+constexpr int kMaxPeers = 8;
+struct P2PPeers {
+  float* x[kMaxPeers];                    // rank r's exposed buckets [2][count]
+  unsigned long long* flag[kMaxPeers];    // rank r's flags [kMaxPeers]: flag[src] = src's epoch
+};
+// layout of every rank's IPC-mapped sync block (flag[r] points at rank r's): [0, 8) gradient
+// flags, [8, 16) moments flags, then doubles [2 parity][kMaxPeers][4] moment slots
+__host__ __device__ inline unsigned long long* p2p_mflags(unsigned long long* base) { return base + kMaxPeers; }
+__host__ __device__ inline double* p2p_slots(unsigned long long* base) {
+  return reinterpret_cast<double*>(base + 2 * kMaxPeers);
+}
+constexpr size_t kSyncBytes = sizeof(unsigned long long) * 2 * kMaxPeers + sizeof(double) * 2 * kMaxPeers * 4;
+cudaError_t launch_p2p_moments(const P2PPeers& pe, int world, int rank, unsigned long long epoch,
+                               const double* local, double* mean_std, int unbiased, cudaStream_t s);
+cudaError_t launch_p2p_allreduce(const P2PPeers& pe, int world, int rank, int64_t off,
+                                 int64_t count, unsigned long long epoch, float* out,
+                                 cudaStream_t s);
 cudaError_t launch_gradnorm(const float* bucket, int64_t P, double* part, unsigned int* counter,
                             float max_norm, double* norm_out, float* coef_out, cudaStream_t s);
 cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s);

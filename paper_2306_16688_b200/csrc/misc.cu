@@ -289,6 +289,68 @@ __global__ void __launch_bounds__(256) gradnorm_kernel(const float* __restrict__
   }
 }
 
+// a6 as a one-shot allreduce over NVLink peer memory.  The finalise / extras kernels of this
+// step wrote this rank's 1/N-scaled bucket into its exposed buffer x[rank][parity]; here
+// block 0 publishes it (system fence, then a release store of the step's epoch into every
+// rank's flag slot for this rank), every block waits until all ranks have published, then
+// sums the world buffers element by element in rank order 0..world-1 straight from the
+// peers' HBM (ld.global.cg: peer loads bypass the remote L2 and must not hit a stale L1 line).
+// Same order on every rank -> bit-identical sums everywhere (replicated Adam stays in sync).
+// Double buffering by epoch parity is safe: rank A cannot start writing step k+2 into a
+// buffer before rank B has read it for step k, because A's step k+1 waits for B's step k+1
+// publication, which B issues only after finishing step k.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(256) p2p_allreduce_kernel(const P2PPeers pe, int world, int rank,
+                                                            int64_t off, int64_t count,
+                                                            unsigned long long epoch,
+                                                            float* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
+  if (blockIdx.x == 0 && threadIdx.x < world) {
+    __threadfence_system();
+    st_release_sys(pe.flag[threadIdx.x] + rank, epoch);
+  }
+  if (threadIdx.x < world) {
+    const unsigned long long* f = pe.flag[rank] + threadIdx.x;
+    long long t0 = clock64();
+    while (ld_acquire_sys(f) < epoch) {
+      if (clock64() - t0 > (1ll << 33)) __trap();   // ~4 s: a missing rank is an error, not a hang
+    }
+  }
+  __syncthreads();
+  const int64_t nq = count >> 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    float4 s = __ldcg(reinterpret_cast<const float4*>(pe.x[0] + off) + q);
+    for (int r = 1; r < world; ++r) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(pe.x[r] + off) + q);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    reinterpret_cast<float4*>(out)[q] = s;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = 4 * nq + threadIdx.x; i < count; i += blockDim.x) {
+      float s = __ldcg(pe.x[0] + off + i);
+      for (int r = 1; r < world; ++r) s += __ldcg(pe.x[r] + off + i);
+      out[i] = s;
+    }
+}
+
+cudaError_t launch_p2p_allreduce(const P2PPeers& pe, int world, int rank, int64_t off,
+                                 int64_t count, unsigned long long epoch, float* out,
+                                 cudaStream_t s) {
+  return launch_k(p2p_allreduce_kernel, dim3(2 * num_sms()), dim3(256), 0, s, 1, pe, world, rank,
+                  off, count, epoch, out);
+}
+
 cudaError_t launch_gradnorm(const float* bucket, int64_t P, double* part, unsigned int* counter,
                             float max_norm, double* norm_out, float* coef_out, cudaStream_t s) {
   return launch_k(gradnorm_kernel, dim3(kGradNormBlocks), dim3(256), 0, s, 1, bucket, P, part,

@@ -20,7 +20,8 @@ SRL_OK, SRL_EINVAL, SRL_ECUDA, SRL_ENCCL, SRL_ENOMEM, SRL_EUNSUPPORTED, SRL_ESTA
 EXPORTS = ("srl_last_error", "srl_abi_version", "srl_gae", "srl_adv_norm", "srl_nccl_unique_id",
            "srl_ppo_create", "srl_ppo_destroy", "srl_ppo_params", "srl_ppo_adam_state",
            "srl_ppo_load_params", "srl_ppo_step", "srl_ppo_train_step", "srl_batch_upload",
-           "srl_ppo_train_step_slot", "srl_policy_rollout", "srl_allreduce_grads", "srl_prof_enable",
+           "srl_ppo_train_step_slot", "srl_policy_rollout", "srl_ppo_comm_path",
+           "srl_allreduce_grads", "srl_prof_enable",
            "srl_prof_reset", "srl_prof_count", "srl_prof_read", "srl_debug_gemm")
 
 
@@ -82,6 +83,8 @@ def lib():
                                      vp, vp]
     L.srl_batch_upload.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp]
     L.srl_ppo_train_step_slot.argtypes = [vp, C.c_int, i64, vp, vp]
+    L.srl_ppo_comm_path.argtypes = [vp]
+    L.srl_ppo_comm_path.restype = C.c_int
     L.srl_policy_rollout.argtypes = [vp, i64, vp, vp, C.c_uint64, C.c_int, vp, vp, vp, vp]
     L.srl_allreduce_grads.argtypes = [vp, vp, i64, C.c_int, vp]
     L.srl_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
@@ -348,6 +351,11 @@ class PPOContext:
                                         int(bool(deterministic)), _ptr(actions), _ptr(logp),
                                         _ptr(value), _stream(stream)))
         return actions, logp, value
+
+    @property
+    def comm_path(self) -> str:
+        """a6 path of srl_ppo_step: 'none' (world 1), 'nccl' or 'nvlink-p2p'."""
+        return {0: "none", 1: "nccl", 2: "nvlink-p2p"}[lib().srl_ppo_comm_path(self.handle)]
 
     def allreduce_grads(self, buf: torch.Tensor, op: int = 0, stream=None):
         _cuda(buf, torch.float32, "buf")

@@ -20,8 +20,9 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, p2p="1", steps=1):
     import sys
+    os.environ["SRL_P2P_AR"] = p2p
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -42,15 +43,37 @@ def _worker(rank, world, port, q):
         d = to_dev(sh)
         st = P.decode_stats(ctx.train_step(cfg.N, d["rewards"], d["values"], d["dones"], d["obs"],
                                            d["actions"], d["logp_old"]))
+        g1 = ctx.grads().cpu().numpy()
+        for _ in range(steps - 1):       # both buffer parities of the peer path, epochs advance
+            ctx.train_step(cfg.N, d["rewards"], d["values"], d["dones"], d["obs"], d["actions"],
+                           d["logp_old"])
         torch.cuda.synchronize()
-        q.put((rank, st, ctx.params().cpu().numpy(), ctx.grads().cpu().numpy()))
+        q.put((rank, st, ctx.params().cpu().numpy(), g1, ctx.comm_path))
         ctx.close()
     finally:
         dist.destroy_process_group()
 
 
+def _run(world, p2p="1", steps=1):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, p2p, steps)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
 @pytest.mark.parametrize("world", [2, 4])
-def test_nccl_ranks_match_full_batch(world):
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_nccl_ranks_match_full_batch(world, p2p):
+    """p2p = 1: the gradient bucket is reduced by the NVLink peer-memory kernel (default);
+    p2p = 0: by NCCL.  Both must give the full-batch result on every rank."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     import sys
@@ -58,17 +81,8 @@ def test_nccl_ranks_match_full_batch(world):
     import oracle
     import synth
     from ppo_harness import grad_errors, make_inputs
-    import torch.multiprocessing as mp
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda r: r[0])
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    res = _run(world, p2p)
+    assert res[0][4] == ("nvlink-p2p" if p2p == "1" else "nccl")
     cfg = synth.get_config("gfootball").with_(B=16)
     params, full = make_inputs(cfg, seed=3)
     o = oracle.ppo_step(cfg, params, [full], apply=False)
@@ -80,3 +94,23 @@ def test_nccl_ranks_match_full_batch(world):
     G = res[0][3][:cfg.n_params].astype(np.float64)
     errs = grad_errors(cfg, G, o["grad"])
     assert all(v[0] <= 2e-3 and v[1] <= 2e-3 for v in errs.values()), errs
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_allreduce_equals_nccl_over_steps(world):
+    """Three steps (both exposed-buffer parities): the peer-memory reduction (rank-order sum)
+    and NCCL's agree to fp32 rounding on the first gradient and on the final parameters."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    a = _run(world, "1", steps=3)
+    b = _run(world, "0", steps=3)
+    assert a[0][4] == "nvlink-p2p" and b[0][4] == "nccl"
+    for r in a[1:]:
+        assert np.array_equal(r[2], a[0][2])
+    ga, gb = a[0][3].astype(np.float64), b[0][3].astype(np.float64)
+    assert np.linalg.norm(ga - gb) <= 1e-6 * np.linalg.norm(gb)
+    # Adam normalises each entry: a gradient entry within rounding of 0 may take either sign,
+    # moving that parameter by up to 2 lr per step; everything else agrees to rounding
+    d = np.abs(a[0][2].astype(np.float64) - b[0][2].astype(np.float64))
+    assert d.max() <= 2 * 3e-4 * 3 + 1e-6 and np.mean(d > 1e-5) <= 1e-3
+    assert a[0][1]["step"] == 1 and b[0][1]["step"] == 1
