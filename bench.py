@@ -7,7 +7,8 @@ forward -> loss -> backward -> allreduce -> Adam) on synthetic Atari-shaped batc
 
 Scaling is weak: every rank trains its own full config-shaped shard (T x B columns); the
 ranks' shards are disjoint column blocks of one global batch, normalised globally and
-reduced by one NCCL allreduce of the gradient bucket per step.  Rank 0 prints ONE JSON line.
+reduced by one allreduce of the gradient bucket per step (the library's NVLink peer-memory
+kernel by default, NCCL with SRL_P2P_AR=0).  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -379,7 +380,9 @@ def main_ours(args, world, rank, local):
     # stats (NCCL's kernels are not counted)
     L = len(cfg.hidden)
     # per update; epochs x minibatches updates per step (NEXT-3), + grad_norm when clipping
-    per_update = (L + 1 + (L + 1) + L) + 3 + 1 + 1 + (1 if args.max_grad_norm > 0 else 0)
+    p2p = ctx.comm_path == "nvlink-p2p"      # the allreduce is then one of our kernels
+    per_update = ((L + 1 + (L + 1) + L) + 3 + 1 + 1 + (1 if args.max_grad_norm > 0 else 0)
+                  + (1 if p2p else 0))
     updates = max(1, args.epochs) * max(1, args.minibatches)
     per_step = 1 + (1 if world > 1 else 0) + per_update * updates
     cpu = None
