@@ -103,25 +103,30 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
     const int t0 = sc * SC + ch * TC;
     float delta[TC], c[TC], vt[TC];
     uint32_t vbits = 0;                      // bit i: entry t0 + i enters the moments
+    // all loads of the chunk first (clamped in-bounds addresses, no per-row branches), so
+    // the TC rows' DRAM round trips overlap; then the arithmetic with selects only
+    float rr[TC], v0[TC], v1[TC], tq[TC];
+    uint32_t fl[TC], vm[TC];
 #pragma unroll
     for (int i = 0; i < TC; ++i) {
-      const int t = t0 + i;
-      if (col_ok && t < T) {
-        const int64_t e = (int64_t)t * ld + b;
-        const float rr = __ldg(r + e);
-        const float v0 = __ldg(v + e);
-        const uint8_t f = __ldg(d + e);
-        float boot = __ldg(v + e + ld);      // v_{t+1}
-        if (f) boot = (tv && !(f & 1)) ? __ldg(tv + e) : 0.f;
-        delta[i] = rr + gamma * boot - v0;
-        c[i] = f ? 0.f : gl;
-        vt[i] = v0;
-        if (!vmask || __ldg(vmask + e)) vbits |= 1u << i;
-      } else {
-        delta[i] = 0.f;   // rows past T: identity step
-        c[i] = 1.f;
-        vt[i] = 0.f;
-      }
+      const int t = min(t0 + i, T - 1);
+      const int64_t e = (int64_t)t * ld + (col_ok ? b : 0);
+      rr[i] = __ldg(r + e);
+      v0[i] = __ldg(v + e);
+      v1[i] = __ldg(v + e + ld);             // v_{t+1}
+      fl[i] = __ldg(d + e);
+      tq[i] = tv ? __ldg(tv + e) : 0.f;
+      vm[i] = vmask ? __ldg(vmask + e) : 1u;
+    }
+#pragma unroll
+    for (int i = 0; i < TC; ++i) {
+      const bool in = col_ok && t0 + i < T;
+      const uint32_t f = fl[i];
+      const float boot = f ? ((tv && !(f & 1u)) ? tq[i] : 0.f) : v1[i];
+      delta[i] = in ? rr[i] + gamma * boot - v0[i] : 0.f;   // rows past T: identity step
+      c[i] = in ? (f ? 0.f : gl) : 1.f;
+      vt[i] = in ? v0[i] : 0.f;
+      if (in && vm[i]) vbits |= 1u << i;
     }
     // pass 1: chunk summary with A_end = 0
     float a = 0.f, P = 1.f;
