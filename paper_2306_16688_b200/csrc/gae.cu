@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256) p2p_moments_kernel(const P2PPeers pe, int
     const unsigned long long* f = p2p_mflags(pe.flag[rank]) + t;
     long long t0 = clock64();
     while (ld_acq_sys(f) < epoch)
-      if (clock64() - t0 > (1ll << 33)) __trap();   // ~4 s: a missing rank is an error
+      if (clock64() - t0 > (1ll << 35)) __trap();   // ~17 s: a missing rank is an error
     const volatile double* src = p2p_slots(pe.flag[rank]) + (par * kMaxPeers + t) * 4;
     tri[3 * t] = src[0]; tri[3 * t + 1] = src[1]; tri[3 * t + 2] = src[2];
   }

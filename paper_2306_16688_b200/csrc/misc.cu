@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256) p2p_allreduce_kernel(const P2PPeers pe, i
     const unsigned long long* f = pe.flag[rank] + threadIdx.x;
     long long t0 = clock64();
     while (ld_acquire_sys(f) < epoch) {
-      if (clock64() - t0 > (1ll << 33)) __trap();   // ~4 s: a missing rank is an error, not a hang
+      if (clock64() - t0 > (1ll << 35)) __trap();   // ~17 s: a missing rank is an error, not a hang
     }
   }
   __syncthreads();
