@@ -45,7 +45,7 @@ typedef enum srl_status {
 } srl_status;
 
 const char* srl_last_error(void);
-int srl_abi_version(void);                    /* 2 (1 + NEXT-3 fields) */
+int srl_abi_version(void);                    /* 2: round-1 ABI + NEXT-2/NEXT-3 arguments */
 
 /* ---------------------------------------------------------------- a1: GAE
  * Generalised advantage estimation over time-major columns (SPEC.md S:L593-601,
@@ -55,7 +55,9 @@ int srl_abi_version(void);                    /* 2 (1 + NEXT-3 fields) */
  *     A_T = 0,   R_t = A_t + v_t.
  * d_t = 1 means the episode ended AT transition t: it cuts v_{t+1} and A_{t+1}.
  *   rewards  device f32 [T][ld]          values device f32 [T+1][ld] (row T = bootstrap)
- *   dones    device u8  [T][ld] (0/1)    adv_out device f32 [T][ld]   ret_out f32 [T][ld] or NULL
+ *   dones    device u8  [T][ld] flags: 0 = continue, nonzero = episode ended at t (bit 1 with
+ *            bit 0 clear = time limit, see trunc_values)
+ *   adv_out  device f32 [T][ld]          ret_out f32 [T][ld] or NULL
  *   trunc_values device f32 [T][ld] or NULL (NEXT-3, DESIGN.md §3.5 reading R-T, SURVEY C-A2):
  *             a dones byte with bit 0 clear and bit 1 set marks a time-limit truncation at t:
  *             the recursion is still cut but delta_t = r_t + gamma * trunc_values_t - v_t.
