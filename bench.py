@@ -5,8 +5,9 @@ forward -> loss -> backward -> allreduce -> Adam) on synthetic Atari-shaped batc
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config atari] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
-Scaling is weak: every rank trains its own full config-shaped shard (T x B columns); the
-ranks' shards are disjoint column blocks of one global batch, normalised globally and
+Scaling (N > 1): strong by default -- the config's batch is the global batch, split into B/K
+column blocks, one per rank (SURVEY C-A16); the other mode (weak: a full config-sized shard per
+rank) is measured in the same run under "alt_scaling".  Shards are normalised globally and
 reduced by one allreduce of the gradient bucket per step (the library's NVLink peer-memory
 kernel by default, NCCL with SRL_P2P_AR=0).  Rank 0 prints ONE JSON line.
 """
@@ -49,12 +50,16 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps (capped at 100)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     # NEXT-3 PPO variants (defaults = the BASELINE workload: one update per batch, no clipping)
     ap.add_argument("--epochs", type=int, default=1)
     ap.add_argument("--minibatches", type=int, default=1)
     ap.add_argument("--value-clip", type=float, default=0.0)
     ap.add_argument("--max-grad-norm", type=float, default=0.0)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="default: strong for N > 1 (the config batch split B/K, SURVEY C-A16)")
+    ap.add_argument("--no-alt-scaling", action="store_true")
+    ap.add_argument("--no-all-configs", action="store_true")
     return ap.parse_args()
 
 
@@ -121,63 +126,164 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle
-def time_oracle(cfg, budget_s, params=None):
-    """The oracle (as it stands, 1 thread) on a bounded sample of the workload: T x B' columns
-    with B' chosen so the run takes about budget_s.  Returns (samples/s, n, B', seconds)."""
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_sample(cfg, Bp):
+    import synth
+    c = cfg.with_(B=Bp * cfg.agents)
+    b = synth.make_batch(c, seed=0)
+    b["logp_old"] = synth.logp_old_uniform_policy(c, b["xi"])
+    return c, b
+
+
+def time_oracle(cfg, budget_s, threads=1, params=None, nx=None):
+    """The oracle (as it stands; threads > 1 = its all-core block driver) on a bounded sample of
+    the workload: T x B' columns, B' sized so one step takes about budget_s.
+    Returns (samples/s, n, B', seconds)."""
     import oracle
     import synth
     if params is None:
         params = synth.make_params(cfg, 0)
+    nx = nx or {}
 
     def run(Bp):
-        c = cfg.with_(B=Bp * cfg.agents)
-        b = synth.make_batch(c, seed=0)
-        b["logp_old"] = synth.logp_old_uniform_policy(c, b["xi"])
+        c, b = oracle_sample(cfg, Bp)
         t = time.perf_counter()
-        oracle.ppo_step(c, params, [b], apply=True)
+        oracle.ppo_step(c, params, [b], apply=True, threads=threads, **nx)
         return time.perf_counter() - t, b["n"]
 
-    t1, n1 = run(1)
-    Bp = int(max(1, min(cfg.B // cfg.agents, round(budget_s / max(t1, 1e-6)))))
-    if Bp == 1:
-        return n1 / t1, n1, 1, t1
+    Bp0 = max(1, min(cfg.B // cfg.agents, threads))
+    t1, n1 = run(Bp0)
+    Bp = int(max(1, min(cfg.B // cfg.agents, round(Bp0 * budget_s / max(t1, 1e-6)))))
+    if Bp == Bp0:
+        return n1 / t1, n1, Bp0, t1
     t, n = run(Bp)
     return n / t, n, Bp, t
 
 
+def cpu_baselines(cfg, budget_s):
+    """1 thread (the parity build) and all host cores (block driver), SURVEY.md §8(d) D-5."""
+    cores = host_cores()
+    v1, n1, B1, s1 = time_oracle(cfg, budget_s, 1)
+    vN, nN, BN, sN = time_oracle(cfg, budget_s, cores)
+    model = cpu_model()
+    desc = lambda Bp, n, secs, th: (f"{cfg.name}-shaped T={cfg.T}, B'={Bp * cfg.agents} columns ({n} samples; "
+                                    f"{secs:.1f} s), full network, GAE+norm+loss/grad+Adam, C double, "
+                                    f"{th} thread(s) on {model}")
+    return {"value": vN, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": model,
+            "sample": desc(BN, nN, sN, cores),
+            "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": desc(B1, n1, s1, 1)}}
+
+
 def reference_arm(args, world, rank):
-    """--impl reference: the oracle as it stands, on this box's host cores, same metric/unit."""
+    """--impl reference: the oracle as it stands, on this box's host cores (all of them, through
+    its block driver), same metric / unit / config as our arm."""
     import synth
     cfg = synth.get_config(args.config)
     if rank != 0:
         return
-    per_step = max(0.2, 150.0 / max(1, args.steps + args.warmup))
     import oracle
+    cores = host_cores()
+    per_step = max(0.2, 150.0 / max(1, args.steps + args.warmup))
     params = synth.make_params(cfg, 0)
-    # calibrate one column, then size the per-step sample
-    _, _, _, t1 = time_oracle(cfg, 0.0, params)
-    Bp = int(max(1, min(cfg.B // cfg.agents, per_step / max(t1, 1e-6))))
-    c = cfg.with_(B=Bp * cfg.agents)
-    b = synth.make_batch(c, seed=0)
-    b["logp_old"] = synth.logp_old_uniform_policy(c, b["xi"])
     nx = dict(epochs=max(1, args.epochs), minibatches=max(1, args.minibatches),
               value_clip=args.value_clip, max_grad_norm=args.max_grad_norm)
+    _, _, Bp, _ = time_oracle(cfg, per_step, cores, params, nx)
+    c, b = oracle_sample(cfg, Bp)
     for _ in range(args.warmup):
-        oracle.ppo_step(c, params, [b], apply=True, **nx)
+        oracle.ppo_step(c, params, [b], apply=True, threads=cores, **nx)
     t0 = time.perf_counter()
     for k in range(args.steps):
-        oracle.ppo_step(c, params, [b], apply=True, t=k + 1, **nx)
+        oracle.ppo_step(c, params, [b], apply=True, t=k + 1, threads=cores, **nx)
     dt = time.perf_counter() - t0
     value = b["n"] * args.steps / dt
     sample = (f"{cfg.name}-shaped T={cfg.T}, B'={Bp * cfg.agents} columns ({b['n']} samples) per "
-              f"step, full network, GAE+norm+loss/grad+Adam, C double, 1 thread")
+              f"step, full network, GAE+norm+loss/grad+Adam, C double, {cores} threads on {cpu_model()}")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+           "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": cfg.name, "T": cfg.T, "B_per_step": Bp * cfg.agents, **nx},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
+
+
+# ------------------------------------------------------------------ roofline helpers
+def load_peaks():
+    try:
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(pk["hbm_gbs"]), float(pk["bf16_tflops"]), float(pk.get("bf16_tflops_sustained", 0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def kernel_table(recs, Kp, prof_ms):
+    """Per-kernel rows from the profiled region; tensor fractions against the BURST bf16 peak
+    (each GEMM launch is tens of microseconds: a burst, B200_PROFILING.md), HBM against copy."""
+    hbm, tf_burst, _, _ = load_peaks()
+    agg = {}
+    for name, t, fl, by in recs:
+        a = agg.setdefault(name, [0.0, 0, 0.0, 0.0])
+        a[0] += t; a[1] += 1; a[2] += fl; a[3] += by
+    rows = []
+    for name, (t, cnt, fl, by) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+        avg = t / max(cnt, 1)
+        row = {"name": name, "ms_per_step": t / Kp, "share": (t / Kp) / prof_ms, "launches_per_step": cnt / Kp}
+        if fl > 0:
+            tfl = fl / cnt / (avg * 1e-3) / 1e12
+            row.update(tflops=tfl, frac_tensor=tfl / tf_burst)
+        if by > 0:
+            gbs = by / cnt / (avg * 1e-3) / 1e9
+            row.update(gbs=gbs, frac_hbm=gbs / hbm)
+        rows.append(row)
+    return agg, rows
+
+
+def roofline_of(agg, traffic_src=None, config=None):
+    """The dominant kernel (by time; not the exchange) under the roof its algorithmic intensity
+    puts it: tensor above the ridge (burst peak / copy bandwidth), else HBM."""
+    hbm, tf_burst, _, src = load_peaks()
+    dname, (dt, dcnt, dfl, dby) = max(((k, v) for k, v in agg.items() if k != "allreduce"),
+                                      key=lambda kv: kv[1][0])
+    davg_s = dt / dcnt * 1e-3
+    traffic = None
+    if traffic_src:
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            traffic = tr.get(config, {}).get(dname)
+        except Exception:
+            traffic = None
+    ridge = tf_burst * 1e12 / (hbm * 1e9)
+    ai = dfl / dby if dby > 0 else float("inf")
+    if dfl > 0 and ai >= ridge:
+        achieved = dfl / dcnt / davg_s / 1e12
+        r = {"bound": "tensor", "kernel": dname, "achieved": achieved, "peak": tf_burst,
+             "unit": "TFLOP/s", "frac": achieved / tf_burst, "traffic": traffic,
+             "peak_source": f"{src} bf16_tflops (burst; fp16 dense = bf16 dense, nominal ratio 1)"}
+    else:
+        achieved = dby / dcnt / davg_s / 1e9
+        r = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm,
+             "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+             "peak_source": f"{src} hbm_gbs (copy)"}
+    r.update(flops_per_launch=dfl / dcnt, bytes_per_launch=dby / dcnt, intensity_flop_per_byte=ai,
+             ridge_flop_per_byte=ridge, ms_per_launch=davg_s * 1e3)
+    return r
 
 
 # ------------------------------------------------------------------ our arm
@@ -193,37 +299,7 @@ def main_ours(args, world, rank, local):
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
-
-    cfg = synth.get_config(args.config)
-    gcfg = cfg.with_(B=cfg.B * world)          # weak scaling: one config-sized shard per rank
-    b = synth.make_batch(gcfg, seed=0, world=world, rank=rank)
-    b["logp_old"] = synth.logp_old_uniform_policy(cfg, b["xi"])
-    n = b["n"]
-    N = n * world
-    params = torch.from_numpy(synth.make_params(cfg, 0)).to(dev)
-    keys = ("rewards", "values", "dones", "obs", "actions", "logp_old")
-    host = {k: torch.from_numpy(np.ascontiguousarray(b[k])).pin_memory() for k in keys}
-    d = {k: host[k].to(dev) for k in keys}
-    h2d_bytes = sum(host[k].numel() * host[k].element_size() for k in keys)
-
-    nccl_id = None
-    if world > 1:
-        from paper_2306_16688_b200.dist import broadcast_unique_id
-        nccl_id = broadcast_unique_id(device=dev)
-    import dataclasses
-    spec = dataclasses.replace(P.NetSpec.from_config(cfg), epochs=args.epochs,
-                               minibatches=args.minibatches, value_clip=args.value_clip,
-                               max_grad_norm=args.max_grad_norm)
-    ctx = P.PPOContext(spec, max_local_n=n, rank=rank, world=world, nccl_id=nccl_id, device=local)
-    ctx.load_params(params)
-    T, Bk = b["rewards"].shape
-    stats = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8, device=dev)
-    stats_host = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8).pin_memory()
-
-    def step(src):
-        # one C-ABI call: GAE -> global normalisation -> forward/loss/backward -> allreduce -> Adam
-        ctx.train_step(N, src["rewards"], src["values"], src["dones"], src["obs"], src["actions"],
-                       src["logp_old"], stats=stats)
+    scaling = args.scaling or ("strong" if world > 1 else "weak")
 
     def barrier():
         torch.cuda.synchronize()
@@ -238,8 +314,62 @@ def main_ours(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    nccl_id = None
+    if world > 1:
+        from paper_2306_16688_b200.dist import broadcast_unique_id
+    import dataclasses
+
+    def make_ctx(cfg, n):
+        uid = broadcast_unique_id(device=dev) if world > 1 else None
+        spec = dataclasses.replace(P.NetSpec.from_config(cfg), epochs=args.epochs,
+                                   minibatches=args.minibatches, value_clip=args.value_clip,
+                                   max_grad_norm=args.max_grad_norm)
+        ctx = P.PPOContext(spec, max_local_n=n, rank=rank, world=world, nccl_id=uid, device=local)
+        ctx.load_params(torch.from_numpy(synth.make_params(cfg, 0)).to(dev))
+        return ctx
+
+    def timed(step, K, W):
+        for _ in range(W):
+            step()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(K):
+            step()
+        b.record()
+        barrier()
+        return max_over_ranks(a.elapsed_time(b))
+
+    def profiled(ctx, step, Kp):
+        ctx.prof_reset()
+        ctx.profile(True)
+        ms = timed(step, Kp, 0) / Kp
+        ctx.profile(False)
+        return ms, ctx.prof_records()
+
+    cfg = synth.get_config(args.config)
+    # strong: the config's batch is the GLOBAL batch, split B/K over the ranks (C-A16);
+    # weak: every rank holds a full config-sized shard (the global batch grows with K)
+    gcfg = cfg if scaling == "strong" else cfg.with_(B=cfg.B * world)
+    b = synth.make_batch(gcfg, seed=0, world=world, rank=rank)
+    b["logp_old"] = synth.logp_old_uniform_policy(cfg, b["xi"])
+    n = b["n"]
+    N = n * world
+    keys = ("rewards", "values", "dones", "obs", "actions", "logp_old")
+    host = {k: torch.from_numpy(np.ascontiguousarray(b[k])).pin_memory() for k in keys}
+    d = {k: host[k].to(dev) for k in keys}
+    h2d_bytes = sum(host[k].numel() * host[k].element_size() for k in keys)
+    ctx = make_ctx(cfg, n)
+    stats = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8, device=dev)
+    stats_host = torch.zeros(P.srl.STATS_BYTES, dtype=torch.uint8).pin_memory()
+
+    def step():
+        # one C-ABI call: GAE -> global normalisation -> forward/loss/backward -> allreduce -> Adam
+        ctx.train_step(N, d["rewards"], d["values"], d["dones"], d["obs"], d["actions"],
+                       d["logp_old"], stats=stats)
+
     for _ in range(max(3, args.warmup)):
-        step(d)
+        step()
     barrier()
     sampler = ClockSampler(range(world)) if rank == 0 else None
     if sampler:
@@ -247,76 +377,99 @@ def main_ours(args, world, rank, local):
         time.sleep(0.3)
     # ---------------- timed region: device-resident inputs (working set > L2: see config)
     K = args.steps
-    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
     wall0 = time.monotonic()
-    e_start.record()
     h0 = time.perf_counter()
-    for _ in range(K):
-        step(d)
+    ms_total = timed(step, K, 0)
     host_ms = (time.perf_counter() - h0) * 1e3 / K
-    e_end.record()
-    barrier()
     wall1 = time.monotonic()
-    ms_total = max_over_ranks(e_start.elapsed_time(e_end))
     stats_dev = P.decode_stats(stats)
-    # ---------------- profiled region: same steps with an event pair around every launch (the
-    # events serialise the launches, so this region is timed separately from `value`)
+    # ---------------- profiled region: an event pair around every launch (serialises them)
     Kp = min(K, 100)
-    ctx.prof_reset()
-    ctx.profile(True)
-    p_start, p_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    p_start.record()
-    for _ in range(Kp):
-        step(d)
-    p_end.record()
-    barrier()
-    ctx.profile(False)
-    prof_ms = max_over_ranks(p_start.elapsed_time(p_end)) / Kp
-    recs = ctx.prof_records()
+    prof_ms, recs = profiled(ctx, step, Kp)
 
-    # ---------------- end to end: every step's batch goes host (pinned) -> device inside the timed
-    # region through the library's pre-fetch slots (NEXT-1, §4.1): the upload of batch
-    # k+1 on the context's copy stream overlaps the step on batch k; stats are copied back
+    # ---------------- end to end through the pre-fetch slots (NEXT-1, §4.1): every
+    # step's batch goes host (pinned) -> device inside the timed region, the upload of batch
+    # k+1 on the context's copy stream overlapping the step on batch k; stats copied back
     Ke = args.e2e_steps or min(K, 100)
     hb = [host[k] for k in keys]
-    ctx.upload(0, *hb)
-    for j in range(2):
-        ctx.upload((j + 1) % 2, *hb)
-        ctx.train_step_slot(j % 2, N, stats=stats)
-        stats_host.copy_(stats, non_blocking=True)
-    ctx.train_step_slot(0, N, stats=stats)          # drain the primed slot
-    barrier()
-    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    x0.record()
-    ctx.upload(0, *hb)
-    for j in range(Ke):
-        if j + 1 < Ke:
-            ctx.upload((j + 1) % 2, *hb)
-        ctx.train_step_slot(j % 2, N, stats=stats)
-        stats_host.copy_(stats, non_blocking=True)
-    x1.record()
-    barrier()
-    e2e_ms = max_over_ranks(x0.elapsed_time(x1))
-    # ---------------- NEXT-2: policy-worker batched inference on the same batch of observations
-    # (forward + counter-RNG sampling epilogue), device-timed like `value`
+
+    def e2e_run(overlap):
+        ctx.upload(0, *hb)
+        ctx.train_step_slot(0, N, stats=stats)
+        barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record()
+        ctx.upload(0, *hb)
+        for j in range(Ke):
+            if overlap and j + 1 < Ke:
+                ctx.upload((j + 1) % 2, *hb)
+            ctx.train_step_slot(j % 2 if overlap else 0, N, stats=stats)
+            stats_host.copy_(stats, non_blocking=True)
+            if not overlap and j + 1 < Ke:
+                torch.cuda.current_stream().synchronize()   # no pre-fetch: upload after the step
+                ctx.upload(0, *hb)
+        x1.record()
+        barrier()
+        return max_over_ranks(x0.elapsed_time(x1))
+
+    e2e_ms = e2e_run(True)
+    e2e_serial_ms = e2e_run(False)      # ablation (§5.3.4, E14): pre-fetching off
+    # ---------------- NEXT-2: policy-worker batched inference on the same observations
     Ki = min(K, 100)
     inf_out = (torch.empty((n, len(cfg.heads)), dtype=torch.int32, device=dev),
                torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.float32, device=dev))
-    for j in range(3):
-        ctx.rollout(d["obs"], seed=j, actions=inf_out[0], logp=inf_out[1], value=inf_out[2])
-    barrier()
-    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    i0.record()
-    for j in range(Ki):
-        ctx.rollout(d["obs"], seed=j, actions=inf_out[0], logp=inf_out[1], value=inf_out[2])
-    i1.record()
-    barrier()
-    inf_ms = max_over_ranks(i0.elapsed_time(i1)) / Ki
+    seed_box = [0]
+
+    def roll():
+        seed_box[0] += 1
+        ctx.rollout(d["obs"], seed=seed_box[0], actions=inf_out[0], logp=inf_out[1], value=inf_out[2])
+
+    inf_ms = timed(roll, Ki, 3) / Ki
     if sampler:
         time.sleep(0.1)
         sampler.stop()
+    comm_path = ctx.comm_path
+    ctx.close()
+    del d
+
+    # ---------------- the other scaling mode (multi-GPU): same config, same code
+    alt = None
+    if world > 1 and not args.no_alt_scaling:
+        other = "weak" if scaling == "strong" else "strong"
+        acfg = cfg if other == "strong" else cfg.with_(B=cfg.B * world)
+        ab = synth.make_batch_device(acfg, dev, seed=0, world=world, rank=rank)
+        actx = make_ctx(cfg, ab["n"])
+        An = ab["n"] * world
+        ams = timed(lambda: actx.train_step(An, ab["rewards"], ab["values"], ab["dones"], ab["obs"],
+                                            ab["actions"], ab["logp_old"]), K, max(3, args.warmup))
+        alt = {"scaling": other, "value": An * K / (ams * 1e-3), "unit": UNIT,
+               "ms_per_step": ams / K, "samples_per_step": An,
+               "inputs": "device-side synthetic (synth.make_batch_device)"}
+        actx.close()
+        del ab
+
+    # ---------------- every other BASELINE config on this GPU (N = 1 only): samples/s + roofline
+    others = {}
+    if world == 1 and not args.no_all_configs:
+        plan = {"tiny": (300, 100), "atari": None, "gfootball": (30, 20), "smac": (5, 3), "hns": (3, 2)}
+        for name, kk in plan.items():
+            if kk is None or name == cfg.name:
+                continue
+            c = synth.get_config(name)
+            cb = synth.make_batch_device(c, dev, seed=0)
+            cctx = make_ctx(c, cb["n"])
+            cs = lambda: cctx.train_step(cb["n"], cb["rewards"], cb["values"], cb["dones"], cb["obs"],
+                                         cb["actions"], cb["logp_old"])
+            cms = timed(cs, kk[0], 2)
+            pms, crecs = profiled(cctx, cs, kk[1])
+            cagg, _ = kernel_table(crecs, kk[1], pms)
+            others[name] = {"value": cb["n"] * kk[0] / (cms * 1e-3), "unit": UNIT,
+                            "ms_per_step": cms / kk[0], "steps": kk[0], "samples_per_step": cb["n"],
+                            "roofline": roofline_of(cagg),
+                            "inputs": "device-side synthetic (synth.make_batch_device)"}
+            cctx.close()
+            del cb
+            torch.cuda.empty_cache()
 
     if dist:
         dist.barrier()
@@ -325,82 +478,30 @@ def main_ours(args, world, rank, local):
             dist.destroy_process_group()
         return
 
-    # ---------------- per-kernel table and the dominant kernel's roofline
     import math
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    tf_sus = float(peaks.get("bf16_tflops_sustained", 1400.0))
-    peak_src = "measured" if peaks else "fallback"
-    agg = {}
-    for name, t, fl, by in recs:
-        a = agg.setdefault(name, [0.0, 0, 0.0, 0.0])
-        a[0] += t; a[1] += 1; a[2] += fl; a[3] += by
-    step_ms = ms_total / K
-    kernels = []
-    for name, (t, cnt, fl, by) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
-        avg = t / max(cnt, 1)
-        row = {"name": name, "ms_per_step": t / Kp, "share": (t / Kp) / prof_ms, "launches_per_step": cnt / Kp}
-        if fl > 0:
-            row.update(tflops=fl / cnt / (avg * 1e-3) / 1e12, frac_tensor=fl / cnt / (avg * 1e-3) / 1e12 / tf_sus)
-        if by > 0:
-            row.update(gbs=by / cnt / (avg * 1e-3) / 1e9, frac_hbm=by / cnt / (avg * 1e-3) / 1e9 / hbm)
-        kernels.append(row)
-    # dominant kernel by time; its roof is the one its arithmetic intensity (algorithmic FLOP per
-    # algorithmic HBM byte) puts it under: tensor above the ridge (peak FLOP/s / peak B/s), else HBM
-    dname, (dt, dcnt, dfl, dby) = max(((k, v) for k, v in agg.items() if k != "allreduce"),
-                                      key=lambda kv: kv[1][0])   # NCCL's kernel is not ours
-    davg_s = dt / dcnt * 1e-3
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(args.config, {}).get(dname)
-    except Exception:
-        pass
-    ridge = tf_sus * 1e12 / (hbm * 1e9)
-    ai = dfl / dby if dby > 0 else float("inf")
-    if dfl > 0 and ai >= ridge:
-        achieved = dfl / dcnt / davg_s / 1e12
-        roofline = {"bound": "tensor", "kernel": dname, "achieved": achieved, "peak": tf_sus,
-                    "unit": "TFLOP/s", "frac": achieved / tf_sus, "traffic": traffic,
-                    "peak_source": f"{peak_src} bf16_tflops_sustained (fp16 dense = bf16 dense, nominal ratio 1)"}
-    else:
-        achieved = dby / dcnt / davg_s / 1e9
-        roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm,
-                    "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                    "peak_source": f"{peak_src} hbm_gbs (copy)"}
-    roofline.update(flops_per_launch=dfl / dcnt, bytes_per_launch=dby / dcnt,
-                    intensity_flop_per_byte=ai, ridge_flop_per_byte=ridge,
-                    ms_per_launch=davg_s * 1e3)
+    agg, kernels = kernel_table(recs, Kp, prof_ms)
+    roofline = roofline_of(agg, traffic_src=True, config=cfg.name)
     # our kernels per step (srl_ppo_train_step): gae_kernel (merges the moments itself),
-    # + moments merge when world > 1, the 3L+2 GEMMs, finalize_w + finalize_b + extras, adam,
-    # stats (NCCL's kernels are not counted)
+    # + moments exchange when world > 1, the 3L+2 GEMMs, finalize_w + finalize_b + extras, adam,
+    # stats, + the peer-memory allreduce (NCCL's kernels are not counted)
     L = len(cfg.hidden)
-    # per update; epochs x minibatches updates per step (NEXT-3), + grad_norm when clipping
-    p2p = ctx.comm_path == "nvlink-p2p"      # the allreduce is then one of our kernels
+    p2p = comm_path == "nvlink-p2p"
     per_update = ((L + 1 + (L + 1) + L) + 3 + 1 + 1 + (1 if args.max_grad_norm > 0 else 0)
                   + (1 if p2p else 0))
     updates = max(1, args.epochs) * max(1, args.minibatches)
-    per_step = 1 + (1 if world > 1 else 0) + per_update * updates
-    cpu = None
-    if not args.no_cpu_baseline:
-        v, cn, Bp, secs = time_oracle(cfg, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{cfg.name}-shaped T={cfg.T}, B'={Bp * cfg.agents} columns ({cn} samples; "
-                         f"{secs:.1f} s), full network, GAE+norm+loss/grad+Adam, C double, 1 thread"}
+    per_step = 1 + (1 if world > 1 and p2p else 0) + per_update * updates
+    cpu = None if args.no_cpu_baseline else cpu_baselines(cfg, args.cpu_seconds)
     clocks = sampler.summary(wall0, wall1) if sampler else None
     out = {
         "metric": METRIC, "value": N * K / (ms_total * 1e-3), "unit": UNIT, "n_gpus": world,
-        "steps": K, "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "steps": K, "warmup": max(3, args.warmup), "ms_per_step": ms_total / K, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f16",
         "data": "synthetic",
-        "config": {"workload": cfg.name, "T": cfg.T, "B_per_rank": cfg.B, "obs_dim": cfg.obs_dim,
+        "config": {"workload": cfg.name, "T": cfg.T, "B_global": N // cfg.T, "B_per_rank": n // cfg.T,
+                   "obs_dim": cfg.obs_dim,
                    "hidden": list(cfg.hidden), "heads": list(cfg.heads), "samples_per_step": N,
                    "frames_per_step": N * cfg.frame_skip, "parallelism": f"dp{world}",
-                   "grad_allreduce": ctx.comm_path,
+                   "grad_allreduce": comm_path,
                    "epochs": max(1, args.epochs), "minibatches": max(1, args.minibatches),
                    "value_clip": args.value_clip, "max_grad_norm": args.max_grad_norm,
                    "l2": "no flush: per-step working set > L2 (obs %.0f MB + activations %.0f MB + "
@@ -412,7 +513,9 @@ def main_ours(args, world, rank, local):
         "host_submit_ms_per_step": host_ms,
         "profiled_ms_per_step": prof_ms,
         "e2e": {"value": N * Ke / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes * world,
-                "d2h_bytes_per_step": P.srl.STATS_BYTES * world, "steps": Ke},
+                "d2h_bytes_per_step": P.srl.STATS_BYTES * world, "steps": Ke,
+                "no_prefetch": {"value": N * Ke / (e2e_serial_ms * 1e-3), "unit": UNIT,
+                                "what": "ablation: upload after each step, no overlap (PAPER.md §5.3.4)"}},
         "gpu_launches": per_step * K,
         "inference": {"what": "NEXT-2 srl_policy_rollout: forward + sampling epilogue over the "
                               "step's observations (policy-worker batch = the whole batch)",
@@ -425,6 +528,10 @@ def main_ours(args, world, rank, local):
         "last_stats": {k: stats_dev[k] for k in ("loss", "policy_loss", "value_loss", "entropy",
                                                  "clip_fraction", "nonfinite", "step")},
     }
+    if alt:
+        out["alt_scaling"] = alt
+    if others:
+        out["configs"] = others
     if any(math.isnan(x) for x in (out["value"],)):
         raise SystemExit("nan throughput")
     emit(out)

@@ -38,14 +38,16 @@ typedef enum srl_status {
   SRL_OK = 0,
   SRL_EINVAL = 1,        /* bad argument: null pointer, shape, stride, alignment, n > max_local_n */
   SRL_ECUDA = 2,         /* CUDA runtime / launch failure, or no device */
-  SRL_ENCCL = 3,         /* NCCL failure */
+  SRL_ENCCL = 3,         /* cross-rank exchange failure: NCCL error, or a peer-memory wait that
+                            exceeded SRL_COMM_TIMEOUT_S (default 30 s, SPEC.md S:L532
+                            ReduceTimeout); the context is then failed and must be destroyed */
   SRL_ENOMEM = 4,        /* device allocation failed */
   SRL_EUNSUPPORTED = 5,  /* valid request this build does not implement */
   SRL_ESTATE = 6         /* call not valid in the context's state */
 } srl_status;
 
 const char* srl_last_error(void);
-int srl_abi_version(void);                    /* 2: round-1 ABI + NEXT-2/NEXT-3 arguments */
+int srl_abi_version(void);                    /* 3: round-2 ABI (comm_error, srl_debug_exchange) */
 
 /* ---------------------------------------------------------------- a1: GAE
  * Generalised advantage estimation over time-major columns (SPEC.md S:L593-601,
@@ -55,11 +57,11 @@ int srl_abi_version(void);                    /* 2: round-1 ABI + NEXT-2/NEXT-3 
  *     A_T = 0,   R_t = A_t + v_t.
  * d_t = 1 means the episode ended AT transition t: it cuts v_{t+1} and A_{t+1}.
  *   rewards  device f32 [T][ld]          values device f32 [T+1][ld] (row T = bootstrap)
- *   dones    device u8  [T][ld] flags: 0 = continue, nonzero = episode ended at t (bit 1 with
- *            bit 0 clear = time limit, see trunc_values)
+ *   dones    device u8  [T][ld] flags: 0 = continue, nonzero = episode ended at t ((flag & 3) == 2,
+ *            i.e. bit 1 set and bit 0 clear, = time limit, see trunc_values)
  *   adv_out  device f32 [T][ld]          ret_out f32 [T][ld] or NULL
  *   trunc_values device f32 [T][ld] or NULL (NEXT-3, DESIGN.md §3.5 reading R-T, SURVEY C-A2):
- *             a dones byte with bit 0 clear and bit 1 set marks a time-limit truncation at t:
+ *             a dones byte with (flag & 3) == 2 marks a time-limit truncation at t:
  *             the recursion is still cut but delta_t = r_t + gamma * trunc_values_t - v_t.
  *             NULL: every nonzero dones byte is terminal.
  *   valid    device u8 [T][ld] or NULL (NEXT-3 reading R-P, SURVEY C-A17): entries with 0 are
@@ -84,8 +86,9 @@ srl_status srl_gae(int T, int B, int ld, const float* rewards, const float* valu
  *   local_stats device f64 [3] {n, mean, M2} of this rank's adv (from srl_gae), or NULL to
  *               compute them here (warp-shuffle + block reduction over adv).
  *   mean_std_out device f64 [2] {mu, sigma} or NULL.
- * With ctx != NULL and world > 1 the ranks' {n, mean, M2} are all-gathered (NCCL) and merged
- * in rank order (Chan et al.), so mu and sigma are bit-identical on all ranks. */
+ * With ctx != NULL and world > 1 the ranks' {n, mean, M2} are all-gathered (over NVLink peer
+ * memory when the context mapped its peers, else NCCL) and merged in rank order (Chan et al.),
+ * so mu and sigma are bit-identical on all ranks.  Every rank of ctx must make the call. */
 srl_status srl_adv_norm(srl_ctx* ctx, float* adv, int64_t n, const double* local_stats,
                         float eps, int unbiased, int apply, double* mean_std_out,
                         srl_stream_t stream);
@@ -107,7 +110,7 @@ typedef struct srl_ppo_config {
   float adv_eps;            /* 1e-8: A_hat = (A - mu) / (sigma + adv_eps) inside the loss */
   float gamma, gae_lambda;  /* 0.99, 0.95: GAE of srl_ppo_train_step */
   int adv_unbiased;         /* 0: population sigma (default, C-A4); 1: N-1 */
-  int64_t max_local_n;      /* workspace sizing: largest n_local passed to srl_ppo_step */
+  int64_t max_local_n;      /* workspace sizing: largest n_local passed to srl_ppo_step, <= 2^31 - 1 */
   int precision;            /* srl_precision */
   /* NEXT-3 PPO variants (SURVEY.md C-A5 names them as the next extension):
    *   value_clip > 0: value loss max((V-R)^2, (V_c-R)^2), V_c = v_old + clip(V - v_old, +-value_clip)
@@ -136,6 +139,7 @@ typedef struct srl_ppo_stats {
   int64_t fp16_saturated;   /* fp16 stores clamped to +-65504 (all ranks) */
   int64_t step;             /* Adam step t after this call = policy version (Code 1 inc_version) */
   double grad_norm;         /* NEXT-3: global gradient norm before clipping (0 if max_grad_norm == 0) */
+  int64_t comm_error;       /* 1: an exchange wait of this context timed out; Adam was skipped */
 } srl_ppo_stats;
 
 /* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller. */
@@ -236,13 +240,17 @@ srl_status srl_ppo_train_step_slot(srl_ctx* ctx, int slot, int64_t n_global,
                                    srl_ppo_stats* stats_out, srl_stream_t stream);
 
 /* How srl_ppo_step reduces the gradient bucket across ranks (a6): 0 = world 1 (none),
- * 1 = NCCL allreduce, 2 = one-shot allreduce over NVLink peer memory (CUDA IPC-mapped buckets
- * of all ranks summed in rank order; the default when every rank could map every peer;
- * SRL_P2P_AR=0 selects NCCL).  -1 on a null ctx. */
+ * 1 = NCCL allreduce, 2 = two-shot allreduce over NVLink peer memory (CUDA IPC-mapped buckets:
+ * each rank sums its 1/world chunk of all ranks' buckets in rank order, then gathers the other
+ * chunks; the default when every rank could map every peer; SRL_P2P_AR=0 selects NCCL).
+ * -1 on a null ctx. */
 int srl_ppo_comm_path(srl_ctx* ctx);
 
 /* a6: in-place allreduce over the ctx's ranks of a device f32 buffer (SPEC reduce_gradients
- * S:L505-513): op 0 = sum, op 1 = mean.  world == 1: identity (op 1 leaves values as is). */
+ * S:L505-513): op 0 = sum, op 1 = mean (the sum times 1/world in fp32).  world == 1: identity.
+ * With the peer path and count <= P + 8 it is the step's own two-shot rank-order exchange
+ * (bit-identical on all ranks); otherwise NCCL.  Every rank must make the call with the same
+ * count. */
 srl_status srl_allreduce_grads(srl_ctx* ctx, float* buf, int64_t count, int op,
                                srl_stream_t stream);
 
@@ -267,6 +275,20 @@ srl_status srl_prof_read(srl_ctx* ctx, int i, const char** name, float* ms, doub
 srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int a_mn, int lda,
                           const uint16_t* B, int b_mn, int ldb, int bn, int splits, int cg,
                           float* D, srl_stream_t stream);
+
+/* ---------------------------------------------------------------- test hook
+ * The a2/a6 peer-memory exchange kernels for `world` VIRTUAL ranks on one GPU (no real peer):
+ *   x        device f32 [world][ld]: rank r's bucket at x + r*ld (count entries); rank r's
+ *            chunk of x[r] is overwritten with the reduced values (as on real ranks)
+ *   out      device f32 [world][ld]: rank r's result = scale * (sum over ranks 0..world-1 of
+ *            x, in rank order) in every entry < count
+ *   tri      device f64 [world][3] {n, mean, M2} per rank, or NULL; mean_std device f64
+ *            [world][2] rank r's merged {mu, sigma} (sigma population or, unbiased, N-1)
+ * Every flag a rank waits for is pre-published and the phases run in the order the flags
+ * would enforce (all ranks' phase 1, then all ranks' phase 2).  Synchronous.  Tests only. */
+srl_status srl_debug_exchange(int world, int64_t count, int64_t ld, float* x, float* out,
+                              float scale, const double* tri, double* mean_std, int unbiased,
+                              srl_stream_t stream);
 
 #ifdef __cplusplus
 }

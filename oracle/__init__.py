@@ -26,7 +26,9 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with plain gcc (no fast-math: IEEE double semantics)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-Wall",
+        # -fopenmp only for oracle_loss_and_grad_mt (bench.py's all-core timing); every
+        # other function has no pragma and is the same single-threaded code
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-Wall", "-fopenmp",
                                "-o", _SO, _SRC, "-lm"])
     return _SO
 
@@ -48,6 +50,9 @@ def lib():
         _lib.oracle_loss_and_grad.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, i32,
                                               d, d, d, C.c_double, C.c_double, C.c_double,
                                               C.c_double, d, d, d, d, C.c_double]
+        _lib.oracle_loss_and_grad_mt.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, i32,
+                                                 d, d, d, C.c_double, C.c_double, C.c_double,
+                                                 C.c_double, d, d, d, C.c_double, C.c_int]
         _lib.oracle_clip_grad_norm.argtypes = [i64, d, C.c_double]
         _lib.oracle_clip_grad_norm.restype = C.c_double
         u64 = C.POINTER(C.c_uint64)
@@ -122,7 +127,9 @@ def forward(obs_dim, hidden, heads, params, obs):
 
 def loss_and_grad(obs_dim, hidden, heads, params, obs, actions, logp_old, adv_hat, ret,
                   clip_eps=0.2, value_coef=0.5, entropy_coef=0.01, grad_scale=None,
-                  grad=None, sums=None, want_per_sample=False, v_old=None, value_clip=0.0):
+                  grad=None, sums=None, want_per_sample=False, v_old=None, value_clip=0.0,
+                  threads=1):
+    """threads > 1: the all-core timing driver (oracle_loss_and_grad_mt, block-order sums)."""
     p = np.ascontiguousarray(params, dtype=np.float64)
     x = np.ascontiguousarray(np.asarray(obs, dtype=np.float64)[:, :obs_dim])
     n = x.shape[0]
@@ -138,6 +145,16 @@ def loss_and_grad(obs_dim, hidden, heads, params, obs, actions, logp_old, adv_ha
         grad_scale = 1.0 / n
     ps = np.empty(n, np.float64) if want_per_sample else None
     vo = None if v_old is None else np.ascontiguousarray(v_old, dtype=np.float64).reshape(-1)
+    if threads > 1:
+        assert not want_per_sample
+        lib().oracle_loss_and_grad_mt(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads),
+                                      _p(p, C.c_double), n, _p(x, C.c_double), _p(act, C.c_int32),
+                                      _p(lo, C.c_double), _p(ah, C.c_double), _p(rt, C.c_double),
+                                      clip_eps, value_coef, entropy_coef, grad_scale,
+                                      _p(grad, C.c_double), _p(sums, C.c_double),
+                                      _p(vo, C.c_double) if vo is not None else None,
+                                      float(value_clip), int(threads))
+        return grad, sums, None
     lib().oracle_loss_and_grad(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads),
                                _p(p, C.c_double), n, _p(x, C.c_double), _p(act, C.c_int32),
                                _p(lo, C.c_double), _p(ah, C.c_double), _p(rt, C.c_double),
@@ -208,7 +225,7 @@ def minibatch_bounds(n, M):
 
 
 def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, t=1,
-             apply=True, value_clip=0.0, max_grad_norm=0.0, epochs=1, minibatches=1):
+             apply=True, value_clip=0.0, max_grad_norm=0.0, epochs=1, minibatches=1, threads=1):
     """One trainer step of the oracle over K shards (list of dicts from synth.make_batch
     with a ``logp_old`` entry).  Returns a dict with adv/ret per shard, mean/std, grad,
     loss sums and (if apply) the updated params/m/v.
@@ -261,7 +278,7 @@ def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, 
                               cfg.clip_eps, cfg.value_coef, cfg.entropy_coef,
                               grad_scale=1.0 / Nmb, grad=grad, sums=sums,
                               v_old=vo[rows] if value_clip > 0 else None,
-                              value_clip=value_clip)
+                              value_clip=value_clip, threads=threads)
             norm = clip_grad_norm(grad, max_grad_norm) if max_grad_norm > 0 else float(
                 np.sqrt(np.sum(grad * grad)))
             out["grads"].append(grad)

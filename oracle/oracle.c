@@ -24,7 +24,7 @@ void oracle_gae(int T, int B, int ld, const float* r, const float* v, const uint
       double v_t = v[(int64_t)t * ld + b];
       double v_n = v[(int64_t)(t + 1) * ld + b];
       double boot = v_n * m;                                       /* v_{t+1} m_t */
-      if (trunc_values && f != 0 && !(f & 1))                      /* NEXT-3 R-T: time limit */
+      if (trunc_values && (f & 3) == 2)                            /* NEXT-3 R-T: time limit */
         boot = trunc_values[(int64_t)t * ld + b];
       double delta = r_t + gamma * boot - v_t;                     /* delta_t */
       double A = delta + gamma * lambda * m * A_next;              /* A_t */
@@ -312,4 +312,35 @@ void oracle_adam(int64_t P, double* p, double* m, double* v, const double* g, in
     double vhat = v[i] / bc2;
     p[i] -= lr * mhat / (sqrt(vhat) + eps);
   }
+}
+
+/* ---------------------------------------------------------------- all-core timing driver */
+void oracle_loss_and_grad_mt(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                             const double* params, int64_t n, const double* obs,
+                             const int32_t* actions, const double* logp_old,
+                             const double* adv_hat, const double* ret,
+                             double clip_eps, double value_coef, double entropy_coef,
+                             double grad_scale, double* grad, double* sums,
+                             const double* v_old, double value_clip, int threads) {
+  if (threads < 1) threads = 1;
+  const int64_t P = oracle_param_count(obs_dim, L, hidden, H, heads);
+  double* g = (double*)calloc((size_t)threads * (size_t)P, sizeof(double));
+  double* s = (double*)calloc((size_t)threads * 5, sizeof(double));
+  #pragma omp parallel for num_threads(threads) schedule(static, 1)
+  for (int k = 0; k < threads; ++k) {
+    const int64_t lo = n * k / threads, hi = n * (k + 1) / threads;
+    const int H_ = H;
+    const int od = obs_dim;
+    if (hi > lo)
+      oracle_loss_and_grad(obs_dim, L, hidden, H, heads, params, hi - lo, obs + lo * od,
+                           actions + lo * H_, logp_old + lo, adv_hat + lo, ret + lo, clip_eps,
+                           value_coef, entropy_coef, grad_scale, g + (int64_t)k * P, s + 5 * k,
+                           NULL, v_old ? v_old + lo : NULL, value_clip);
+  }
+  for (int k = 0; k < threads; ++k) {            /* block order */
+    for (int64_t i = 0; i < P; ++i) grad[i] += g[(int64_t)k * P + i];
+    for (int j = 0; j < 5; ++j) sums[j] += s[5 * k + j];
+  }
+  free(g);
+  free(s);
 }

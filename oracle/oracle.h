@@ -28,7 +28,7 @@ extern "C" {
  *   A_t = delta_t + gamma * lambda * m_t * A_{t+1},  A_T = 0;   R_t = A_t + v_t  (C-A1, C-A3).
  * r, d: [T][ld], v: [T+1][ld] (row T = bootstrap value).  adv, ret: dense [T][B].
  * d is a flag byte: nonzero ends the episode at t (m_t = 0).  NEXT-3 reading R-T (SURVEY C-A2):
- * with trunc_values [T][ld] non-null, a flag with bit 0 clear and bit 1 set is a time-limit
+ * with trunc_values [T][ld] non-null, a flag with (flag & 3) == 2 (bit 1 set, bit 0 clear) is a time-limit
  * truncation: the recursion is still cut, but delta_t bootstraps from the truncated state,
  *   delta_t = r_t + gamma * trunc_values_t - v_t.
  * trunc_values NULL: every nonzero flag is terminal (the core's reading). */
@@ -102,6 +102,19 @@ void oracle_rollout(int obs_dim, int L, const int* hidden, int H, const int* hea
  *   p -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps). */
 void oracle_adam(int64_t P, double* p, double* m, double* v, const double* g, int64_t t,
                  double lr, double b1, double b2, double eps);
+
+/* Timing driver for bench.py's all-core cpu_baseline: splits the n
+ * samples into `threads` contiguous blocks, runs oracle_loss_and_grad on each block in its
+ * own OpenMP thread into its own zeroed grad / sums buffers, then adds the buffers in block
+ * order (fixed, deterministic).  The per-sample arithmetic is exactly oracle_loss_and_grad's;
+ * only the order of the final sums differs (pinned against the 1-thread call to 1e-12). */
+void oracle_loss_and_grad_mt(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                             const double* params, int64_t n, const double* obs,
+                             const int32_t* actions, const double* logp_old,
+                             const double* adv_hat, const double* ret,
+                             double clip_eps, double value_coef, double entropy_coef,
+                             double grad_scale, double* grad, double* sums,
+                             const double* v_old, double value_clip, int threads);
 
 #ifdef __cplusplus
 }

@@ -89,7 +89,7 @@ static srl_status require_device() {
 }
 
 extern "C" const char* srl_last_error(void) { return g_err.c_str(); }
-extern "C" int srl_abi_version(void) { return 2; }
+extern "C" int srl_abi_version(void) { return 3; }
 
 // ------------------------------------------------------------------ a1
 extern "C" srl_status srl_gae(int T, int B, int ld, const float* rewards, const float* values,
@@ -189,7 +189,37 @@ struct srl_ctx {
   unsigned long long epoch = 0, mepoch = 0;
   int64_t xstride() const { return (P + 8 + 63) / 64 * 64; }   // 256-B aligned halves
   float* gn_coef() const { return reinterpret_cast<float*>(gn + kGradNormBlocks + 1); }
+  // bounded exchange waits (SPEC.md S:L532 ReduceTimeout): device + host-mapped error words
+  CommCtl cc{};
+  int* err_pinned = nullptr;                   // host view of cc.err_host
+  bool failed = false;                         // a peer wait timed out or NCCL failed: no more steps
 };
+
+static unsigned long long comm_timeout_ns() {
+  const char* e = getenv("SRL_COMM_TIMEOUT_S");
+  double s = e ? atof(e) : 30.0;
+  if (!(s > 0.0)) s = 30.0;
+  return (unsigned long long)(s * 1e9);
+}
+
+// every call on a multi-rank context first looks at the exchange error words (no device sync:
+// the host-mapped word is read directly) and at NCCL's asynchronous error state
+static srl_status comm_check(srl_ctx* c, const char* who) {
+  if (c->world == 1) return SRL_OK;
+  if (!c->failed && c->err_pinned && *reinterpret_cast<volatile int*>(c->err_pinned)) c->failed = true;
+  if (!c->failed && c->comm) {
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      c->failed = true;
+    }
+  }
+  if (c->failed)
+    FAIL(SRL_ENCCL, std::string(who) + ": the context's cross-rank exchange failed (a peer wait "
+                    "exceeded SRL_COMM_TIMEOUT_S or NCCL reported an error); destroy the context");
+  return SRL_OK;
+}
 
 static bool get_tmap(srl_ctx* c, CUtensorMap* out, const void* base, uint64_t inner,
                      uint64_t outer, uint64_t row_bytes, uint32_t bi, uint32_t bo,
@@ -273,6 +303,7 @@ static void free_ctx(srl_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (c->err_pinned) cudaFreeHost(c->err_pinned);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);
   delete c;
@@ -339,8 +370,8 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
     A += cfg->head_sizes[h];
   }
   if (A + 1 > kHeadCols) FAIL(SRL_EINVAL, "srl_ppo_create: sum(head_sizes) + 1 must be <= 64");
-  if (cfg->max_local_n < 1 || cfg->max_local_n > (int64_t)1 << 31)
-    FAIL(SRL_EINVAL, "srl_ppo_create: need 1 <= max_local_n <= 2^31");
+  if (cfg->max_local_n < 1 || cfg->max_local_n > (int64_t)INT32_MAX)
+    FAIL(SRL_EINVAL, "srl_ppo_create: need 1 <= max_local_n <= 2^31 - 1");
   if (cfg->precision != SRL_PREC_F16_SCALED) FAIL(SRL_EUNSUPPORTED, "srl_ppo_create: precision");
   if (!(cfg->value_clip >= 0.f) || !(cfg->max_grad_norm >= 0.f) || cfg->epochs > 1000 ||
       cfg->minibatches > 4096)
@@ -451,6 +482,16 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if ((st = dalloc(c, &c->gae_counter, sizeof(unsigned int) * 4))) return bail(st);
   if ((st = dalloc(c, &c->gn, sizeof(double) * (kGradNormBlocks + 2)))) return bail(st);
   if ((st = dalloc(c, &c->gn_counter, sizeof(unsigned int) * 4))) return bail(st);
+  if ((st = dalloc(c, &c->cc.err_dev, sizeof(int) * 4))) return bail(st);
+  if (cudaHostAlloc(reinterpret_cast<void**>(&c->err_pinned), sizeof(int) * 4, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->cc.err_host), c->err_pinned, 0) != cudaSuccess) {
+    c->err_pinned = nullptr;
+    set_error("srl_ppo_create: mapped host allocation failed");
+    free_ctx(c);
+    return SRL_ENOMEM;
+  }
+  std::memset(c->err_pinned, 0, sizeof(int) * 4);
+  c->cc.timeout_ns = comm_timeout_ns();
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(id.internal, nccl_id, 128);
@@ -561,7 +602,10 @@ extern "C" srl_status srl_adv_norm(srl_ctx* ctx, float* adv, int64_t n, const do
   if (n < 1) FAIL(SRL_EINVAL, "srl_adv_norm: n < 1");
   if (!adv && (!local_stats || apply)) FAIL(SRL_EINVAL, "srl_adv_norm: null adv");
   if (srl_status st = require_device()) return st;
-  if (ctx) CK(cudaSetDevice(ctx->device));
+  if (ctx) {
+    CK(cudaSetDevice(ctx->device));
+    if (srl_status st = comm_check(ctx, "srl_adv_norm")) return st;
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   double* scratch = nullptr;   // [kMomentBlocks*3] partials, [3] local, [world*3] gathered, [2] ms
   const int world = ctx ? ctx->world : 1;
@@ -576,7 +620,11 @@ extern "C" srl_status srl_adv_norm(srl_ctx* ctx, float* adv, int64_t n, const do
     CK(launch_merge_moments(scratch, kMomentBlocks, local, nullptr, 0, s));
     local_stats = local;
   }
-  if (world > 1) {
+  if (world > 1 && ctx->p2p) {
+    // the same NVLink peer-memory exchange srl_ppo_train_step uses (rank-order merge)
+    CK(launch_p2p_moments(ctx->peers, world, ctx->rank, ++ctx->mepoch, local_stats, ms, unbiased,
+                          ctx->cc, 3, s));
+  } else if (world > 1) {
     CKN(ncclAllGather(local_stats, gathered, 3, ncclDouble, ctx->comm, s));
     CK(launch_merge_moments(gathered, world, nullptr, ms, unbiased, s));
   } else {
@@ -590,13 +638,36 @@ extern "C" srl_status srl_adv_norm(srl_ctx* ctx, float* adv, int64_t n, const do
 }
 
 // ------------------------------------------------------------------ a6
+static __global__ void scale_kernel(float* x, int64_t n, float a) {
+  griddep_wait();
+  griddep_launch();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= a;
+}
+
 extern "C" srl_status srl_allreduce_grads(srl_ctx* c, float* buf, int64_t count, int op,
                                           srl_stream_t stream) {
   if (!c || !buf || count < 0 || (op != 0 && op != 1)) FAIL(SRL_EINVAL, "srl_allreduce_grads: bad args");
   if (c->world == 1 || count == 0) return SRL_OK;
   CK(cudaSetDevice(c->device));
+  if (srl_status st = comm_check(c, "srl_allreduce_grads")) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  CKN(ncclAllReduce(buf, buf, (size_t)count, ncclFloat, op == 1 ? ncclAvg : ncclSum, c->comm, s));
+  const float scale = op == 1 ? 1.f / (float)c->world : 1.f;
+  if (c->p2p && count <= c->xstride()) {
+    // the step's two-shot peer-memory exchange: stage into this rank's exposed buffer of the
+    // next epoch's parity, reduce in rank order, result back into buf (identical on all ranks)
+    const unsigned long long epoch = c->epoch + 1;
+    const int64_t xoff = (int64_t)(epoch & 1ull) * c->xstride();
+    CK(cudaMemcpyAsync(c->xbuf + xoff, buf, sizeof(float) * count, cudaMemcpyDeviceToDevice, s));
+    c->epoch = epoch;
+    CK(launch_p2p_allreduce(c->peers, c->world, c->rank, xoff, count, epoch, scale, buf, c->cc, 3, s));
+    return SRL_OK;
+  }
+  CKN(ncclAllReduce(buf, buf, (size_t)count, ncclFloat, ncclSum, c->comm, s));
+  if (op == 1) {
+    int64_t blocks = std::min<int64_t>((count + 255) / 256, 4 * c->sms);
+    CK(launch_k(scale_kernel, dim3((unsigned)blocks), dim3(256), 0, s, 1, buf, count, scale));
+  }
   return SRL_OK;
 }
 
@@ -655,6 +726,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
                                    const double* adv_mean_std, int apply,
                                    srl_ppo_stats* stats_out, srl_stream_t stream) {
   if (!c) FAIL(SRL_EINVAL, "srl_ppo_step: null ctx");
+  if (srl_status st = comm_check(c, "srl_ppo_step")) return st;
   if (n_local < 1 || n_local > c->max_n || n_global < (valid ? 1 : n_local))
     FAIL(SRL_EINVAL, "srl_ppo_step: need 1 <= n_local <= max_local_n, n_global >= n_local "
                      "(>= 1 with a valid mask)");
@@ -823,7 +895,8 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     else if (p2p) {
       ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8) * c->world);
       c->epoch = epoch;
-      CK(launch_p2p_allreduce(c->peers, c->world, c->rank, xoff, c->P + 8, epoch, c->grads, s));
+      CK(launch_p2p_allreduce(c->peers, c->world, c->rank, xoff, c->P + 8, epoch, 1.f, c->grads,
+                              c->cc, 3, s));
     }
     else if (c->world > 1) {
       ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8));
@@ -839,11 +912,13 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     // ---------------- a7: Adam + fp16 shadow refresh
     ProfScope ps(c, s, "adam", 0.0, 30.0 * c->P);
     CK(launch_adam(segs, c->P, c->params, c->m, c->v, c->grads, c->t_dev, c->cfg.lr,
-                   c->cfg.beta1, c->cfg.beta2, c->cfg.adam_eps, s, gclip ? c->gn_coef() : nullptr));
+                   c->cfg.beta1, c->cfg.beta2, c->cfg.adam_eps, s, gclip ? c->gn_coef() : nullptr,
+                   c->world > 1 ? c->cc.err_dev : nullptr));
   }
   CK(launch_stats(c->grads, c->P, adv_mean_std, n_global, c->cfg.value_coef, c->cfg.entropy_coef,
                   c->t_dev, apply, stats_out, s, c->counters,
-                  (apply && c->cfg.max_grad_norm > 0.f) ? c->gn_norm() : nullptr));
+                  (apply && c->cfg.max_grad_norm > 0.f) ? c->gn_norm() : nullptr,
+                  c->world > 1 ? c->cc.err_dev : nullptr));
   return SRL_OK;
 }
 
@@ -855,6 +930,7 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
                                          const int32_t* actions, const float* logp_old,
                                          srl_ppo_stats* stats_out, srl_stream_t stream) {
   if (!c) FAIL(SRL_EINVAL, "srl_ppo_train_step: null ctx");
+  if (srl_status st = comm_check(c, "srl_ppo_train_step")) return st;
   if (T < 1 || B < 1 || (int64_t)T * B > c->max_n || n_global < (valid ? 1 : (int64_t)T * B))
     FAIL(SRL_EINVAL, "srl_ppo_train_step: need 1 <= T*B <= max_local_n, T*B <= n_global "
                      "(n_global >= 1 with a valid mask)");
@@ -877,7 +953,7 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
     ProfScope ps(c, s, "adv_norm", 0.0, 24.0 * c->world);
     if (c->p2p && !ar_overlap()) {
       CK(launch_p2p_moments(c->peers, c->world, c->rank, ++c->mepoch, c->gae_stats, c->mean_std,
-                            c->cfg.adv_unbiased, s));
+                            c->cfg.adv_unbiased, c->cc, 3, s));
     } else {
       double* gathered = c->norm_scratch;
       CKN(ncclAllGather(c->gae_stats, gathered, 3, ncclDouble, c->comm, s));
@@ -1090,5 +1166,58 @@ extern "C" srl_status srl_debug_gemm(int M, int N, int K, const uint16_t* A, int
               (int64_t)g.part_split_stride, M, N, (int64_t)g.ld_part, D));
   CK(cudaGetLastError());
   CK(cudaFreeAsync(part, s));
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ test hook: a2/a6 exchange
+// The production exchange kernels (p2p_allreduce_kernel, p2p_moments_kernel) run for `world`
+// VIRTUAL ranks on this one GPU: rank r's exposed bucket is x + r*ld and its sync block a local
+// allocation.  No launch ever waits on another (B200_PROFILING.md: ranks that spin on each
+// other must not be separate launches on one GPU): every flag a rank would wait for is
+// pre-published, and the phases run in order -- phase 1 (publish + reduce my chunk) of every
+// rank, then phase 2 (gather the other chunks) of every rank -- which is the order the real
+// flags enforce.
+static __global__ void fill_u64_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+extern "C" srl_status srl_debug_exchange(int world, int64_t count, int64_t ld, float* x, float* out,
+                                         float scale, const double* tri, double* mean_std,
+                                         int unbiased, srl_stream_t stream) {
+  if (world < 1 || world > kMaxPeers || count < 1 || ld < count || ld % 4 || !x || !out)
+    FAIL(SRL_EINVAL, "srl_debug_exchange: need 1 <= world <= 8, 1 <= count <= ld, ld % 4 == 0");
+  if ((tri == nullptr) != (mean_std == nullptr)) FAIL(SRL_EINVAL, "srl_debug_exchange: tri and mean_std go together");
+  if (srl_status st = require_device()) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long* sync = nullptr;
+  int* err = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&sync), kSyncBytes * world, s));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&err), sizeof(int) * 2, s));
+  CK(cudaMemsetAsync(sync, 0, kSyncBytes * world, s));
+  CK(cudaMemsetAsync(err, 0, sizeof(int) * 2, s));
+  const unsigned long long epoch = 1;
+  P2PPeers pe{};
+  for (int r = 0; r < world; ++r) {
+    pe.x[r] = x + (int64_t)r * ld;
+    pe.flag[r] = sync + (int64_t)r * kSyncWords;
+    // pre-publish every flag a rank waits for: phase-1 slots and the reduced-chunk slots
+    CK(launch_k(fill_u64_kernel, dim3(4), dim3(256), 0, s, 1, pe.flag[r], (int64_t)(2 * kMaxPeers), epoch));
+    CK(launch_k(fill_u64_kernel, dim3(4), dim3(256), 0, s, 1, p2p_rflags(pe.flag[r]),
+                (int64_t)kMaxPeers * kXBlocks, epoch));
+  }
+  CommCtl cc{err, err + 1, 1000000000ull};
+  for (int ph = 1; ph <= 2; ++ph)
+    for (int r = 0; r < world; ++r) {
+      CK(launch_p2p_allreduce(pe, world, r, 0, count, epoch, scale, out + (int64_t)r * ld, cc, ph, s));
+      if (tri) CK(launch_p2p_moments(pe, world, r, epoch, tri + 3 * r, mean_std + 2 * r, unbiased, cc, ph, s));
+    }
+  CK(cudaGetLastError());
+  int herr[2] = {0, 0};
+  CK(cudaMemcpyAsync(herr, err, sizeof(herr), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaFreeAsync(sync, s));
+  CK(cudaFreeAsync(err, s));
+  if (herr[0] || herr[1]) FAIL(SRL_ENCCL, "srl_debug_exchange: a pre-published wait timed out");
   return SRL_OK;
 }

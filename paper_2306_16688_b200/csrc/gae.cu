@@ -11,7 +11,7 @@
 //   register-resident), writes adv/ret and accumulates moments.
 // Integer inputs with gamma = lambda = 1 stay exact, so the result is bit-identical to the
 // sequential recursion (C-B1).
-// NEXT-3: a flag byte with bit 0 clear and bit 1 set is a time-limit truncation (reading R-T):
+// NEXT-3: a flag byte with (flag & 3) == 2 (bit 1 set, bit 0 clear) is a time-limit truncation (reading R-T):
 // with trunc values the cut step bootstraps from them; a valid mask (reading R-P) leaves
 // padding entries out of the moments (adv/ret are still written for every entry).  Moments per block are {n, mean, M2} in double, merged in a
 // fixed order (deterministic), shifted sums inside a thread.
@@ -122,7 +122,7 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
     for (int i = 0; i < TC; ++i) {
       const bool in = col_ok && t0 + i < T;
       const uint32_t f = fl[i];
-      const float boot = f ? ((tv && !(f & 1u)) ? tq[i] : 0.f) : v1[i];
+      const float boot = f ? ((tv && (f & 3u) == 2u) ? tq[i] : 0.f) : v1[i];
       delta[i] = in ? rr[i] + gamma * boot - v0[i] : 0.f;   // rows past T: identity step
       c[i] = in ? (f ? 0.f : gl) : 1.f;
       vt[i] = in ? v0[i] : 0.f;
@@ -333,44 +333,46 @@ __global__ void __launch_bounds__(256) merge_moments_kernel(const double* __rest
 // rank (parity of the epoch), fences, release-stores the epoch into rank r's flag; then waits
 // for every rank's flag here and merges the world triples in rank order with the same
 // merge_parts_block as the NCCL path (identical result on every rank and on both paths).
-__device__ __forceinline__ void st_rel_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
+// phases bit 0: publish this rank's triple; bit 1: wait for every rank's and merge.  A wait
+// past the timeout raises the CommCtl error words and leaves mean_std as it was.
 __global__ void __launch_bounds__(256) p2p_moments_kernel(const P2PPeers pe, int world, int rank,
                                                           unsigned long long epoch,
                                                           const double* __restrict__ local,
-                                                          double* mean_std, int unbiased) {
+                                                          double* mean_std, int unbiased,
+                                                          const CommCtl cc, int phases) {
   griddep_wait();
   griddep_launch();
   __shared__ double tri[kMaxPeers * 3];
+  __shared__ int s_ok;
   const int t = threadIdx.x;
   const int par = (int)(epoch & 1ull);
-  if (t < world) {
+  if (t == 0) s_ok = 1;
+  __syncthreads();
+  if ((phases & 1) && t < world) {
     double* dst = p2p_slots(pe.flag[t]) + (par * kMaxPeers + rank) * 4;
     dst[0] = local[0]; dst[1] = local[1]; dst[2] = local[2];
     __threadfence_system();
-    st_rel_sys(p2p_mflags(pe.flag[t]) + rank, epoch);
-    const unsigned long long* f = p2p_mflags(pe.flag[rank]) + t;
-    long long t0 = clock64();
-    while (ld_acq_sys(f) < epoch)
-      if (clock64() - t0 > (1ll << 35)) __trap();   // ~17 s: a missing rank is an error
-    const volatile double* src = p2p_slots(pe.flag[rank]) + (par * kMaxPeers + t) * 4;
-    tri[3 * t] = src[0]; tri[3 * t + 1] = src[1]; tri[3 * t + 2] = src[2];
+    st_release_sys(p2p_mflags(pe.flag[t]) + rank, epoch);
+  }
+  if (!(phases & 2)) return;
+  if (t < world) {
+    if (wait_epoch(p2p_mflags(pe.flag[rank]) + t, epoch, cc)) {
+      const volatile double* src = p2p_slots(pe.flag[rank]) + (par * kMaxPeers + t) * 4;
+      tri[3 * t] = src[0]; tri[3 * t + 1] = src[1]; tri[3 * t + 2] = src[2];
+    } else {
+      s_ok = 0;
+    }
   }
   __syncthreads();
+  if (!s_ok) return;
   merge_parts_block(tri, world, nullptr, mean_std, unbiased);
 }
 
 cudaError_t launch_p2p_moments(const P2PPeers& pe, int world, int rank, unsigned long long epoch,
-                               const double* local, double* mean_std, int unbiased, cudaStream_t s) {
+                               const double* local, double* mean_std, int unbiased,
+                               const CommCtl& cc, int phases, cudaStream_t s) {
   return launch_k(p2p_moments_kernel, dim3(1), dim3(256), 0, s, 1, pe, world, rank, epoch, local,
-                  mean_std, unbiased);
+                  mean_std, unbiased, cc, phases);
 }
 
 cudaError_t launch_merge_moments(const double* part, int count, double* out, double* mean_std,

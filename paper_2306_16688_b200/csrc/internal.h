@@ -109,33 +109,91 @@ cudaError_t launch_extras(int64_t P, float inv_n, const double* stats_part, int 
                           const unsigned long long* counters, float* bucket, cudaStream_t s);
 cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float* v,
                         const float* bucket, const int64_t* t_dev, float lr, float b1,
-                        float b2, float eps, cudaStream_t s, const float* coef = nullptr);
+                        float b2, float eps, cudaStream_t s, const float* coef = nullptr,
+                        const int* comm_err = nullptr);
 constexpr int kGradNormBlocks = 296;   // 2 x 148 SMs
 // a6 over NVLink peer memory (world <= 8 on one node): every rank's exposed bucket (double
 // buffered by step parity) and flag array, mapped into this process with CUDA IPC
 constexpr int kMaxPeers = 8;
+constexpr int kXBlocks = 148;             // CTAs of the two-shot exchange = sub-blocks per chunk
 struct P2PPeers {
   float* x[kMaxPeers];                    // rank r's exposed buckets [2][count]
-  unsigned long long* flag[kMaxPeers];    // rank r's flags [kMaxPeers]: flag[src] = src's epoch
+  unsigned long long* flag[kMaxPeers];    // rank r's sync block (layout below)
 };
-// layout of every rank's IPC-mapped sync block (flag[r] points at rank r's): [0, 8) gradient
-// flags, [8, 16) moments flags, then doubles [2 parity][kMaxPeers][4] moment slots
+// layout of every rank's IPC-mapped sync block (flag[r] points at rank r's), in u64 words:
+//   [0, 8)    bucket-published flags, slot src = src's epoch            (exchange phase 1)
+//   [8, 16)   moments flags, slot src = src's moments epoch             (a2)
+//   [16, 80)  doubles [2 parity][kMaxPeers][4] moment slots             (a2)
+//   [80, 80 + kMaxPeers * kXBlocks) reduced-chunk flags [src][block]    (exchange phase 2)
 __host__ __device__ inline unsigned long long* p2p_mflags(unsigned long long* base) { return base + kMaxPeers; }
 __host__ __device__ inline double* p2p_slots(unsigned long long* base) {
   return reinterpret_cast<double*>(base + 2 * kMaxPeers);
 }
-constexpr size_t kSyncBytes = sizeof(unsigned long long) * 2 * kMaxPeers + sizeof(double) * 2 * kMaxPeers * 4;
+__host__ __device__ inline unsigned long long* p2p_rflags(unsigned long long* base) {
+  return base + 2 * kMaxPeers + 2 * kMaxPeers * 4;
+}
+constexpr size_t kSyncWords = 2 * kMaxPeers + 2 * kMaxPeers * 4 + kMaxPeers * kXBlocks;
+constexpr size_t kSyncBytes = sizeof(unsigned long long) * kSyncWords;
+// bounded waits of the exchange kernels (SPEC.md S:L532 ReduceTimeout): a wait that exceeds
+// timeout_ns sets *err_dev and *err_host (host-mapped) to 1 and the kernel leaves without
+// trapping; Adam then skips (err_dev) and the next srl_* call on the context returns SRL_ENCCL.
+struct CommCtl {
+  int* err_dev;                 // device word, read by adam_kernel / stats_kernel
+  int* err_host;                // device alias of pinned host memory, read by the host
+  unsigned long long timeout_ns;
+};
+// phases: bit 0 = publish / reduce my chunk, bit 1 = gather the other chunks (3 = both; the
+// single-GPU virtual-rank test runs bit 0 for every rank, then bit 1 for every rank).
 cudaError_t launch_p2p_moments(const P2PPeers& pe, int world, int rank, unsigned long long epoch,
-                               const double* local, double* mean_std, int unbiased, cudaStream_t s);
+                               const double* local, double* mean_std, int unbiased,
+                               const CommCtl& cc, int phases, cudaStream_t s);
 cudaError_t launch_p2p_allreduce(const P2PPeers& pe, int world, int rank, int64_t off,
-                                 int64_t count, unsigned long long epoch, float* out,
-                                 cudaStream_t s);
+                                 int64_t count, unsigned long long epoch, float scale, float* out,
+                                 const CommCtl& cc, int phases, cudaStream_t s);
 cudaError_t launch_gradnorm(const float* bucket, int64_t P, double* part, unsigned int* counter,
                             float max_norm, double* norm_out, float* coef_out, cudaStream_t s);
 cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s);
 cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,
                          int64_t n_global, float value_coef, float entropy_coef,
                          int64_t* t_dev, int apply, void* stats_out, cudaStream_t s,
-                         unsigned long long* counters = nullptr, const double* gnorm = nullptr);
+                         unsigned long long* counters = nullptr, const double* gnorm = nullptr,
+                         const int* comm_err = nullptr);
+// spin helpers shared by the exchange kernels (misc.cu, gae.cu)
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void comm_fail(const CommCtl& cc) {
+  *reinterpret_cast<volatile int*>(cc.err_dev) = 1;
+  *reinterpret_cast<volatile int*>(cc.err_host) = 1;
+  __threadfence_system();
+}
+// wait until *f >= epoch; false (and the error raised) after cc.timeout_ns or once another
+// wait of this step has failed
+__device__ __forceinline__ bool wait_epoch(const unsigned long long* f, unsigned long long epoch,
+                                           const CommCtl& cc) {
+  if (ld_acquire_sys(f) >= epoch) return true;
+  const unsigned long long t0 = globaltimer_ns();
+  uint32_t it = 0;
+  while (ld_acquire_sys(f) < epoch) {
+    if ((++it & 255u) == 0) {
+      if (*reinterpret_cast<volatile int*>(cc.err_dev)) return false;
+      if (globaltimer_ns() - t0 > cc.timeout_ns) {
+        comm_fail(cc);
+        return false;
+      }
+    }
+  }
+  return true;
+}
 
 }  // namespace srl

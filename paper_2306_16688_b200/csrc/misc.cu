@@ -170,10 +170,11 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
                                                    const float* __restrict__ g,
                                                    const int64_t* __restrict__ t_dev, float lr,
                                                    float b1, float b2, float eps,
-                                                   const float* __restrict__ coef) {
+                                                   const float* __restrict__ coef,
+                                                   const int* __restrict__ comm_err) {
   griddep_wait();
   griddep_launch();
-  if (g[P + 5] > 0.f) return;
+  if (g[P + 5] > 0.f || (comm_err && *comm_err)) return;
   const float cf = coef ? *coef : 1.f;           // NEXT-3 global-norm clip coefficient
   const Segment& s = t.s[blockIdx.y];            // one segment per grid row
   const int cnt = s.rows * s.cols;
@@ -232,13 +233,13 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
 
 cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float* v,
                         const float* bucket, const int64_t* t_dev, float lr, float b1, float b2,
-                        float eps, cudaStream_t s, const float* coef) {
+                        float eps, cudaStream_t s, const float* coef, const int* comm_err) {
   int64_t maxq = 1;
   for (int i = 0; i < t.n; ++i) maxq = std::max<int64_t>(maxq, ((int64_t)t.s[i].rows * t.s[i].cols + 3) / 4);
   int64_t bx = (maxq + 255) / 256;
   if (bx > 4 * num_sms()) bx = 4 * num_sms();
   return launch_k(adam_kernel, dim3((unsigned)bx, (unsigned)t.n), dim3(256), 0, s, 1, t, P, p, m,
-                  v, bucket, t_dev, lr, b1, b2, eps, coef);
+                  v, bucket, t_dev, lr, b1, b2, eps, coef, comm_err);
 }
 
 // NEXT-3 global gradient-norm clipping (reading R-G, PyTorch clip_grad_norm_ semantics):
@@ -289,66 +290,106 @@ __global__ void __launch_bounds__(256) gradnorm_kernel(const float* __restrict__
   }
 }
 
-// a6 as a one-shot allreduce over NVLink peer memory.  The finalise / extras kernels of this
-// step wrote this rank's 1/N-scaled bucket into its exposed buffer x[rank][parity]; here
-// block 0 publishes it (system fence, then a release store of the step's epoch into every
-// rank's flag slot for this rank), every block waits until all ranks have published, then
-// sums the world buffers element by element in rank order 0..world-1 straight from the
-// peers' HBM (ld.global.cg: peer loads bypass the remote L2 and must not hit a stale L1 line).
-// Same order on every rank -> bit-identical sums everywhere (replicated Adam stays in sync).
-// Double buffering by epoch parity is safe: rank A cannot start writing step k+2 into a
-// buffer before rank B has read it for step k, because A's step k+1 waits for B's step k+1
-// publication, which B issues only after finishing step k.
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+// a6 as a two-shot allreduce over NVLink peer memory (reduce-scatter, then all-gather; SPEC
+// reduce_gradients S:L505-513, "gradient synchronisation").  The finalise /
+// extras kernels of this step wrote this rank's 1/N-scaled bucket into its exposed buffer
+// x[rank][parity].  The bucket is cut into `world` chunks (float4 aligned); chunk r belongs
+// to rank r and is cut into gridDim.x sub-blocks, one per CTA.
+//   phase 1: block 0 publishes the bucket (system fence, release store of the step's epoch
+//     into every rank's phase-1 slot for this rank); every CTA waits for all ranks, then sums
+//     ITS sub-block of MY chunk over the world buffers in rank order 0..world-1 (ld.global.cg
+//     from the peers' HBM), writes the result to `out` and back into x[rank] in place (no
+//     other rank reads that range of x[rank] in phase 1), and publishes a per-(rank, block)
+//     flag to every rank.
+//   phase 2: CTA g waits for the flag (j, g) of every other rank j and copies sub-block g of
+//     chunk j from x[j] into `out`.
+// Every element is summed once, by its owner, in rank order: bit-identical on all ranks.
+// Traffic per rank 2 (world-1)/world x bytes over NVLink (the one-shot form read world-1 x).
+// Double buffering by epoch parity is safe: rank A writes step k+2 into a buffer only after
+// its step k+1 exchange saw B's step k+1 phase-1 publication, which B issues after finishing
+// step k (including its phase-2 reads of A's buffer).
+// Waits are bounded (CommCtl): on timeout the error words are raised and the kernel leaves.
+__device__ __forceinline__ int64_t split4(int64_t len, int k, int parts) {
+  return k >= parts ? len : ((len * k / parts) & ~int64_t(3));   // float4-aligned cut points
 }
 
-__global__ void __launch_bounds__(256) p2p_allreduce_kernel(const P2PPeers pe, int world, int rank,
-                                                            int64_t off, int64_t count,
-                                                            unsigned long long epoch,
-                                                            float* __restrict__ out) {
-  griddep_wait();
-  griddep_launch();
-  if (blockIdx.x == 0 && threadIdx.x < world) {
-    __threadfence_system();
-    st_release_sys(pe.flag[threadIdx.x] + rank, epoch);
-  }
-  if (threadIdx.x < world) {
-    const unsigned long long* f = pe.flag[rank] + threadIdx.x;
-    long long t0 = clock64();
-    while (ld_acquire_sys(f) < epoch) {
-      if (clock64() - t0 > (1ll << 35)) __trap();   // ~17 s: a missing rank is an error, not a hang
-    }
-  }
-  __syncthreads();
-  const int64_t nq = count >> 2;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
-       q += (int64_t)gridDim.x * blockDim.x) {
+__device__ __forceinline__ void sum_range(const P2PPeers& pe, int world, int64_t off, int64_t lo,
+                                          int64_t hi, float scale, float* out, float* own) {
+  const int64_t q0 = (lo + 3) >> 2, q1 = hi >> 2;        // lo is a multiple of 4
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     float4 s = __ldcg(reinterpret_cast<const float4*>(pe.x[0] + off) + q);
     for (int r = 1; r < world; ++r) {
       const float4 v = __ldcg(reinterpret_cast<const float4*>(pe.x[r] + off) + q);
       s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
+    s.x *= scale; s.y *= scale; s.z *= scale; s.w *= scale;
     reinterpret_cast<float4*>(out)[q] = s;
+    reinterpret_cast<float4*>(own)[q] = s;
   }
-  if (blockIdx.x == 0)
-    for (int64_t i = 4 * nq + threadIdx.x; i < count; i += blockDim.x) {
-      float s = __ldcg(pe.x[0] + off + i);
-      for (int r = 1; r < world; ++r) s += __ldcg(pe.x[r] + off + i);
-      out[i] = s;
+  for (int64_t i = 4 * q1 + threadIdx.x; i < hi; i += blockDim.x) {   // ragged end of the bucket
+    float s = __ldcg(pe.x[0] + off + i);
+    for (int r = 1; r < world; ++r) s += __ldcg(pe.x[r] + off + i);
+    s *= scale;
+    out[i] = s;
+    own[i] = s;
+  }
+}
+
+__global__ void __launch_bounds__(512) p2p_allreduce_kernel(const P2PPeers pe, int world, int rank,
+                                                            int64_t off, int64_t count,
+                                                            unsigned long long epoch, float scale,
+                                                            float* __restrict__ out,
+                                                            const CommCtl cc, int phases) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ int s_ok;
+  const int g = blockIdx.x, G = gridDim.x;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (phases & 1) {
+    if (g == 0 && threadIdx.x < world) {
+      __threadfence_system();
+      st_release_sys(pe.flag[threadIdx.x] + rank, epoch);
     }
+    if (threadIdx.x < world && !wait_epoch(pe.flag[rank] + threadIdx.x, epoch, cc)) s_ok = 0;
+    __syncthreads();
+    if (!s_ok) return;
+    const int64_t c0 = split4(count, rank, world), c1 = split4(count, rank + 1, world);
+    const int64_t lo = c0 + split4(c1 - c0, g, G), hi = c0 + split4(c1 - c0, g + 1, G);
+    sum_range(pe, world, off, lo, hi, scale, out, pe.x[rank] + off);
+    __syncthreads();
+    if (threadIdx.x < world) {
+      __threadfence_system();
+      st_release_sys(p2p_rflags(pe.flag[threadIdx.x]) + rank * kXBlocks + g, epoch);
+    }
+  }
+  if (phases & 2) {
+    for (int j = 0; j < world; ++j) {
+      if (j == rank) continue;
+      if (threadIdx.x == 0 && !wait_epoch(p2p_rflags(pe.flag[rank]) + j * kXBlocks + g, epoch, cc))
+        s_ok = 0;
+      __syncthreads();
+      if (!s_ok) return;
+      const int64_t c0 = split4(count, j, world), c1 = split4(count, j + 1, world);
+      const int64_t lo = c0 + split4(c1 - c0, g, G), hi = c0 + split4(c1 - c0, g + 1, G);
+      const float* src = pe.x[j] + off;
+      for (int64_t q = (lo >> 2) + threadIdx.x; q < (hi >> 2); q += blockDim.x)
+        reinterpret_cast<float4*>(out)[q] = __ldcg(reinterpret_cast<const float4*>(src) + q);
+      for (int64_t i = (hi & ~int64_t(3)) + threadIdx.x; i < hi; i += blockDim.x)
+        if (i >= lo) out[i] = __ldcg(src + i);
+    }
+  }
 }
 
 cudaError_t launch_p2p_allreduce(const P2PPeers& pe, int world, int rank, int64_t off,
-                                 int64_t count, unsigned long long epoch, float* out,
-                                 cudaStream_t s) {
-  return launch_k(p2p_allreduce_kernel, dim3(2 * num_sms()), dim3(256), 0, s, 1, pe, world, rank,
-                  off, count, epoch, out);
+                                 int64_t count, unsigned long long epoch, float scale, float* out,
+                                 const CommCtl& cc, int phases, cudaStream_t s) {
+  // the same grid on every rank (the sub-block partition must agree): a function of count only
+  int64_t G = count / (4 * 1024);
+  if (G > kXBlocks) G = kXBlocks;
+  if (G < 1) G = 1;
+  return launch_k(p2p_allreduce_kernel, dim3((unsigned)G), dim3(512), 0, s, 1, pe, world, rank,
+                  off, count, epoch, scale, out, cc, phases);
 }
 
 cudaError_t launch_gradnorm(const float* bucket, int64_t P, double* part, unsigned int* counter,
@@ -379,12 +420,14 @@ cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s) {
 __global__ void stats_kernel(const float* __restrict__ bucket, int64_t P,
                              const double* __restrict__ mean_std, int64_t n_global, float cv,
                              float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
-                             unsigned long long* counters, const double* gnorm) {
+                             unsigned long long* counters, const double* gnorm,
+                             const int* comm_err) {
   griddep_wait();
   griddep_launch();
   const float* ex = bucket + P;
+  const int cerr = comm_err ? *comm_err : 0;
   if (counters) { counters[0] = 0; counters[1] = 0; }   // ready for the next step
-  if (apply && ex[5] == 0.f) t_dev[0] += 1;   // policy version (Code 1 inc_version)
+  if (apply && ex[5] == 0.f && !cerr) t_dev[0] += 1;   // policy version (Code 1 inc_version)
   if (!out) return;
   out->policy_loss = ex[0];
   out->value_loss = ex[1];
@@ -399,15 +442,16 @@ __global__ void stats_kernel(const float* __restrict__ bucket, int64_t P,
   out->fp16_saturated = (int64_t)ex[6];
   out->step = t_dev[0];
   out->grad_norm = gnorm ? *gnorm : 0.0;
+  out->comm_error = cerr;
 }
 
 cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,
                          int64_t n_global, float value_coef, float entropy_coef, int64_t* t_dev,
                          int apply, void* stats_out, cudaStream_t s, unsigned long long* counters,
-                         const double* gnorm) {
+                         const double* gnorm, const int* comm_err) {
   return launch_k(stats_kernel, dim3(1), dim3(1), 0, s, 1, bucket, P, mean_std, n_global,
                   value_coef, entropy_coef, t_dev, apply, static_cast<srl_ppo_stats*>(stats_out),
-                  counters, gnorm);
+                  counters, gnorm, comm_err);
 }
 
 }  // namespace srl

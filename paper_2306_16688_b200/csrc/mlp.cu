@@ -1,6 +1,7 @@
 // mlp.cu -- TMA descriptor encoding and the GEMM instantiations used by the trainer step.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "internal.h"
@@ -50,11 +51,15 @@ static cudaError_t launch_one(const CUtensorMap& ta, const CUtensorMap& tb, cons
   if (a.stages < 2) return cudaErrorInvalidConfiguration;
   const size_t smem = 1024 + smem_layout(BN, E, a.stages, a.colsum_ld, CG, zcols).total;
   if (smem + 512 > kSmemLimit) return cudaErrorInvalidConfiguration;
-  static size_t configured = 0;
-  if (smem > configured) {
+  // the attribute is per device: cache the configured size per device id (atomic: contexts on
+  // several devices may launch from several threads)
+  static std::atomic<size_t> configured[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  if (smem > configured[dev].load(std::memory_order_relaxed)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
+    configured[dev].store(smem, std::memory_order_relaxed);
   }
   cudaError_t e = launch_k(kern, dim3((unsigned)grid), dim3(kThreads), smem, s, CG, ta, tb, to, ty, a);
   if (e != cudaSuccess) return e;

@@ -22,7 +22,8 @@ EXPORTS = ("srl_last_error", "srl_abi_version", "srl_gae", "srl_adv_norm", "srl_
            "srl_ppo_load_params", "srl_ppo_step", "srl_ppo_train_step", "srl_batch_upload",
            "srl_ppo_train_step_slot", "srl_policy_rollout", "srl_ppo_comm_path",
            "srl_allreduce_grads", "srl_prof_enable",
-           "srl_prof_reset", "srl_prof_count", "srl_prof_read", "srl_debug_gemm")
+           "srl_prof_reset", "srl_prof_count", "srl_prof_read", "srl_debug_gemm",
+           "srl_debug_exchange")
 
 
 class SrlError(RuntimeError):
@@ -47,7 +48,7 @@ class PPOStatsC(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("policy_loss", "value_loss", "entropy", "clip_fraction",
                                           "approx_kl", "loss", "adv_mean", "adv_std")] + \
                [(k, C.c_int64) for k in ("n_global", "nonfinite", "fp16_saturated", "step")] + \
-               [("grad_norm", C.c_double)]
+               [("grad_norm", C.c_double), ("comm_error", C.c_int64)]
 
 
 STATS_BYTES = C.sizeof(PPOStatsC)
@@ -89,6 +90,7 @@ def lib():
     L.srl_allreduce_grads.argtypes = [vp, vp, i64, C.c_int, vp]
     L.srl_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
                                  C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
+    L.srl_debug_exchange.argtypes = [C.c_int, i64, i64, vp, vp, C.c_float, vp, vp, C.c_int, vp]
     L.srl_prof_enable.argtypes = [vp, C.c_int]
     L.srl_prof_reset.argtypes = [vp]
     L.srl_prof_count.argtypes = [vp]
@@ -114,9 +116,21 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
-def _cuda(t, dtype, name):
+def _cuda(t, dtype, name, shape=None, numel=None):
+    """Argument check before the C call (the library trusts shapes it cannot see)."""
     if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
         raise SrlError(f"{name}: need a contiguous CUDA {dtype} tensor, got {t.dtype} on {t.device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise SrlError(f"{name}: need shape {tuple(shape)}, got {tuple(t.shape)}")
+    if numel is not None and t.numel() != numel:
+        raise SrlError(f"{name}: need {numel} elements, got {t.numel()}")
+    return t
+
+
+def _host(t, dtype, name, numel):
+    if t.is_cuda or t.dtype != dtype or not t.is_contiguous() or t.numel() != numel:
+        raise SrlError(f"{name}: need a contiguous host {dtype} tensor of {numel} elements, got "
+                       f"{t.dtype} {tuple(t.shape)} on {t.device}")
     return t
 
 
@@ -219,6 +233,7 @@ class PPOContext:
         self._hid = (C.c_int * len(spec.hidden))(*spec.hidden)
         self._heads = (C.c_int * len(spec.heads))(*spec.heads)
         ld = spec.ld_obs or (spec.obs_dim + 7) // 8 * 8
+        self.ld_obs = ld
         self.cfg = PPOConfigC(spec.obs_dim, ld, len(spec.hidden), self._hid, len(spec.heads),
                               self._heads, spec.clip_eps, spec.value_coef, spec.entropy_coef,
                               spec.lr, spec.beta1, spec.beta2, spec.adam_eps, spec.adv_eps,
@@ -270,15 +285,16 @@ class PPOContext:
     def step(self, n_global, obs, actions, logp_old, adv, ret, adv_mean_std=None, apply=True,
              stats=None, stream=None, v_old=None, valid=None):
         """srl_ppo_step; returns the device stats buffer (uint8 [sizeof srl_ppo_stats])."""
-        _cuda(obs, torch.float16, "obs")
-        _cuda(actions, torch.int32, "actions")
-        for t, nm in ((logp_old, "logp_old"), (adv, "adv"), (ret, "ret")):
-            _cuda(t, torch.float32, nm)
-        if v_old is not None:
-            _cuda(v_old, torch.float32, "v_old")
-        if valid is not None:
-            _cuda(valid, torch.uint8, "valid")
         n_local = logp_old.numel()
+        H, ld = len(self.spec.heads), self.ld_obs
+        _cuda(obs, torch.float16, "obs", numel=n_local * ld)
+        _cuda(actions, torch.int32, "actions", numel=n_local * H)
+        for t, nm in ((logp_old, "logp_old"), (adv, "adv"), (ret, "ret")):
+            _cuda(t, torch.float32, nm, numel=n_local)
+        if v_old is not None:
+            _cuda(v_old, torch.float32, "v_old", numel=n_local)
+        if valid is not None:
+            _cuda(valid, torch.uint8, "valid", numel=n_local)
         if stats is None:
             stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
         _check(lib().srl_ppo_step(self.handle, n_local, int(n_global), _ptr(obs), _ptr(actions),
@@ -307,6 +323,17 @@ class PPOContext:
                    stream=None, trunc_values=None, valid=None):
         """srl_ppo_train_step: GAE -> normalisation -> update in one call (device inputs)."""
         T, B = rewards.shape
+        n, H, ld = T * B, len(self.spec.heads), self.ld_obs
+        _cuda(rewards, torch.float32, "rewards")
+        _cuda(values, torch.float32, "values", shape=(T + 1, B))
+        _cuda(dones, torch.uint8, "dones", shape=(T, B))
+        _cuda(obs, torch.float16, "obs", numel=n * ld)
+        _cuda(actions, torch.int32, "actions", numel=n * H)
+        _cuda(logp_old, torch.float32, "logp_old", numel=n)
+        if trunc_values is not None:
+            _cuda(trunc_values, torch.float32, "trunc_values", shape=(T, B))
+        if valid is not None:
+            _cuda(valid, torch.uint8, "valid", numel=n)
         if stats is None:
             stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
         _check(lib().srl_ppo_train_step(self.handle, T, B, int(n_global), _ptr(rewards),
@@ -318,10 +345,18 @@ class PPOContext:
     def upload(self, slot, rewards, values, dones, obs, actions, logp_old, trunc_values=None,
                valid=None):
         """NEXT-1: async H2D of a host batch (pinned CPU tensors) into device slot 0/1."""
-        for t in (rewards, values, dones, obs, actions, logp_old, trunc_values, valid):
-            if t is not None and (t.is_cuda or not t.is_contiguous()):
-                raise SrlError("upload: need contiguous host tensors")
         T, B = rewards.shape
+        n, H, ld = T * B, len(self.spec.heads), self.ld_obs
+        _host(rewards, torch.float32, "rewards", n)
+        _host(values, torch.float32, "values", (T + 1) * B)
+        _host(dones, torch.uint8, "dones", n)
+        _host(obs, torch.float16, "obs", n * ld)
+        _host(actions, torch.int32, "actions", n * H)
+        _host(logp_old, torch.float32, "logp_old", n)
+        if trunc_values is not None:
+            _host(trunc_values, torch.float32, "trunc_values", n)
+        if valid is not None:
+            _host(valid, torch.uint8, "valid", n)
         _check(lib().srl_batch_upload(self.handle, slot, T, B, _ptr(rewards), _ptr(values),
                                       _ptr(dones), _ptr(obs), _ptr(actions), _ptr(logp_old),
                                       _ptr(trunc_values), _ptr(valid)))
@@ -336,10 +371,10 @@ class PPOContext:
     def rollout(self, obs, keys=None, seed=0, deterministic=False, actions=None, logp=None,
                 value=None, stream=None):
         """NEXT-2 srl_policy_rollout: batched policy inference -> (actions i32 [n][H], logp, value)."""
-        _cuda(obs, torch.float16, "obs")
         n = obs.shape[0]
+        _cuda(obs, torch.float16, "obs", numel=n * self.ld_obs)
         if keys is not None:
-            _cuda(keys, torch.int64, "keys")
+            _cuda(keys, torch.int64, "keys", numel=n)
         dev = obs.device
         if actions is None:
             actions = torch.empty((n, len(self.spec.heads)), dtype=torch.int32, device=dev)
@@ -375,3 +410,20 @@ def debug_gemm(A, a_mn, B, b_mn, M, N, K, bn=128, splits=1, cg=1, stream=None):
     _check(lib().srl_debug_gemm(M, N, K, _ptr(A), int(a_mn), A.shape[1], _ptr(B), int(b_mn),
                                 B.shape[1], bn, splits, cg, _ptr(D), _stream(stream)))
     return D
+
+
+def debug_exchange(x, scale=1.0, tri=None, unbiased=False, stream=None):
+    """Test hook (srl_debug_exchange): the a6/a2 peer-memory exchange kernels for
+    world = x.shape[0] virtual ranks on this GPU.  x f32 [world][ld] (reduced in place);
+    returns (out [world][ld], mean_std [world][2] or None)."""
+    _cuda(x, torch.float32, "x")
+    world, ld = x.shape
+    out = torch.zeros_like(x)
+    ms = None
+    if tri is not None:
+        _cuda(tri, torch.float64, "tri", shape=(world, 3))
+        ms = torch.zeros((world, 2), dtype=torch.float64, device=x.device)
+    count = ld
+    _check(lib().srl_debug_exchange(world, count, ld, _ptr(x), _ptr(out), float(scale), _ptr(tri),
+                                    _ptr(ms), int(unbiased), _stream(stream)))
+    return out, ms

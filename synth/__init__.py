@@ -10,3 +10,4 @@ from .gen import (  # noqa: F401
     splitmix64, uniform, normal, make_batch, make_params, shard_columns,
     logp_old_uniform_policy,
 )
+from .torch_gen import make_batch_device  # noqa: F401

@@ -104,3 +104,47 @@ def oracle_term_scales(cfg, params, shards, o):
     near = np.sum(np.minimum(np.abs(rho - (1 + cfg.clip_eps)), np.abs(rho - (1 - cfg.clip_eps))) <= 1e-3)
     return dict(pg=np.mean(np.abs(rho * ahat)), v=o["sums"][1] / N, ent=o["sums"][2] / N,
                 kl=np.mean(np.abs(lp)), clip_near=near / N)
+
+
+def near_kink(cfg, params, obs, actions, logp_old, margin=KINK_MARGIN / 2, v_old=None, ret=None,
+              value_clip=0.0):
+    """Samples whose loss is within `margin` of a non-differentiable point at `params`, by the
+    oracle (DESIGN.md §3.3 R-K, §3.5 R-V): the log-ratio near log(1 +- eps), or (value clipping)
+    |V - v_old| near the band edge or the two value losses within `margin` of a tie.
+    The default margin is half the fixtures' (whose samples sit AT KINK_MARGIN, up to fp32
+    rounding of logp_old) and still 5x the kernel's ~1e-3 log-prob error."""
+    xi = oracle.log_pi(cfg, params, obs, actions) - np.asarray(logp_old, np.float64)
+    near = np.zeros(xi.size, bool)
+    for k in (np.log(1 + cfg.clip_eps), np.log(1 - cfg.clip_eps)):
+        near |= np.abs(xi - k) < margin
+    if value_clip > 0:
+        V = oracle.forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, obs)[:, -1]
+        vo = np.asarray(v_old, np.float64)
+        R = np.asarray(ret, np.float64)
+        d = V - vo
+        vc = vo + np.clip(d, -value_clip, value_clip)
+        near |= np.abs(np.abs(d) - value_clip) < margin
+        near |= (np.abs(d) > value_clip) & (np.abs((vc - R) ** 2 - (V - R) ** 2) < margin)
+    return near
+
+
+def value_kink_free(cfg, params, b, value_clip, margin=KINK_MARGIN, rounds=20):
+    """Nudge the rollout values (v_old = values rows 0..T-1, which also feed GAE) until no
+    sample is within `margin` of a value-clip kink at `params` (fixture for R-V parity)."""
+    b = dict(b)
+    vals = np.array(b["values"], np.float32)
+    T, Bk = vals.shape[0] - 1, vals.shape[1]
+    V = oracle.forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, b["obs"])[:, -1]
+    for _ in range(rounds):
+        _, r = oracle.gae(b["rewards"], vals, b["dones"], cfg.gamma, cfg.lam)
+        vo = vals[:-1].reshape(-1).astype(np.float64)
+        R = r.reshape(-1)
+        d = V - vo
+        vc = vo + np.clip(d, -value_clip, value_clip)
+        bad = np.abs(np.abs(d) - value_clip) < margin
+        bad |= (np.abs(d) > value_clip) & (np.abs((vc - R) ** 2 - (V - R) ** 2) < margin)
+        if not bad.any():
+            b["values"] = vals
+            return b
+        vals[:-1].reshape(-1)[bad] += np.float32(0.05)
+    raise RuntimeError("value_kink_free: did not converge")

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.srl_abi_version() == 2
+    assert L.srl_abi_version() == 3
 
 
 def test_sass_is_sm100a_tcgen05():

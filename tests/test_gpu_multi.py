@@ -114,3 +114,82 @@ def test_p2p_allreduce_equals_nccl_over_steps(world):
     d = np.abs(a[0][2].astype(np.float64) - b[0][2].astype(np.float64))
     assert d.max() <= 2 * 3e-4 * 3 + 1e-6 and np.mean(d > 1e-5) <= 1e-3
     assert a[0][1]["step"] == 1 and b[0][1]["step"] == 1
+
+
+def _api_worker(rank, world, port, q, p2p):
+    """srl_allreduce_grads (op 0 / 1, a bucket-sized buffer on the peer path and an oversized
+    one through NCCL) and srl_adv_norm(ctx, world > 1) with data on every rank."""
+    import sys
+    os.environ["SRL_P2P_AR"] = p2p
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        import synth
+        import paper_2306_16688_b200 as P
+        from paper_2306_16688_b200.dist import broadcast_unique_id
+        cfg = synth.get_config("gfootball").with_(B=16)
+        uid = broadcast_unique_id(device=torch.device("cuda", rank))
+        ctx = P.PPOContext(P.NetSpec.from_config(cfg), max_local_n=cfg.T * cfg.B // world,
+                           rank=rank, world=world, nccl_id=uid, device=rank)
+        res = {"path": ctx.comm_path}
+        for name, count in (("small", ctx.P + 8), ("big", 3 * ctx.P + 5)):
+            for op in (0, 1):
+                g = torch.Generator().manual_seed(1000 * op + count)
+                allx = torch.randn((world, count), generator=g)      # every rank's input
+                buf = allx[rank].clone().cuda()
+                ctx.allreduce_grads(buf, op=op)
+                res[(name, op)] = (buf.cpu().numpy(), allx.numpy())
+        g = torch.Generator().manual_seed(77)
+        alla = torch.randn((world, 5000), generator=g, dtype=torch.float64) * 3 + 1
+        adv = alla[rank].float().cuda()
+        ms = P.adv_norm(adv, ctx=ctx)
+        res["ms"] = (ms.cpu().numpy(), alla.float().double().numpy())
+        torch.cuda.synchronize()
+        q.put((rank, res))
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_allreduce_grads_and_adv_norm_api(world, p2p):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    import torch.multiprocessing as mp
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _port()
+    procs = [mpc.Process(target=_api_worker, args=(r, world, port, q, p2p)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert res[0][1]["path"] == ("nvlink-p2p" if p2p == "1" else "nccl")
+    for key in [("small", 0), ("small", 1), ("big", 0), ("big", 1)]:
+        outs = [r[1][key][0] for r in res]
+        allx = res[0][1][key][1]
+        ref = allx[0].copy()
+        for k in range(1, world):
+            ref = ref + allx[k]                       # fp32 rank-order sum
+        if key[1] == 1:
+            ref = ref * np.float32(1.0 / world)
+        for o in outs[1:]:                            # identical on every rank
+            assert np.array_equal(o, outs[0])
+        if p2p == "1" and key[0] == "small":          # the peer path: rank order, bit-exact
+            assert np.array_equal(outs[0], ref)
+        else:                                         # NCCL's order: fp32 rounding
+            assert np.allclose(outs[0], ref, rtol=1e-5, atol=1e-5 * np.abs(ref).max())
+    ms, alla = res[0][1]["ms"]
+    _, mu, sd = oracle.adv_norm(alla.reshape(-1))
+    for r in res:
+        assert np.array_equal(r[1]["ms"][0], ms)
+    assert abs(ms[0] - mu) <= 1e-12 * sd and abs(ms[1] - sd) <= 1e-12 * sd

@@ -128,17 +128,32 @@ def test_grad_norm_clip_identical_g(frac):
     assert st["step"] == 1
 
 
+def _probe_grad(cfg, p0, n_mb, obs, actions, logp_old, adv, ret, ms, vold, keep, **kw):
+    """The kernel's gradient at parameters p0 over the kept rows of one minibatch (padding
+    mask = the rows away from every kink), mean over the minibatch's n_mb rows."""
+    probe = _ctx(cfg, p0.astype(np.float32), n_mb, **kw)
+    vm = torch.from_numpy(keep.astype(np.uint8)).cuda()
+    probe.step(n_mb, obs, actions, logp_old, adv, ret, ms, apply=False, v_old=vold, valid=vm)
+    return probe.grads().cpu().numpy().astype(np.float64)[:cfg.n_params]
+
+
 @pytest.mark.parametrize("E,M", [(2, 1), (1, 3), (2, 2)])
 def test_epochs_minibatches_equal_composed_steps(E, M):
     """srl_ppo_train_step with E x M updates is bit-identical to E x M srl_ppo_step calls on
-    the minibatch row ranges (R-M), and each update's gradient matches the oracle's gradient
-    of that minibatch at the parameters the update started from.  Value clipping and
-    gradient-norm clipping on, so all of NEXT-3 runs in one step."""
+    the minibatch row ranges (R-M).  Each update's gradient is held to per-tensor C-T3 against
+    the oracle's gradient of that minibatch at the parameters the update started from:
+    update 1 on every sample (the fixture is kink-free at theta_0 for the policy clip and the
+    value clip); later updates, whose parameters have moved, on the samples the oracle finds
+    away from both kinks at those parameters (DESIGN.md §3.3 R-K, §3.5 R-V), through the
+    kernel's padding mask.  Value clipping and gradient-norm clipping on: all of NEXT-3 runs."""
     import paper_2306_16688_b200 as P
+    from ppo_harness import near_kink, value_kink_free
     cfg = synth.get_config("gfootball").with_(B=20)
     params, b = make_inputs(cfg, seed=13)
+    ev = 0.2
+    b = value_kink_free(cfg, params, b, ev)
     n = b["n"]
-    kw = dict(epochs=E, minibatches=M, value_clip=0.2, max_grad_norm=0.05)
+    kw = dict(epochs=E, minibatches=M, value_clip=ev, max_grad_norm=0.05)
     dv = to_dev(b)
     a = _ctx(cfg, params, n, **kw)
     st = P.decode_stats(a.train_step(n, dv["rewards"], dv["values"], dv["dones"], dv["obs"],
@@ -149,21 +164,33 @@ def test_epochs_minibatches_equal_composed_steps(E, M):
     ms = P.adv_norm(adv, local_stats=gst)
     vold = dv["values"][:-1].reshape(-1)
     mu, sd = ms.cpu().numpy()
+    u = 0
     for e in range(E):
         for lo, hi in oracle.minibatch_bounds(n, M):
             p0 = c.params().cpu().numpy().astype(np.float64)
             c.step(hi - lo, dv["obs"][lo:hi], dv["actions"][lo:hi], dv["logp_old"][lo:hi],
                    adv[lo:hi], ret[lo:hi], ms, apply=True, v_old=vold[lo:hi])
-            G = c.grads().cpu().numpy().astype(np.float64)[:cfg.n_params]
             ah = (adv[lo:hi].cpu().numpy().astype(np.float64) - mu) / (sd + 1e-8)
+            rr, vo = ret[lo:hi].cpu().numpy(), vold[lo:hi].cpu().numpy()
+            near = near_kink(cfg, p0, b["obs"][lo:hi], b["actions"][lo:hi], b["logp_old"][lo:hi],
+                             v_old=vo, ret=rr, value_clip=ev)
+            keep = ~near
+            if u == 0:
+                assert not near.any()              # the fixture is kink-free at theta_0
+                G = c.grads().cpu().numpy().astype(np.float64)[:cfg.n_params]
+            else:
+                assert keep.mean() > 0.9
+                G = _probe_grad(cfg, p0, hi - lo, dv["obs"][lo:hi], dv["actions"][lo:hi],
+                                dv["logp_old"][lo:hi], adv[lo:hi], ret[lo:hi], ms, vold[lo:hi],
+                                keep, value_clip=ev)
+            rows = np.flatnonzero(keep)
             g, _, _ = oracle.loss_and_grad(
-                cfg.obs_dim, cfg.hidden, cfg.heads, p0, b["obs"][lo:hi], b["actions"][lo:hi],
-                b["logp_old"][lo:hi], ah, ret[lo:hi].cpu().numpy(), cfg.clip_eps,
-                cfg.value_coef, cfg.entropy_coef, v_old=vold[lo:hi].cpu().numpy(),
-                value_clip=0.2)
-            # kink flips of the value clip are possible at later updates (params moved):
-            # compare at the C-T3 bound on the whole vector
-            assert np.linalg.norm(G - g) <= 5 * TOL * np.linalg.norm(g)
+                cfg.obs_dim, cfg.hidden, cfg.heads, p0, b["obs"][lo:hi][rows],
+                b["actions"][lo:hi][rows], b["logp_old"][lo:hi][rows], ah[rows], rr[rows],
+                cfg.clip_eps, cfg.value_coef, cfg.entropy_coef, grad_scale=1.0 / (hi - lo),
+                v_old=vo[rows], value_clip=ev)
+            _check_grads(cfg, G, g)                # per tensor C-T3
+            u += 1
     torch.cuda.synchronize()
     assert torch.equal(a.params(), c.params()) and torch.equal(a.grads(), c.grads())
     assert st["step"] == E * M
@@ -189,7 +216,8 @@ def test_minibatches_reject_bad_sizes():
 # ------------------------------------------------------------------ R-T / R-P in the GAE scan
 def _flags_tv_valid(rng, T, B):
     u = rng.random((T, B))
-    f = np.where(u < 0.03, 1, np.where(u < 0.06, 2, np.where(u < 0.07, 3, 0))).astype(np.uint8)
+    # 1 terminal, 2 time limit, 3 terminal (bit 0 wins), 4 terminal, 6 time limit ((f & 3) == 2)
+    f = np.select([u < 0.03, u < 0.06, u < 0.07, u < 0.075, u < 0.08], [1, 2, 3, 4, 6], 0).astype(np.uint8)
     valid = (rng.random((T, B)) < 0.8).astype(np.uint8)
     return f, valid
 

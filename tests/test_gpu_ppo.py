@@ -182,3 +182,62 @@ def test_prefetch_slots_equal_device_path():
     assert torch.equal(a.params(), c.params()) and torch.equal(a.grads(), c.grads())
     with pytest.raises(P.SrlError):
         c.train_step_slot(0, b["n"])          # consumed: nothing uploaded into slot 0 since
+
+
+def test_prefetch_slots_against_oracle():
+    """NEXT-1 slot path (host batch -> device slot on the copy stream -> train step) checked
+    against the ORACLE at every one of 3 chained steps, not against the device path:
+    step k's gradient vs the oracle's gradient of the batch at the parameters step k started
+    from (C-T3; from step 2 on over the samples the oracle finds away from the clip kinks at
+    those parameters, through the padding mask), and step k's parameter / Adam-moment update
+    vs the oracle's Adam (C-6) applied to that same gradient with the moments carried in
+    double from step 1 (C-T5, 'identical G')."""
+    import paper_2306_16688_b200 as P
+    from ppo_harness import near_kink
+    cfg = synth.get_config("gfootball").with_(B=16)
+    params, b = make_inputs(cfg, seed=8)
+    n = b["n"]
+    keys = ("rewards", "values", "dones", "obs", "actions", "logp_old")
+    host = [torch.from_numpy(np.ascontiguousarray(b[k])).pin_memory() for k in keys]
+    spec = P.NetSpec.from_config(cfg)
+    c = P.PPOContext(spec, max_local_n=n)
+    c.load_params(torch.from_numpy(params).cuda())
+    o0 = oracle.ppo_step(cfg, params, [b], apply=False)
+    ahat = (o0["adv"][0] - o0["mean"]) / (o0["std"] + 1e-8)
+    m = np.zeros(cfg.n_params)
+    v = np.zeros(cfg.n_params)
+    c.upload(0, *host)
+    for k in range(3):
+        p_k = c.params().cpu().numpy().astype(np.float64)
+        if k + 1 < 3:
+            c.upload((k + 1) % 2, *host)
+        st = P.decode_stats(c.train_step_slot(k % 2, n))
+        torch.cuda.synchronize()
+        G = c.grads().cpu().numpy().astype(np.float64)[:cfg.n_params]
+        near = near_kink(cfg, p_k, b["obs"], b["actions"], b["logp_old"])
+        if k == 0:
+            assert not near.any()
+            Gk = G
+        else:
+            assert near.mean() < 0.05
+            probe = P.PPOContext(spec, max_local_n=n)
+            probe.load_params(torch.from_numpy(p_k.astype(np.float32)).cuda())
+            d = {kk: torch.from_numpy(np.ascontiguousarray(b[kk])).cuda() for kk in keys}
+            adv, ret, gst = P.gae(d["rewards"], d["values"], d["dones"], cfg.gamma, cfg.lam)
+            ms = P.adv_norm(adv.reshape(-1), local_stats=gst)
+            probe.step(n, d["obs"], d["actions"], d["logp_old"], adv.reshape(-1), ret.reshape(-1), ms,
+                       apply=False, valid=torch.from_numpy((~near).astype(np.uint8)).cuda())
+            Gk = probe.grads().cpu().numpy().astype(np.float64)[:cfg.n_params]
+        rows = np.flatnonzero(~near)
+        g, _, _ = oracle.loss_and_grad(cfg.obs_dim, cfg.hidden, cfg.heads, p_k, b["obs"][rows],
+                                       b["actions"][rows], b["logp_old"][rows], ahat[rows],
+                                       o0["ret"][0][rows], cfg.clip_eps, cfg.value_coef,
+                                       cfg.entropy_coef, grad_scale=1.0 / n)
+        _check_grads(cfg, Gk, g)
+        p_ref = p_k.copy()
+        oracle.adam(p_ref, m, v, G, k + 1, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps)
+        p_next = c.params().cpu().numpy().astype(np.float64)
+        assert np.linalg.norm((p_next - p_k) - (p_ref - p_k)) <= 1e-5 * np.linalg.norm(p_ref - p_k)
+        mg = c.adam_state()[0].cpu().numpy().astype(np.float64)
+        assert np.abs(mg - m).max() <= 1e-6 * np.abs(m).max()
+        assert st["step"] == k + 1

@@ -4,6 +4,7 @@ import pytest
 
 import oracle
 import synth
+from ppo_harness import make_inputs
 
 
 def test_adam_step1_closed_form():
@@ -68,3 +69,16 @@ def test_kshard_opposite_grads_cancel():
     rng = np.random.default_rng(3)
     g = rng.normal(size=1000)
     assert np.array_equal(g + (-g), np.zeros_like(g))
+
+
+@pytest.mark.parametrize("threads", [2, 3, 8])
+def test_all_core_driver_equals_single_thread(threads):
+    """bench.py's all-core cpu_baseline driver (oracle_loss_and_grad_mt) computes the same
+    gradient and loss sums as oracle_loss_and_grad, up to the order of the block sums."""
+    cfg = synth.get_config("gfootball").with_(B=6)
+    params, b = make_inputs(cfg, seed=2)
+    o1 = oracle.ppo_step(cfg, params, [b], apply=True)
+    oT = oracle.ppo_step(cfg, params, [b], apply=True, threads=threads)
+    assert np.linalg.norm(oT["grad"] - o1["grad"]) <= 1e-12 * np.linalg.norm(o1["grad"])
+    assert np.allclose(oT["sums"], o1["sums"], rtol=1e-12, atol=1e-12)
+    assert np.linalg.norm(oT["params"] - o1["params"]) <= 1e-12 * np.linalg.norm(o1["params"])

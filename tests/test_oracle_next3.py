@@ -185,6 +185,11 @@ def test_truncation_hand_case():
     # a terminal flag (bit 0) wins over a truncation bit
     a3, _ = oracle.gae(r, v, np.array([[0], [3], [0]], np.uint8), 0.5, 1.0, trunc_values=tv)
     assert a3[1, 0] == 1.0
+    # only (flag & 3) == 2 is a time limit (DESIGN.md §3.5 R-T): 0x04 is terminal, 0x06 truncates
+    a4, _ = oracle.gae(r, v, np.array([[0], [4], [0]], np.uint8), 0.5, 1.0, trunc_values=tv)
+    assert a4[1, 0] == 1.0
+    a6, _ = oracle.gae(r, v, np.array([[0], [6], [0]], np.uint8), 0.5, 1.0, trunc_values=tv)
+    assert a6[:, 0].tolist() == [3.25, 4.5, 2.5]
 
 
 def test_truncation_equals_split_column_with_bootstrap():
