@@ -44,15 +44,16 @@ def lib():
                                     d, d]
         _lib.oracle_moments.argtypes = [d, i64, d, d]
         _lib.oracle_adv_norm.argtypes = [d, i64, C.c_double, C.c_int, d, d, d]
-        _lib.oracle_param_count.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip]
-        _lib.oracle_param_count.restype = i64
-        _lib.oracle_forward.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, d]
-        _lib.oracle_loss_and_grad.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, i32,
-                                              d, d, d, C.c_double, C.c_double, C.c_double,
-                                              C.c_double, d, d, d, d, C.c_double]
+        for sfx in ("", "_ac"):
+            getattr(_lib, "oracle_param_count" + sfx).argtypes = [C.c_int, C.c_int, ip, C.c_int, ip]
+            getattr(_lib, "oracle_param_count" + sfx).restype = i64
+            getattr(_lib, "oracle_forward" + sfx).argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, d]
+            getattr(_lib, "oracle_loss_and_grad" + sfx).argtypes = [
+                C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, i32, d, d, d, C.c_double, C.c_double,
+                C.c_double, C.c_double, d, d, d, d, C.c_double]
         _lib.oracle_loss_and_grad_mt.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, d, i64, d, i32,
                                                  d, d, d, C.c_double, C.c_double, C.c_double,
-                                                 C.c_double, d, d, d, C.c_double, C.c_int]
+                                                 C.c_double, d, d, d, C.c_double, C.c_int, C.c_int]
         _lib.oracle_clip_grad_norm.argtypes = [i64, d, C.c_double]
         _lib.oracle_clip_grad_norm.restype = C.c_double
         u64 = C.POINTER(C.c_uint64)
@@ -111,25 +112,33 @@ def adv_norm(a, eps=1e-8, unbiased=False):
 
 
 # ------------------------------------------------------------------ C-3 / C-4
-def param_count(obs_dim, hidden, heads):
-    return lib().oracle_param_count(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads))
+def _sfx(separate):
+    return "_ac" if separate else ""
 
 
-def forward(obs_dim, hidden, heads, params, obs):
+def param_count(obs_dim, hidden, heads, separate=False):
+    """separate: the NEXT-3 separate actor / critic trunks (oracle_*_ac, reading R-AC)."""
+    return getattr(lib(), "oracle_param_count" + _sfx(separate))(
+        obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads))
+
+
+def forward(obs_dim, hidden, heads, params, obs, separate=False):
     p = np.ascontiguousarray(params, dtype=np.float64)
     x = np.ascontiguousarray(obs, dtype=np.float64)[:, :obs_dim].copy()
     n = x.shape[0]
     out = np.empty((n, sum(heads) + 1), np.float64)
-    lib().oracle_forward(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads),
-                         _p(p, C.c_double), n, _p(x, C.c_double), _p(out, C.c_double))
+    getattr(lib(), "oracle_forward" + _sfx(separate))(
+        obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads), _p(p, C.c_double), n,
+        _p(x, C.c_double), _p(out, C.c_double))
     return out
 
 
 def loss_and_grad(obs_dim, hidden, heads, params, obs, actions, logp_old, adv_hat, ret,
                   clip_eps=0.2, value_coef=0.5, entropy_coef=0.01, grad_scale=None,
                   grad=None, sums=None, want_per_sample=False, v_old=None, value_clip=0.0,
-                  threads=1):
-    """threads > 1: the all-core timing driver (oracle_loss_and_grad_mt, block-order sums)."""
+                  threads=1, separate=False):
+    """threads > 1: the all-core timing driver (oracle_loss_and_grad_mt, block-order sums).
+    separate: the separate actor / critic trunks (oracle_loss_and_grad_ac)."""
     p = np.ascontiguousarray(params, dtype=np.float64)
     x = np.ascontiguousarray(np.asarray(obs, dtype=np.float64)[:, :obs_dim])
     n = x.shape[0]
@@ -153,9 +162,9 @@ def loss_and_grad(obs_dim, hidden, heads, params, obs, actions, logp_old, adv_ha
                                       clip_eps, value_coef, entropy_coef, grad_scale,
                                       _p(grad, C.c_double), _p(sums, C.c_double),
                                       _p(vo, C.c_double) if vo is not None else None,
-                                      float(value_clip), int(threads))
+                                      float(value_clip), int(threads), int(bool(separate)))
         return grad, sums, None
-    lib().oracle_loss_and_grad(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads),
+    getattr(lib(), "oracle_loss_and_grad" + _sfx(separate))(obs_dim, len(hidden), _ints(hidden), len(heads), _ints(heads),
                                _p(p, C.c_double), n, _p(x, C.c_double), _p(act, C.c_int32),
                                _p(lo, C.c_double), _p(ah, C.c_double), _p(rt, C.c_double),
                                clip_eps, value_coef, entropy_coef, grad_scale,
@@ -206,7 +215,7 @@ def adam(p, m, v, g, t, lr=3e-4, b1=0.9, b2=0.999, eps=1e-8):
 # ------------------------------------------------------------------ one trainer step
 def log_pi(cfg, params, obs, actions):
     """log pi_theta(a|s) summed over heads, by the oracle forward (test-fixture helper)."""
-    z = forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, obs)
+    z = forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, obs, separate=sep(cfg))
     out = np.zeros(z.shape[0])
     s = 0
     for h, a in enumerate(cfg.heads):
@@ -216,6 +225,10 @@ def log_pi(cfg, params, obs, actions):
         out += lsm[np.arange(z.shape[0]), actions[:, h]]
         s += a
     return out
+
+
+def sep(cfg):
+    return bool(getattr(cfg, "separate_critic", False))
 
 
 def minibatch_bounds(n, M):
@@ -278,7 +291,7 @@ def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, 
                               cfg.clip_eps, cfg.value_coef, cfg.entropy_coef,
                               grad_scale=1.0 / Nmb, grad=grad, sums=sums,
                               v_old=vo[rows] if value_clip > 0 else None,
-                              value_clip=value_clip, threads=threads)
+                              value_clip=value_clip, threads=threads, separate=sep(cfg))
             norm = clip_grad_norm(grad, max_grad_norm) if max_grad_norm > 0 else float(
                 np.sqrt(np.sum(grad * grad)))
             out["grads"].append(grad)

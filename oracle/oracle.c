@@ -115,6 +115,73 @@ void oracle_forward(int obs_dim, int L, const int* hidden, int H, const int* hea
 }
 
 /* ---------------------------------------------------------------- C-4 loss and gradient */
+/* one sample's PPO loss terms from its head outputs z[A+1] (logits..., V), and the gradient
+ * of loss_i w.r.t. z, times grad_scale, into delta[A+1].  lsm, p: [A+1] scratch; Hh: [H]. */
+static void sample_loss(int H, const int* heads, int A, const double* z, const int32_t* act,
+                        double logp_old, double Ah, double R, const double* v_old_i,
+                        double value_clip, double clip_eps, double value_coef,
+                        double entropy_coef, double grad_scale, double* lsm, double* p,
+                        double* Hh, double* delta, double* sums, double* loss_out) {
+  /* per-head log-softmax (max-subtracted), probabilities, log-prob, entropy */
+  double logpi = 0.0, ent = 0.0;
+  int s = 0;
+  for (int h = 0; h < H; ++h) {
+    double mx = z[s];
+    for (int j = 1; j < heads[h]; ++j) mx = z[s + j] > mx ? z[s + j] : mx;
+    double se = 0.0;
+    for (int j = 0; j < heads[h]; ++j) se += exp(z[s + j] - mx);
+    double lse = mx + log(se);
+    double hh = 0.0;
+    for (int j = 0; j < heads[h]; ++j) {
+      lsm[s + j] = z[s + j] - lse;
+      p[s + j] = exp(lsm[s + j]);
+      hh -= p[s + j] * lsm[s + j];
+    }
+    Hh[h] = hh;
+    ent += hh;
+    logpi += lsm[s + act[h]];
+    s += heads[h];
+  }
+  const double rho = exp(logpi - logp_old);
+  const double rho_c = rho < 1.0 - clip_eps ? 1.0 - clip_eps
+                     : (rho > 1.0 + clip_eps ? 1.0 + clip_eps : rho);
+  const double s1 = rho * Ah, s2 = rho_c * Ah;
+  const double l_pg = -(s1 < s2 ? s1 : s2);
+  const double V = z[A];
+  double l_v = (V - R) * (V - R);
+  double dV = 2.0 * (V - R);                                    /* d l_v / dV */
+  if (value_clip > 0.0 && v_old_i) {                            /* NEXT-3 value clipping */
+    const double dlt = V - *v_old_i;
+    const double Vc = *v_old_i + (dlt < -value_clip ? -value_clip : (dlt > value_clip ? value_clip : dlt));
+    const double l_c = (Vc - R) * (Vc - R);
+    if (l_c > l_v) {
+      l_v = l_c;
+      dV = (fabs(dlt) <= value_clip) ? 2.0 * (Vc - R) : 0.0;
+    }
+  }
+  *loss_out = l_pg + value_coef * l_v - entropy_coef * ent;
+  sums[0] += l_pg;
+  sums[1] += l_v;
+  sums[2] += ent;
+  sums[3] += fabs(rho - 1.0) > clip_eps ? 1.0 : 0.0;
+  sums[4] += logp_old - logpi;
+
+  /* per-sample logit gradient (closed form, see header), times grad_scale = 1/N */
+  const double mask = (Ah >= 0.0) ? (rho <= 1.0 + clip_eps ? 1.0 : 0.0)
+                                  : (rho >= 1.0 - clip_eps ? 1.0 : 0.0);
+  s = 0;
+  for (int h = 0; h < H; ++h) {
+    for (int j = 0; j < heads[h]; ++j) {
+      double onehot = (j == act[h]) ? 1.0 : 0.0;
+      double g = -mask * Ah * rho * (onehot - p[s + j])
+                 + entropy_coef * p[s + j] * (lsm[s + j] + Hh[h]);
+      delta[s + j] = grad_scale * g;
+    }
+    s += heads[h];
+  }
+  delta[A] = grad_scale * value_coef * dV;
+}
+
 void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const int* heads,
                           const double* params, int64_t n, const double* obs,
                           const int32_t* actions, const double* logp_old,
@@ -141,67 +208,11 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
 
   for (int64_t i = 0; i < n; ++i) {
     forward_one(L, d, params, obs + i * obs_dim, ys, maxw, z);
-
-    /* per-head log-softmax (max-subtracted), probabilities, log-prob, entropy */
-    double logpi = 0.0, ent = 0.0;
-    int s = 0;
-    for (int h = 0; h < H; ++h) {
-      double mx = z[s];
-      for (int j = 1; j < heads[h]; ++j) mx = z[s + j] > mx ? z[s + j] : mx;
-      double se = 0.0;
-      for (int j = 0; j < heads[h]; ++j) se += exp(z[s + j] - mx);
-      double lse = mx + log(se);
-      double hh = 0.0;
-      for (int j = 0; j < heads[h]; ++j) {
-        lsm[s + j] = z[s + j] - lse;
-        p[s + j] = exp(lsm[s + j]);
-        hh -= p[s + j] * lsm[s + j];
-      }
-      Hh[h] = hh;
-      ent += hh;
-      logpi += lsm[s + actions[i * H + h]];
-      s += heads[h];
-    }
-    const double Ah = adv_hat[i];
-    const double rho = exp(logpi - logp_old[i]);
-    const double rho_c = rho < 1.0 - clip_eps ? 1.0 - clip_eps
-                       : (rho > 1.0 + clip_eps ? 1.0 + clip_eps : rho);
-    const double s1 = rho * Ah, s2 = rho_c * Ah;
-    const double l_pg = -(s1 < s2 ? s1 : s2);
-    const double V = z[A];
-    double l_v = (V - ret[i]) * (V - ret[i]);
-    double dV = 2.0 * (V - ret[i]);                               /* d l_v / dV */
-    if (value_clip > 0.0 && v_old) {                              /* NEXT-3 value clipping */
-      const double dlt = V - v_old[i];
-      const double Vc = v_old[i] + (dlt < -value_clip ? -value_clip : (dlt > value_clip ? value_clip : dlt));
-      const double l_c = (Vc - ret[i]) * (Vc - ret[i]);
-      if (l_c > l_v) {
-        l_v = l_c;
-        dV = (fabs(dlt) <= value_clip) ? 2.0 * (Vc - ret[i]) : 0.0;
-      }
-    }
-    const double loss_i = l_pg + value_coef * l_v - entropy_coef * ent;
+    double loss_i;
+    sample_loss(H, heads, A, z, actions + i * H, logp_old[i], adv_hat[i], ret[i],
+                (value_clip > 0.0 && v_old) ? v_old + i : NULL, value_clip, clip_eps,
+                value_coef, entropy_coef, grad_scale, lsm, p, Hh, delta, sums, &loss_i);
     if (per_sample) per_sample[i] = loss_i;
-    sums[0] += l_pg;
-    sums[1] += l_v;
-    sums[2] += ent;
-    sums[3] += fabs(rho - 1.0) > clip_eps ? 1.0 : 0.0;
-    sums[4] += logp_old[i] - logpi;
-
-    /* per-sample logit gradient (closed form, see header), times grad_scale = 1/N */
-    const double mask = (Ah >= 0.0) ? (rho <= 1.0 + clip_eps ? 1.0 : 0.0)
-                                    : (rho >= 1.0 - clip_eps ? 1.0 : 0.0);
-    s = 0;
-    for (int h = 0; h < H; ++h) {
-      for (int j = 0; j < heads[h]; ++j) {
-        double onehot = (j == actions[i * H + h]) ? 1.0 : 0.0;
-        double g = -mask * Ah * rho * (onehot - p[s + j])
-                   + entropy_coef * p[s + j] * (lsm[s + j] + Hh[h]);
-        delta[s + j] = grad_scale * g;
-      }
-      s += heads[h];
-    }
-    delta[A] = grad_scale * value_coef * dV;
 
     /* backprop through the layers, l = L (head) down to 0 */
     for (int l = L; l >= 0; --l) {
@@ -223,6 +234,153 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
     }
   }
   free(ys); free(z); free(lsm); free(p); free(Hh); free(delta); free(dy);
+}
+
+/* ---------------------------------------------------------------- NEXT-3 separate trunks */
+/* Layout (DESIGN.md §3.5 reading R-AC): actor trunk (L tanh layers W_l[out][in], b_l), actor
+ * head W_pi[A][h_L], b_pi[A], then critic trunk (same widths), critic head w_v[1][h_L], b_v. */
+static int64_t trunk_count(int L, const int* d) {       /* d[0..L]: obs, hidden widths */
+  int64_t P = 0;
+  for (int l = 0; l < L; ++l) P += (int64_t)d[l + 1] * d[l] + d[l + 1];
+  return P;
+}
+
+int64_t oracle_param_count_ac(int obs_dim, int L, const int* hidden, int H, const int* heads) {
+  int d[64];
+  layer_dims(obs_dim, L, hidden, H, heads, d);
+  const int A = d[L + 1] - 1;
+  return 2 * trunk_count(L, d) + (int64_t)A * d[L] + A + d[L] + 1;
+}
+
+/* one trunk: ys row l (l = 0..L) = y_l, y_0 = x;  y_l = tanh(W_l y_{l-1} + b_l) */
+static void trunk_fwd(int L, const int* d, const double* p, const double* x, double* ys, int maxw) {
+  memcpy(ys, x, sizeof(double) * d[0]);
+  int64_t off = 0;
+  for (int l = 0; l < L; ++l) {
+    const double* W = p + off;
+    const double* b = W + (int64_t)d[l + 1] * d[l];
+    const double* in = ys + (int64_t)l * maxw;
+    double* out = ys + (int64_t)(l + 1) * maxw;
+    for (int o = 0; o < d[l + 1]; ++o) {
+      double acc = b[o];
+      for (int i = 0; i < d[l]; ++i) acc += W[(int64_t)o * d[l] + i] * in[i];
+      out[o] = tanh(acc);
+    }
+    off += (int64_t)d[l + 1] * d[l] + d[l + 1];
+  }
+}
+
+/* a linear head on y: out[r] = b[r] + sum_k W[r][k] y[k], r < rows */
+static void head_fwd(int rows, int in, const double* W, const double* y, double* out) {
+  const double* b = W + (int64_t)rows * in;
+  for (int r = 0; r < rows; ++r) {
+    double acc = b[r];
+    for (int k = 0; k < in; ++k) acc += W[(int64_t)r * in + k] * y[k];
+    out[r] = acc;
+  }
+}
+
+/* backprop of a head + trunk: dlt[rows] = dloss/d(head out) (scaled); adds the head's and the
+ * trunk's gradients.  delta, dy: [maxw] scratch. */
+static void head_trunk_bwd(int L, const int* d, int rows, const double* p_trunk,
+                           const double* W_head, const double* ys, int maxw, const double* dlt,
+                           double* g_trunk, double* g_head, double* delta, double* dy) {
+  const int in = d[L];
+  const double* yL = ys + (int64_t)L * maxw;
+  for (int r = 0; r < rows; ++r) {
+    for (int k = 0; k < in; ++k) g_head[(int64_t)r * in + k] += dlt[r] * yL[k];
+    g_head[(int64_t)rows * in + r] += dlt[r];
+  }
+  for (int k = 0; k < in; ++k) {
+    double acc = 0.0;
+    for (int r = 0; r < rows; ++r) acc += dlt[r] * W_head[(int64_t)r * in + k];
+    delta[k] = acc * (1.0 - yL[k] * yL[k]);                      /* tanh' of layer L */
+  }
+  int64_t offs[64];
+  offs[0] = 0;
+  for (int l = 0; l < L; ++l) offs[l + 1] = offs[l] + (int64_t)d[l + 1] * d[l] + d[l + 1];
+  for (int l = L - 1; l >= 0; --l) {                             /* trunk layer l: d[l] -> d[l+1] */
+    const double* W = p_trunk + offs[l];
+    double* gW = g_trunk + offs[l];
+    double* gb = gW + (int64_t)d[l + 1] * d[l];
+    const double* inl = ys + (int64_t)l * maxw;
+    for (int o = 0; o < d[l + 1]; ++o) {
+      for (int k = 0; k < d[l]; ++k) gW[(int64_t)o * d[l] + k] += delta[o] * inl[k];
+      gb[o] += delta[o];
+    }
+    if (l == 0) break;
+    for (int k = 0; k < d[l]; ++k) {
+      double acc = 0.0;
+      for (int o = 0; o < d[l + 1]; ++o) acc += delta[o] * W[(int64_t)o * d[l] + k];
+      dy[k] = acc;
+    }
+    for (int k = 0; k < d[l]; ++k) delta[k] = dy[k] * (1.0 - inl[k] * inl[k]);
+  }
+}
+
+void oracle_forward_ac(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                       const double* params, int64_t n, const double* obs, double* out) {
+  int d[64];
+  layer_dims(obs_dim, L, hidden, H, heads, d);
+  const int A = d[L + 1] - 1;
+  int maxw = 0;
+  for (int l = 0; l <= L; ++l) maxw = d[l] > maxw ? d[l] : maxw;
+  const int64_t T = trunk_count(L, d);
+  const double* pa = params;                                  /* actor trunk */
+  const double* wpi = pa + T;                                 /* actor head [A][h_L] + [A] */
+  const double* pc = wpi + (int64_t)A * d[L] + A;             /* critic trunk */
+  const double* wv = pc + T;                                  /* critic head [1][h_L] + [1] */
+  double* ya = (double*)malloc(sizeof(double) * (size_t)(L + 1) * maxw);
+  double* yc = (double*)malloc(sizeof(double) * (size_t)(L + 1) * maxw);
+  for (int64_t i = 0; i < n; ++i) {
+    trunk_fwd(L, d, pa, obs + i * obs_dim, ya, maxw);
+    trunk_fwd(L, d, pc, obs + i * obs_dim, yc, maxw);
+    head_fwd(A, d[L], wpi, ya + (int64_t)L * maxw, out + i * (A + 1));
+    head_fwd(1, d[L], wv, yc + (int64_t)L * maxw, out + i * (A + 1) + A);
+  }
+  free(ya);
+  free(yc);
+}
+
+void oracle_loss_and_grad_ac(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                             const double* params, int64_t n, const double* obs,
+                             const int32_t* actions, const double* logp_old,
+                             const double* adv_hat, const double* ret,
+                             double clip_eps, double value_coef, double entropy_coef,
+                             double grad_scale, double* grad, double* sums, double* per_sample,
+                             const double* v_old, double value_clip) {
+  int d[64];
+  layer_dims(obs_dim, L, hidden, H, heads, d);
+  const int A = d[L + 1] - 1;
+  int maxw = 0;
+  for (int l = 0; l <= L + 1; ++l) maxw = d[l] > maxw ? d[l] : maxw;
+  const int64_t T = trunk_count(L, d);
+  const int64_t o_pi = T, o_c = T + (int64_t)A * d[L] + A, o_v = o_c + T;
+  double* ya = (double*)malloc(sizeof(double) * (size_t)(L + 1) * maxw);
+  double* yc = (double*)malloc(sizeof(double) * (size_t)(L + 1) * maxw);
+  double* z = (double*)malloc(sizeof(double) * (size_t)(A + 1));
+  double* lsm = (double*)malloc(sizeof(double) * (size_t)(A + 1));
+  double* p = (double*)malloc(sizeof(double) * (size_t)(A + 1));
+  double* Hh = (double*)malloc(sizeof(double) * (size_t)(H > 0 ? H : 1));
+  double* dz = (double*)malloc(sizeof(double) * (size_t)(A + 1));
+  double* delta = (double*)malloc(sizeof(double) * (size_t)maxw);
+  double* dy = (double*)malloc(sizeof(double) * (size_t)maxw);
+  for (int64_t i = 0; i < n; ++i) {
+    trunk_fwd(L, d, params, obs + i * obs_dim, ya, maxw);
+    trunk_fwd(L, d, params + o_c, obs + i * obs_dim, yc, maxw);
+    head_fwd(A, d[L], params + o_pi, ya + (int64_t)L * maxw, z);
+    head_fwd(1, d[L], params + o_v, yc + (int64_t)L * maxw, z + A);
+    double loss_i;
+    sample_loss(H, heads, A, z, actions + i * H, logp_old[i], adv_hat[i], ret[i],
+                (value_clip > 0.0 && v_old) ? v_old + i : NULL, value_clip, clip_eps,
+                value_coef, entropy_coef, grad_scale, lsm, p, Hh, dz, sums, &loss_i);
+    if (per_sample) per_sample[i] = loss_i;
+    /* logits -> actor head + trunk; V -> critic head + trunk */
+    head_trunk_bwd(L, d, A, params, params + o_pi, ya, maxw, dz, grad, grad + o_pi, delta, dy);
+    head_trunk_bwd(L, d, 1, params + o_c, params + o_v, yc, maxw, dz + A, grad + o_c, grad + o_v,
+                   delta, dy);
+  }
+  free(ya); free(yc); free(z); free(lsm); free(p); free(Hh); free(dz); free(delta); free(dy);
 }
 
 /* ---------------------------------------------------------------- NEXT-2 rollout */
@@ -321,9 +479,10 @@ void oracle_loss_and_grad_mt(int obs_dim, int L, const int* hidden, int H, const
                              const double* adv_hat, const double* ret,
                              double clip_eps, double value_coef, double entropy_coef,
                              double grad_scale, double* grad, double* sums,
-                             const double* v_old, double value_clip, int threads) {
+                             const double* v_old, double value_clip, int threads, int ac) {
   if (threads < 1) threads = 1;
-  const int64_t P = oracle_param_count(obs_dim, L, hidden, H, heads);
+  const int64_t P = ac ? oracle_param_count_ac(obs_dim, L, hidden, H, heads)
+                       : oracle_param_count(obs_dim, L, hidden, H, heads);
   double* g = (double*)calloc((size_t)threads * (size_t)P, sizeof(double));
   double* s = (double*)calloc((size_t)threads * 5, sizeof(double));
   #pragma omp parallel for num_threads(threads) schedule(static, 1)
@@ -332,10 +491,10 @@ void oracle_loss_and_grad_mt(int obs_dim, int L, const int* hidden, int H, const
     const int H_ = H;
     const int od = obs_dim;
     if (hi > lo)
-      oracle_loss_and_grad(obs_dim, L, hidden, H, heads, params, hi - lo, obs + lo * od,
-                           actions + lo * H_, logp_old + lo, adv_hat + lo, ret + lo, clip_eps,
-                           value_coef, entropy_coef, grad_scale, g + (int64_t)k * P, s + 5 * k,
-                           NULL, v_old ? v_old + lo : NULL, value_clip);
+      (ac ? oracle_loss_and_grad_ac : oracle_loss_and_grad)(
+          obs_dim, L, hidden, H, heads, params, hi - lo, obs + lo * od, actions + lo * H_,
+          logp_old + lo, adv_hat + lo, ret + lo, clip_eps, value_coef, entropy_coef, grad_scale,
+          g + (int64_t)k * P, s + 5 * k, NULL, v_old ? v_old + lo : NULL, value_clip);
   }
   for (int k = 0; k < threads; ++k) {            /* block order */
     for (int64_t i = 0; i < P; ++i) grad[i] += g[(int64_t)k * P + i];

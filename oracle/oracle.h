@@ -75,6 +75,24 @@ void oracle_loss_and_grad(int obs_dim, int L, const int* hidden, int H, const in
                           double grad_scale, double* grad, double* sums, double* per_sample,
                           const double* v_old, double value_clip);
 
+/* NEXT-3 separate actor and critic trunks (
+ * DESIGN.md §3.5 reading R-AC): the same obs feeds an actor trunk (L tanh layers, widths
+ * hidden) with a linear policy head (A logits) and a critic trunk (same widths) with a linear
+ * value head (1 output).  Flat layout: actor trunk W_l[out][in], b_l for l = 1..L; W_pi[A][h_L],
+ * b_pi[A]; critic trunk likewise; w_v[1][h_L], b_v[1].  out / loss / gradient exactly as the
+ * shared-trunk functions (logits..., V), the policy and entropy terms reaching the actor only
+ * and the value term the critic only. */
+int64_t oracle_param_count_ac(int obs_dim, int L, const int* hidden, int H, const int* heads);
+void oracle_forward_ac(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                       const double* params, int64_t n, const double* obs, double* out);
+void oracle_loss_and_grad_ac(int obs_dim, int L, const int* hidden, int H, const int* heads,
+                             const double* params, int64_t n, const double* obs,
+                             const int32_t* actions, const double* logp_old,
+                             const double* adv_hat, const double* ret,
+                             double clip_eps, double value_coef, double entropy_coef,
+                             double grad_scale, double* grad, double* sums, double* per_sample,
+                             const double* v_old, double value_clip);
+
 /* NEXT-3 global gradient-norm clipping (PyTorch clip_grad_norm_ semantics, C-A5 extension):
  *   norm = sqrt(sum g_i^2);  if max_norm / (norm + 1e-6) < 1: g *= max_norm / (norm + 1e-6).
  * Returns the pre-clip norm.  max_norm <= 0: no-op (norm still returned). */
@@ -107,14 +125,15 @@ void oracle_adam(int64_t P, double* p, double* m, double* v, const double* g, in
  * samples into `threads` contiguous blocks, runs oracle_loss_and_grad on each block in its
  * own OpenMP thread into its own zeroed grad / sums buffers, then adds the buffers in block
  * order (fixed, deterministic).  The per-sample arithmetic is exactly oracle_loss_and_grad's;
- * only the order of the final sums differs (pinned against the 1-thread call to 1e-12). */
+ * only the order of the final sums differs (pinned against the 1-thread call to 1e-12).
+ * ac != 0: the separate-trunk network (oracle_loss_and_grad_ac). */
 void oracle_loss_and_grad_mt(int obs_dim, int L, const int* hidden, int H, const int* heads,
                              const double* params, int64_t n, const double* obs,
                              const int32_t* actions, const double* logp_old,
                              const double* adv_hat, const double* ret,
                              double clip_eps, double value_coef, double entropy_coef,
                              double grad_scale, double* grad, double* sums,
-                             const double* v_old, double value_clip, int threads);
+                             const double* v_old, double value_clip, int threads, int ac);
 
 #ifdef __cplusplus
 }

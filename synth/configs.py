@@ -29,6 +29,7 @@ class Config:
     beta2: float = 0.999
     adam_eps: float = 1e-8
     recipe: str = "tiny"       # reward / done process, SURVEY.md §8(d) D-1
+    separate_critic: bool = False   # NEXT-3: separate actor and critic trunks (reading R-AC)
     notes: str = field(default="", compare=False)
 
     @property
@@ -48,9 +49,24 @@ class Config:
         return (self.obs_dim,) + tuple(self.hidden) + (self.n_actions + 1,)
 
     @property
-    def n_params(self) -> int:
+    def layer_shapes(self):
+        """(out, in) of every weight matrix in flat-layout order (C-A10; R-AC with
+        separate_critic: actor trunk, policy head [A], critic trunk, value head [1])."""
         d = self.dims
-        return sum(d[i + 1] * d[i] + d[i + 1] for i in range(len(d) - 1))
+        if not self.separate_critic:
+            return [(d[i + 1], d[i]) for i in range(len(d) - 1)]
+        trunk = [(d[i + 1], d[i]) for i in range(len(d) - 2)]
+        return trunk + [(self.n_actions, d[-2])] + trunk + [(1, d[-2])]
+
+    @property
+    def head_layers(self):
+        """indices into layer_shapes of the linear head layers"""
+        L = len(self.hidden)
+        return (L, 2 * L + 1) if self.separate_critic else (L,)
+
+    @property
+    def n_params(self) -> int:
+        return sum(o * i + o for o, i in self.layer_shapes)
 
     def with_(self, **kw) -> "Config":
         from dataclasses import replace

@@ -157,15 +157,13 @@ def make_params(cfg: Config, seed: int = 0, head_gain: float = 1.0) -> np.ndarra
     W, b ~ U(-1/sqrt(fan_in), +1/sqrt(fan_in)) (PyTorch nn.Linear default, C-A11);
     the head layer is multiplied by ``head_gain``.
     """
-    d = cfg.dims
     parts, off = [], 0
-    for l in range(len(d) - 1):
-        fi, fo = d[l], d[l + 1]
+    for l, (fo, fi) in enumerate(cfg.layer_shapes):
         k = 1.0 / np.sqrt(fi)
         cnt = fo * fi + fo
         u = uniform(seed, A_PARAM, np.arange(off, off + cnt, dtype=np.uint64))
         p = (2.0 * u - 1.0) * k
-        if l == len(d) - 2:
+        if l in cfg.head_layers:
             p = p * head_gain
         parts.append(p)
         off += cnt

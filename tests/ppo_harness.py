@@ -73,13 +73,12 @@ def gpu_step(cfg, params, shards, apply=True, ctx=None, n_steps=1):
 
 def tensor_slices(cfg):
     """(name, slice) of every W_l and b_l in the flat layout (C-A10)."""
-    d = cfg.dims
     off, out = 0, []
-    for l in range(len(d) - 1):
-        nw = d[l + 1] * d[l]
+    for l, (o, i) in enumerate(cfg.layer_shapes):
+        nw = o * i
         out.append((f"W{l + 1}", slice(off, off + nw)))
-        out.append((f"b{l + 1}", slice(off + nw, off + nw + d[l + 1])))
-        off += nw + d[l + 1]
+        out.append((f"b{l + 1}", slice(off + nw, off + nw + o)))
+        off += nw + o
     return out
 
 
