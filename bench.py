@@ -255,20 +255,38 @@ def kernel_table(recs, Kp, prof_ms):
     return agg, rows
 
 
-def roofline_of(agg, traffic_src=None, config=None):
+def ncu_traffic(config, step_names, dname):
+    """DRAM bytes per launch of kernel `dname` from the committed ncu launch list of this
+    config (profiles/ncu_traffic.json, tools/ncu_summary.py): its launches are in the same
+    order as one step's profiled records, so the k-th record is the k-th launch."""
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[config]
+        src = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["_source"][config]
+    except Exception:
+        return None, None
+    labels, by = tr.get("launches", []), tr.get("dram_bytes", [])
+    if len(labels) != len(step_names):
+        return None, src
+    for name, lab, b in zip(step_names, labels, by):
+        short = {"fwd_l1": "fwd", "fwd_hidden": "fwd", "dX_hidden": "dX", "dX_head": "dX",
+                 "dW_hidden": "dW", "dW_l1": "dW", "dW_head": "dW"}.get(name, name)
+        if short != lab:
+            return None, src
+        if name == dname:
+            return b, src
+    return None, src
+
+
+def roofline_of(agg, step_names=None, config=None):
     """The dominant kernel (by time; not the exchange) under the roof its algorithmic intensity
     puts it: tensor above the ridge (burst peak / copy bandwidth), else HBM."""
     hbm, tf_burst, _, src = load_peaks()
-    dname, (dt, dcnt, dfl, dby) = max(((k, v) for k, v in agg.items() if k != "allreduce"),
+    dname, (dt, dcnt, dfl, dby) = max(((k, v) for k, v in agg.items() if k not in ("allreduce", "stats")),
                                       key=lambda kv: kv[1][0])
     davg_s = dt / dcnt * 1e-3
-    traffic = None
-    if traffic_src:
-        try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-            traffic = tr.get(config, {}).get(dname)
-        except Exception:
-            traffic = None
+    traffic, tsrc = (None, None)
+    if step_names:
+        traffic, tsrc = ncu_traffic(config, step_names, dname)
     ridge = tf_burst * 1e12 / (hbm * 1e9)
     ai = dfl / dby if dby > 0 else float("inf")
     if dfl > 0 and ai >= ridge:
@@ -282,7 +300,9 @@ def roofline_of(agg, traffic_src=None, config=None):
              "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
              "peak_source": f"{src} hbm_gbs (copy)"}
     r.update(flops_per_launch=dfl / dcnt, bytes_per_launch=dby / dcnt, intensity_flop_per_byte=ai,
-             ridge_flop_per_byte=ridge, ms_per_launch=davg_s * 1e3)
+             ridge_flop_per_byte=ridge, ms_per_launch=davg_s * 1e3,
+             traffic_source=(f"profiles/{tsrc} (ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                             f"of this launch)") if traffic is not None else None)
     return r
 
 
@@ -480,16 +500,15 @@ def main_ours(args, world, rank, local):
 
     import math
     agg, kernels = kernel_table(recs, Kp, prof_ms)
-    roofline = roofline_of(agg, traffic_src=True, config=cfg.name)
-    # our kernels per step (srl_ppo_train_step): gae_kernel (merges the moments itself),
-    # + moments exchange when world > 1, the 3L+2 GEMMs, finalize_w + finalize_b + extras, adam,
-    # stats, + the peer-memory allreduce (NCCL's kernels are not counted)
+    nper = len(recs) // max(Kp, 1)
+    step_names = [r[0] for r in recs[:nper] if not (r[0] == "allreduce" and comm_path == "nccl")]
+    roofline = roofline_of(agg, step_names=step_names, config=cfg.name)
+    # our kernels per step: every launch srl_ppo_train_step makes is one profiled record
+    # (the profiling region runs the same steps); NCCL's allreduce is not ours
+    ours = sum(1 for r in recs if not (r[0] == "allreduce" and comm_path == "nccl"))
+    per_step = ours / Kp
     L = len(cfg.hidden)
-    p2p = comm_path == "nvlink-p2p"
-    per_update = ((L + 1 + (L + 1) + L) + 3 + 1 + 1 + (1 if args.max_grad_norm > 0 else 0)
-                  + (1 if p2p else 0))
     updates = max(1, args.epochs) * max(1, args.minibatches)
-    per_step = 1 + (1 if world > 1 and p2p else 0) + per_update * updates
     cpu = None if args.no_cpu_baseline else cpu_baselines(cfg, args.cpu_seconds)
     clocks = sampler.summary(wall0, wall1) if sampler else None
     out = {
@@ -516,7 +535,7 @@ def main_ours(args, world, rank, local):
                 "d2h_bytes_per_step": P.srl.STATS_BYTES * world, "steps": Ke,
                 "no_prefetch": {"value": N * Ke / (e2e_serial_ms * 1e-3), "unit": UNIT,
                                 "what": "ablation: upload after each step, no overlap (PAPER.md §5.3.4)"}},
-        "gpu_launches": per_step * K,
+        "gpu_launches": int(round(per_step * K)),
         "inference": {"what": "NEXT-2 srl_policy_rollout: forward + sampling epilogue over the "
                               "step's observations (policy-worker batch = the whole batch)",
                       "value": N / (inf_ms * 1e-3), "unit": "samples/s", "ms_per_call": inf_ms,

@@ -123,6 +123,12 @@ typedef struct srl_ppo_config {
   float value_clip;
   float max_grad_norm;
   int epochs, minibatches;
+  /* NEXT-3 separate actor and critic trunks (DESIGN.md §3.5 reading R-AC):
+   *   0: one shared tanh trunk, head [logits..., value] (C-A9).
+   *   1: an actor trunk and a critic trunk of the same widths on the same obs; the policy head
+   *      (A logits) on the actor's last layer, the value head on the critic's.  Flat layout:
+   *      actor trunk (W_l, b_l), W_pi[A][h_L], b_pi[A], critic trunk, w_v[1][h_L], b_v[1]. */
+  int separate_critic;
 } srl_ppo_config;
 
 /* Device-resident statistics written by srl_ppo_step (global means over n_global). */

@@ -237,8 +237,16 @@ def minibatch_bounds(n, M):
     return [(k * n // M, (k + 1) * n // M) for k in range(M)]
 
 
+def default_threads():
+    """Threads of the oracle's block driver in ppo_step (ORACLE_THREADS, default all cores)."""
+    try:
+        return max(1, int(os.environ.get("ORACLE_THREADS", "0")) or len(os.sched_getaffinity(0)))
+    except Exception:
+        return 1
+
+
 def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, t=1,
-             apply=True, value_clip=0.0, max_grad_norm=0.0, epochs=1, minibatches=1, threads=1):
+             apply=True, value_clip=0.0, max_grad_norm=0.0, epochs=1, minibatches=1, threads=None):
     """One trainer step of the oracle over K shards (list of dicts from synth.make_batch
     with a ``logp_old`` entry).  Returns a dict with adv/ret per shard, mean/std, grad,
     loss sums and (if apply) the updated params/m/v.
@@ -253,7 +261,13 @@ def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, 
 
     Optional shard keys (NEXT-3): ``trunc_values`` [T][Bk] (reading R-T, time-limit
     bootstrap in GAE) and ``valid`` [T][Bk] u8 (reading R-P: padding samples, valid = 0,
-    are left out of the normalisation moments, the loss and N)."""
+    are left out of the normalisation moments, the loss and N).
+
+    threads: the per-sample loss/gradient of a shard with >= 1024 rows goes through the
+    block driver (oracle_loss_and_grad_mt: the same per-sample arithmetic, block sums added in
+    block order -- pinned to the 1-thread call); None = default_threads()."""
+    if threads is None:
+        threads = default_threads()
     advs, rets, vms = [], [], []
     for sh in shards:
         a, r = gae(sh["rewards"], sh["values"], sh["dones"], cfg.gamma, cfg.lam,
@@ -291,7 +305,8 @@ def ppo_step(cfg, params, shards, *, eps=1e-8, unbiased=False, adam_state=None, 
                               cfg.clip_eps, cfg.value_coef, cfg.entropy_coef,
                               grad_scale=1.0 / Nmb, grad=grad, sums=sums,
                               v_old=vo[rows] if value_clip > 0 else None,
-                              value_clip=value_clip, threads=threads, separate=sep(cfg))
+                              value_clip=value_clip, threads=threads if rows.size >= 1024 else 1,
+                              separate=sep(cfg))
             norm = clip_grad_norm(grad, max_grad_norm) if max_grad_norm > 0 else float(
                 np.sqrt(np.sum(grad * grad)))
             out["grads"].append(grad)

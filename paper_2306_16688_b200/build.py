@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 SO = os.path.join(HERE, "libsrl.so")
-SOURCES = ["gae.cu", "mlp.cu", "misc.cu", "api.cu"]
+SOURCES = ["gae.cu", "mlp.cu", "misc.cu", "api.cu", "head_fused.cu"]
 HEADERS = ["ptx.cuh", "gemm_tc.cuh", "internal.h"]
 
 

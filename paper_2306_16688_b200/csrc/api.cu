@@ -123,8 +123,10 @@ struct Lay {
   int bn_dw, cg_dw, dw_n_tiles, dw_m_tiles, splits_max;
   float* part;             // dW partials [splits][out or in][ld_part]
   int64_t part_rows, ld_part;
-  float* colsum;           // db partials of this layer: [sms][4][out] (hidden) / [sms][4][64] (head)
+  float* colsum;           // db partials of this layer: [sms][out] (hidden) / [sms][64] (head)
   int colsum_ld;
+  int t = 0, l = 0;        // trunk (0 actor / shared, 1 critic) and layer index
+  float* dz_colsum = nullptr;   // head only: column sums of dZ_L [sms][T*h_L] (db of layer L)
 };
 
 struct srl_ctx {
@@ -132,6 +134,15 @@ struct srl_ctx {
   srl_ppo_config cfg{};
   std::vector<int> hidden, heads, dims;
   int L = 0, A = 0;
+  // NEXT-3 separate trunks (DESIGN.md §3.5 R-AC): T = 2 trunks side by side in every activation
+  // buffer (trunk t owns columns [t*h, (t+1)*h)); lay[t*L + l] = hidden layer l of trunk t,
+  // lay[T*L] = the head over both trunks' last layer (block-structured fp16 weights)
+  int T = 1;
+  int64_t pi_w = 0, pi_b = 0, v_w = 0, v_b = 0;   // R-AC flat offsets of the two heads
+  float* hbias = nullptr;                          // R-AC: contiguous fp32 head bias mirror [64]
+  Lay& hid(int t, int l) { return lay[t * L + l]; }
+  Lay& head() { return lay[T * L]; }
+  int hidx(int t, int l) const { return t * L + l; }
   int64_t P = 0, max_n = 0;
   uint64_t digest = 0;
   std::vector<Lay> lay;
@@ -193,6 +204,7 @@ struct srl_ctx {
   CommCtl cc{};
   int* err_pinned = nullptr;                   // host view of cc.err_host
   bool failed = false;                         // a peer wait timed out or NCCL failed: no more steps
+  unsigned* gbar = nullptr;                    // grid-barrier words of update_kernel
 };
 
 static unsigned long long comm_timeout_ns() {
@@ -257,6 +269,12 @@ struct ProfScope {
   }
 };
 
+// SRL_HEAD_FUSED=0: the head block as three kernels (head GEMM + loss, dX, split-K dW)
+static bool head_fused_enabled() {
+  const char* e = getenv("SRL_HEAD_FUSED");
+  return !(e && e[0] == '0');
+}
+
 static bool dw512_enabled() {   // opt-in: measured ~5% slower dW + finalize on the Atari shape
   const char* e = getenv("SRL_DW512");
   return e && e[0] == '1';
@@ -317,34 +335,61 @@ extern "C" srl_status srl_nccl_unique_id(uint8_t out[128]) {
   return SRL_OK;
 }
 
+// the flat parameter vector as segments with their gradient sources (split-K / per-CTA
+// partials and column sums, indexed like c->lay) and fp16 shadows
 static SegTable make_segs(srl_ctx* c, const std::vector<int>& splits,
-                          const std::vector<int>& colsum_parts) {
+                          const std::vector<int>& colsum_parts, int dz_parts) {
   SegTable t{};
   t.n = 0;
-  for (int l = 0; l <= c->L; ++l) {
-    const Lay& y = c->lay[l];
+  const int L = c->L, T = c->T;
+  const Lay& hd = c->head();
+  const int hL = c->dims[L];
+  const int hi = T * L;                                   // head index in c->lay
+  auto nsp = [&](int i) { return splits.empty() ? 0 : splits[i]; };
+  auto ncs = [&](int i) { return colsum_parts.empty() ? 0 : colsum_parts[i]; };
+  for (int tr = 0; tr < T; ++tr)
+    for (int l = 0; l < L; ++l) {
+      const Lay& y = c->hid(tr, l);
+      const int i = c->hidx(tr, l);
+      Segment w{};
+      w.off = y.w_off; w.rows = y.out; w.cols = y.in; w.is_bias = 0;
+      w.part = y.part; w.splits = nsp(i); w.ld_part = y.ld_part;
+      w.split_stride = y.part_rows * y.ld_part; w.transposed = 0;
+      w.w16 = y.w16; w.w16_ld = y.w16_ld;
+      t.s[t.n++] = w;
+      Segment b{};
+      b.off = y.b_off; b.rows = 1; b.cols = y.out; b.is_bias = 1;
+      if (l + 1 < L) {           // db_l from the dX epilogue of layer l+1 of this trunk
+        b.colsum = y.colsum; b.nparts = ncs(i); b.colsum_ld = y.colsum_ld;
+      } else {                   // db_L from the head's dX (this trunk's columns of dZ_L)
+        b.colsum = hd.dz_colsum + tr * hL; b.nparts = dz_parts; b.colsum_ld = T * hL;
+      }
+      t.s[t.n++] = b;
+    }
+  // head: the dW^T partial [T*hL][64] (transposed) and the per-CTA column sums of g [64]
+  auto head_w = [&](int64_t off, int rows, int row0, int col0) {
     Segment w{};
-    w.off = y.w_off;
-    w.rows = y.out;
-    w.cols = y.in;
-    w.is_bias = 0;
-    w.part = y.part;
-    w.splits = splits.empty() ? 0 : splits[l];
-    w.ld_part = y.ld_part;
-    w.split_stride = y.part_rows * y.ld_part;
-    w.transposed = (l == c->L);
-    w.w16 = y.w16;
-    w.w16_ld = y.w16_ld;
+    w.off = off; w.rows = rows; w.cols = hL; w.is_bias = 0;
+    w.part = hd.part + (int64_t)row0 * hd.ld_part + col0; w.splits = nsp(hi);
+    w.ld_part = hd.ld_part; w.split_stride = hd.part_rows * hd.ld_part; w.transposed = 1;
+    w.w16 = hd.w16 + (int64_t)col0 * hd.w16_ld + row0; w.w16_ld = hd.w16_ld;
     t.s[t.n++] = w;
+  };
+  auto head_b = [&](int64_t off, int cols, int col0) {
     Segment b{};
-    b.off = y.b_off;
-    b.rows = 1;
-    b.cols = y.out;
-    b.is_bias = 1;
-    b.colsum = y.colsum;
-    b.nparts = colsum_parts.empty() ? 0 : colsum_parts[l];
-    b.colsum_ld = y.colsum_ld;
+    b.off = off; b.rows = 1; b.cols = cols; b.is_bias = 1;
+    b.colsum = hd.colsum + col0; b.nparts = ncs(hi); b.colsum_ld = hd.colsum_ld;
+    b.b32 = T > 1 ? c->hbias + col0 : nullptr;
     t.s[t.n++] = b;
+  };
+  if (T == 1) {
+    head_w(hd.w_off, hd.out, 0, 0);
+    head_b(hd.b_off, hd.out, 0);
+  } else {                       // policy head on the actor's columns, value on the critic's
+    head_w(c->pi_w, c->A, 0, 0);
+    head_b(c->pi_b, c->A, 0);
+    head_w(c->v_w, 1, hL, c->A);
+    head_b(c->v_b, 1, c->A);
   }
   return t;
 }
@@ -401,22 +446,46 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   c->dims.push_back(A + 1);
   std::vector<int> dig(c->dims);
   dig.insert(dig.end(), c->heads.begin(), c->heads.end());
+  if (cfg->separate_critic) dig.push_back(-2);     // R-AC: a different flat layout
   c->digest = fnv1a(dig);
 
   auto bail = [&](srl_status st) { free_ctx(c); return st; };
+  c->T = cfg->separate_critic ? 2 : 1;
+  const int T = c->T, L = c->L, hL = c->dims[L];
   int64_t off = 0;
   int max_h = 0;
-  c->lay.resize(c->L + 1);
-  for (int l = 0; l <= c->L; ++l) {
-    Lay& y = c->lay[l];
-    y.in = c->dims[l];
-    y.out = c->dims[l + 1];
-    y.w_off = off;
-    y.b_off = off + (int64_t)y.out * y.in;
-    off = y.b_off + y.out;
-    y.w16_ld = (l == 0) ? (y.in + 7) / 8 * 8 : y.in;
-    y.w16_rows = (l == c->L) ? kHeadCols : y.out;
-    if (l < c->L) max_h = std::max(max_h, y.out);
+  c->lay.resize(T * L + 1);
+  for (int tr = 0; tr < T; ++tr) {
+    for (int l = 0; l < L; ++l) {
+      Lay& y = c->hid(tr, l);
+      y.t = tr; y.l = l;
+      y.in = c->dims[l];
+      y.out = c->dims[l + 1];
+      y.w_off = off;
+      y.b_off = off + (int64_t)y.out * y.in;
+      off = y.b_off + y.out;
+      y.w16_ld = (l == 0) ? (y.in + 7) / 8 * 8 : y.in;
+      y.w16_rows = y.out;
+      max_h = std::max(max_h, T * y.out);
+    }
+    if (T == 1) {
+      Lay& y = c->head();
+      y.w_off = off;
+      y.b_off = off + (int64_t)(A + 1) * hL;
+      off = y.b_off + A + 1;
+    } else if (tr == 0) {        // R-AC: W_pi [A][h_L], b_pi [A] after the actor trunk
+      c->pi_w = off; c->pi_b = off + (int64_t)A * hL; off = c->pi_b + A;
+    } else {                     // w_v [1][h_L], b_v [1] after the critic trunk
+      c->v_w = off; c->v_b = off + hL; off = c->v_b + 1;
+    }
+  }
+  {
+    Lay& y = c->head();
+    y.t = 0; y.l = L;
+    y.in = T * hL;               // the head reads both trunks' last layer
+    y.out = A + 1;
+    y.w16_ld = y.in;
+    y.w16_rows = kHeadCols;
   }
   c->P = off;
   srl_status st;
@@ -428,38 +497,43 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if ((st = dalloc(c, &c->counters, sizeof(unsigned long long) * 4))) return bail(st);
   if ((st = dalloc(c, &c->stats_part, sizeof(double) * 8 * c->sms))) return bail(st);
   if ((st = dalloc(c, &c->norm_scratch, sizeof(double) * (3 * kMomentBlocks + 3 * world + 8)))) return bail(st);
+  if ((st = dalloc(c, &c->hbias, sizeof(float) * kHeadCols))) return bail(st);
   const int64_t n = c->max_n;
-  for (int l = 0; l <= c->L; ++l) {
-    Lay& y = c->lay[l];
+  for (size_t li = 0; li < c->lay.size(); ++li) {
+    Lay& y = c->lay[li];
+    const bool is_head = li + 1 == c->lay.size();
     if ((st = dalloc(c, &y.w16, sizeof(__half) * (size_t)y.w16_rows * y.w16_ld))) return bail(st);
     // epilogue-heavy GEMMs (fwd tanh, dX dtanh) use 128-wide tiles: 4 TMEM accumulators
     // 256-wide outputs run on CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles): half the
     // shared-memory operand traffic per FLOP of a 1-SM 128 x 128 tile
-    if (l == c->L) { y.bn_fwd = kHeadCols; y.cg_fwd = 1; }
+    if (is_head) { y.bn_fwd = kHeadCols; y.cg_fwd = 1; }
     else if (y.out % 256 == 0) { y.bn_fwd = 256; y.cg_fwd = 2; }
     else { y.bn_fwd = (y.out % 128 == 0) ? 128 : 64; y.cg_fwd = 1; }
     if (y.in % 256 == 0) { y.bn_dx = 256; y.cg_dx = 2; }
     else { y.bn_dx = (y.in % 128 == 0) ? 128 : 64; y.cg_dx = 1; }
     // dW: hidden layer: D[out][in] = dZ^T X; head: D^T[in][64] = Y^T g
-    const int dM = (l == c->L) ? y.in : y.out;
-    const int dN = (l == c->L) ? kHeadCols : y.in;
-    y.bn_dw = (l == c->L) ? kHeadCols : pick_bn(dN);
+    const int dM = is_head ? y.in : y.out;
+    const int dN = is_head ? kHeadCols : y.in;
+    y.bn_dw = is_head ? kHeadCols : pick_bn(dN);
     // 512-wide dW tiles (two N = 256 MMAs sharing the dZ tile): the layer's dZ is read once
     // per split instead of once per 256 columns (SRL_DW512=1 enables)
-    if (l < c->L && dN % 512 == 0 && dM >= 256 && dw512_enabled()) y.bn_dw = 512;
-    y.cg_dw = (l < c->L && dM >= 256 && y.bn_dw >= 128) ? 2 : 1;
+    if (!is_head && dN % 512 == 0 && dM >= 256 && dw512_enabled()) y.bn_dw = 512;
+    y.cg_dw = (!is_head && dM >= 256 && y.bn_dw >= 128) ? 2 : 1;
     y.dw_m_tiles = (dM + 128 * y.cg_dw - 1) / (128 * y.cg_dw);
     y.dw_n_tiles = (dN + y.bn_dw - 1) / y.bn_dw;
     y.splits_max = std::max(1, (c->sms / y.cg_dw) / (y.dw_m_tiles * y.dw_n_tiles));
     y.part_rows = dM;
     y.ld_part = (int64_t)y.dw_n_tiles * y.bn_dw;
-    if ((st = dalloc(c, &y.part, sizeof(float) * y.splits_max * y.part_rows * y.ld_part))) return bail(st);
-    y.colsum_ld = (l == c->L) ? kHeadCols : y.out;
+    // the fused head kernel writes one dW_h^T partial per CTA (up to one per SM)
+    const int part_splits = is_head ? std::max(y.splits_max, c->sms) : y.splits_max;
+    if ((st = dalloc(c, &y.part, sizeof(float) * part_splits * y.part_rows * y.ld_part))) return bail(st);
+    y.colsum_ld = is_head ? kHeadCols : y.out;
     if ((st = dalloc(c, &y.colsum, sizeof(float) * c->sms * y.colsum_ld))) return bail(st);
+    if (is_head && (st = dalloc(c, &y.dz_colsum, sizeof(float) * c->sms * y.in))) return bail(st);
   }
   c->Y.resize(c->L);
   for (int l = 0; l < c->L; ++l)
-    if ((st = dalloc(c, &c->Y[l], sizeof(__half) * (size_t)n * c->dims[l + 1]))) return bail(st);
+    if ((st = dalloc(c, &c->Y[l], sizeof(__half) * (size_t)n * T * c->dims[l + 1]))) return bail(st);
   if ((st = dalloc(c, &c->G16, sizeof(__half) * (size_t)n * kHeadCols))) return bail(st);
   for (int k = 0; k < 2; ++k)
     if ((st = dalloc(c, &c->dZ[k], sizeof(__half) * (size_t)n * max_h))) return bail(st);
@@ -483,6 +557,7 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if ((st = dalloc(c, &c->gn, sizeof(double) * (kGradNormBlocks + 2)))) return bail(st);
   if ((st = dalloc(c, &c->gn_counter, sizeof(unsigned int) * 4))) return bail(st);
   if ((st = dalloc(c, &c->cc.err_dev, sizeof(int) * 4))) return bail(st);
+  if ((st = dalloc(c, &c->gbar, sizeof(unsigned) * 4))) return bail(st);
   if (cudaHostAlloc(reinterpret_cast<void**>(&c->err_pinned), sizeof(int) * 4, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->cc.err_host), c->err_pinned, 0) != cudaSuccess) {
     c->err_pinned = nullptr;
@@ -590,7 +665,7 @@ extern "C" srl_status srl_ppo_load_params(srl_ctx* c, const float* params_dev,
   CK(cudaMemsetAsync(c->m, 0, sizeof(float) * c->P, s));
   CK(cudaMemsetAsync(c->v, 0, sizeof(float) * c->P, s));
   CK(cudaMemsetAsync(c->t_dev, 0, sizeof(int64_t), s));
-  SegTable t = make_segs(c, {}, {});
+  SegTable t = make_segs(c, {}, {}, 0);
   CK(launch_shadow(t, c->params, s));
   return SRL_OK;
 }
@@ -693,29 +768,32 @@ static srl_status gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUte
   } while (0)
 
 // a3: the hidden layers of the forward pass, Y_l = tanh(Y_{l-1} W_l^T + b_l), into c->Y
+// a3: the hidden layers of the forward pass, Y_l = tanh(Y_{l-1} W_l^T + b_l), into c->Y; with
+// separate trunks each layer runs once per trunk on that trunk's column half (both read obs)
 static srl_status forward_hidden(srl_ctx* c, int n, const __half* X0, cudaStream_t s) {
-  const int L = c->L;
+  const int L = c->L, T = c->T;
   const int sms = c->sms;
   const int ld_obs = c->cfg.ld_obs;
-  for (int l = 0; l < L; ++l) {
-    const Lay& y = c->lay[l];
-    CUtensorMap ta, tb;
-    const __half* X = l == 0 ? X0 : c->Y[l - 1];
-    const int ldx = l == 0 ? ld_obs : y.in;
-    TMC(ta, X, y.in, n, (uint64_t)ldx * 2, 64, 128);
-    TMC(tb, y.w16, y.in, y.out, (uint64_t)y.w16_ld * 2, 64, y.bn_fwd / y.cg_fwd);
-    CUtensorMap to;
-    TMC(to, c->Y[l], y.out, n, (uint64_t)y.out * 2, 32, 32, 64);
-    GemmArgs g{};
-    g.M = n; g.N = y.out;
-    g.m_tiles = (n + 128 * y.cg_fwd - 1) / (128 * y.cg_fwd); g.n_tiles = y.out / y.bn_fwd; g.k_splits = 1;
-    g.kb_total = (y.in + 63) / 64; g.kb_per_split = g.kb_total;
-    g.bias = c->params + y.b_off;
-    ProfScope ps(c, s, l == 0 ? "fwd_l1" : "fwd_hidden", 2.0 * n * y.in * y.out,
-                 2.0 * n * (y.in + y.out) + 2.0 * y.in * y.out + 4.0 * y.out);
-    if (srl_status st = gemm(y.bn_fwd, false, false, tanh_accurate() ? EPI_TANH_ACC : EPI_TANH, y.cg_fwd,
-                             ta, tb, to, to, g, sms, s)) return st;
-  }
+  for (int l = 0; l < L; ++l)
+    for (int tr = 0; tr < T; ++tr) {
+      const Lay& y = c->hid(tr, l);
+      CUtensorMap ta, tb;
+      const __half* X = l == 0 ? X0 : c->Y[l - 1] + (size_t)tr * y.in;
+      const int ldx = l == 0 ? ld_obs : T * y.in;
+      TMC(ta, X, y.in, n, (uint64_t)ldx * 2, 64, 128);
+      TMC(tb, y.w16, y.in, y.out, (uint64_t)y.w16_ld * 2, 64, y.bn_fwd / y.cg_fwd);
+      CUtensorMap to;
+      TMC(to, c->Y[l] + (size_t)tr * y.out, y.out, n, (uint64_t)T * y.out * 2, 32, 32, 64);
+      GemmArgs g{};
+      g.M = n; g.N = y.out;
+      g.m_tiles = (n + 128 * y.cg_fwd - 1) / (128 * y.cg_fwd); g.n_tiles = y.out / y.bn_fwd; g.k_splits = 1;
+      g.kb_total = (y.in + 63) / 64; g.kb_per_split = g.kb_total;
+      g.bias = c->params + y.b_off;
+      ProfScope ps(c, s, l == 0 ? "fwd_l1" : "fwd_hidden", 2.0 * n * y.in * y.out,
+                   2.0 * n * (y.in + y.out) + 2.0 * y.in * y.out + 4.0 * y.out);
+      if (srl_status st = gemm(y.bn_fwd, false, false, tanh_accurate() ? EPI_TANH_ACC : EPI_TANH, y.cg_fwd,
+                               ta, tb, to, to, g, sms, s)) return st;
+    }
   return SRL_OK;
 }
 
@@ -747,19 +825,19 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   // ---------------- a3: forward hidden layers Y_l = tanh(Y_{l-1} W_l^T + b_l)
   if (srl_status st = forward_hidden(c, n, X0, s)) return st;
   // ---------------- a4: head GEMM + fused PPO loss -> per-sample dlogits G16
-  const Lay& hd = c->lay[L];
-  int grid_loss = 0;
-  {
-    CUtensorMap ta, tb;
-    TMC(ta, c->Y[L - 1], hd.in, n, (uint64_t)hd.in * 2, 64, 128);
-    TMC(tb, hd.w16, hd.in, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
-    CUtensorMap to;
-    TMC(to, c->G16, kHeadCols, n, (uint64_t)kHeadCols * 2, 32, 32, 64);
-    GemmArgs g{};
-    g.M = n; g.N = kHeadCols;
-    g.m_tiles = (n + 127) / 128; g.n_tiles = 1; g.k_splits = 1;
-    g.kb_total = (hd.in + 63) / 64; g.kb_per_split = g.kb_total;
-    g.bias = c->params + hd.b_off;
+  const int T = c->T;
+  const int HI = T * L;                                 // the head's index in c->lay
+  const Lay& hd = c->head();
+  int grid_loss = 0, dz_parts = 0;
+  const int hL = hd.in;                                 // T * h_L: both trunks' last layer
+  const float* hbias = T == 1 ? c->params + hd.b_off : c->hbias;
+  const int zcols = c->A + 1 + (int)c->heads.size();
+  const bool fused = head_fused_enabled() && hL % 128 == 0 && hL <= 512 &&
+                     head_fused_smem(hL, zcols) + 512 <= kSmemLimit;
+  std::vector<int> splits(HI + 1, 1), colsum_parts(HI + 1, 0);
+  int cur = 0;
+  auto loss_args = [&](GemmArgs& g) {
+    g.bias = hbias;
     g.colsum = hd.colsum; g.colsum_ld = kHeadCols;
     g.counters = c->counters;
     g.actions = actions; g.logp_old = logp_old; g.adv = adv; g.ret = ret;
@@ -770,17 +848,51 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     g.entropy_coef = c->cfg.entropy_coef; g.adv_eps = c->cfg.adv_eps;
     g.v_old = vclip ? v_old : nullptr; g.value_clip = c->cfg.value_clip;
     g.valid = valid;
+  };
+  if (fused) {
+    // a4 + the head's a5 in one kernel: loss, dZ_L, db_L / db_h column sums, dW_h^T partials
+    CUtensorMap ty, tw, to;
+    TMC(ty, c->Y[L - 1], hL, n, (uint64_t)hL * 2, 64, 128);
+    TMC(tw, hd.w16, hL, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
+    TMC(to, c->dZ[cur], hL, n, (uint64_t)hL * 2, 32, 32, 64);
+    GemmArgs g{};
+    g.M = n; g.N = kHeadCols;
+    g.m_tiles = (n + 127) / 128; g.n_tiles = 1; g.k_splits = 1;
+    loss_args(g);
+    g.part = hd.part; g.ld_part = hd.ld_part; g.part_split_stride = hd.part_rows * hd.ld_part;
+    const int grid = std::min(g.m_tiles, sms);
+    const double Ap1 = (double)hd.out;
+    ProfScope ps(c, s, "head_fused", 6.0 * n * hL * Ap1,
+                 4.0 * n * hL + (16.0 + 4.0 * g.n_heads) * n + 2.0 * kHeadCols * hL);
+    cudaError_t e = launch_head_fused(ty, tw, to, g, hL, hd.dz_colsum, grid, s);
+    if (e != cudaSuccess) FAIL(SRL_ECUDA, std::string("head_fused launch: ") + cudaGetErrorString(e));
+    grid_loss = grid;
+    splits[HI] = grid;
+    colsum_parts[HI] = grid;
+    dz_parts = grid;
+  } else {
+    CUtensorMap ta, tb;
+    TMC(ta, c->Y[L - 1], hd.in, n, (uint64_t)hd.in * 2, 64, 128);
+    TMC(tb, hd.w16, hd.in, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
+    CUtensorMap to;
+    TMC(to, c->G16, kHeadCols, n, (uint64_t)kHeadCols * 2, 32, 32, 64);
+    GemmArgs g{};
+    g.M = n; g.N = kHeadCols;
+    g.m_tiles = (n + 127) / 128; g.n_tiles = 1; g.k_splits = 1;
+    g.kb_total = (hd.in + 63) / 64; g.kb_per_split = g.kb_total;
+    loss_args(g);
     ProfScope ps(c, s, "head_loss", 2.0 * n * hd.in * hd.out,
                  2.0 * n * hd.in + 2.0 * n * kHeadCols + (16.0 + 4.0 * g.n_heads) * n);
     if (srl_status st = gemm(64, false, false, EPI_LOSS, 1, ta, tb, to, to, g, sms, s, &grid_loss)) return st;
+    colsum_parts[HI] = grid_loss;
   }
   // ---------------- a5: backward.  dW via split-K partials, dX with fused dtanh + db sums
-  std::vector<int> splits(L + 1, 1), colsum_parts(L + 1, 0);
-  colsum_parts[L] = grid_loss;
-  auto dW = [&](int l, const __half* Amat, int lda, const __half* Bmat, int ldb) -> srl_status {
-    const Lay& y = c->lay[l];
-    const int dM = (l == L) ? y.in : y.out;
-    const int dN = (l == L) ? kHeadCols : y.in;
+  // dW of layer index i (c->lay): D[dM][dN] = A^T B over the n samples (MN-major operands)
+  auto dW = [&](int i, const __half* Amat, int lda, const __half* Bmat, int ldb) -> srl_status {
+    const Lay& y = c->lay[i];
+    const bool is_head = i == HI;
+    const int dM = is_head ? y.in : y.out;
+    const int dN = is_head ? kHeadCols : y.in;
     CUtensorMap ta, tb;
     TMC(ta, Amat, dM, n, (uint64_t)lda * 2, 64, 64);
     TMC(tb, Bmat, dN, n, (uint64_t)ldb * 2, 64, 64);
@@ -793,34 +905,37 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     S = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
     g.k_splits = S;
     g.part = y.part; g.ld_part = y.ld_part; g.part_split_stride = y.part_rows * y.ld_part;
-    splits[l] = S;
-    const int realN = (l == L) ? y.out : dN;
-    ProfScope ps(c, s, l == L ? "dW_head" : (l == 0 ? "dW_l1" : "dW_hidden"),
+    splits[i] = S;
+    const int realN = is_head ? y.out : dN;
+    ProfScope ps(c, s, is_head ? "dW_head" : (y.l == 0 ? "dW_l1" : "dW_hidden"),
                  2.0 * n * dM * realN, 2.0 * n * (dM + dN) + 4.0 * S * dM * y.ld_part);
     return gemm(y.bn_dw, true, true, EPI_PART, y.cg_dw, ta, tb, ta, ta, g, sms, s);
   };
-  auto dX = [&](int l, const __half* dz_in, int k_width, __half* dz_out) -> srl_status {
-    // dZ_{in of layer l} = (dZ_out_l W_l) * (1 - Y_{l-1}^2), colsum -> db of layer l-1
-    const Lay& y = c->lay[l];
-    const Lay& yp = c->lay[l - 1];
+  // dX of layer index i: dZ_in = (dZ_out W) * (1 - Y_in^2) with the input's column sums;
+  // operands as (pointer, row stride) so a trunk works on its column half
+  auto dX = [&](int i, const __half* dz_in, int k_width, int ld_in, __half* dz_out,
+                const __half* yprev, int ld_out, float* colsum, int colsum_ld) -> srl_status {
+    const Lay& y = c->lay[i];
+    const bool is_head = i == HI;
     CUtensorMap ta, tb;
-    TMC(ta, dz_in, k_width, n, (uint64_t)k_width * 2, 64, 128);
+    TMC(ta, dz_in, k_width, n, (uint64_t)ld_in * 2, 64, 128);
     TMC(tb, y.w16, y.in, y.w16_rows, (uint64_t)y.w16_ld * 2, 64, 64);
     CUtensorMap to, ty;
-    TMC(to, dz_out, y.in, n, (uint64_t)y.in * 2, 32, 32, 64);
-    TMC(ty, c->Y[l - 1], y.in, n, (uint64_t)y.in * 2, 32, 32, 64);
+    TMC(to, dz_out, y.in, n, (uint64_t)ld_out * 2, 32, 32, 64);
+    TMC(ty, yprev, y.in, n, (uint64_t)ld_out * 2, 32, 32, 64);
     GemmArgs g{};
     g.M = n; g.N = y.in;
     g.m_tiles = (n + 128 * y.cg_dx - 1) / (128 * y.cg_dx); g.n_tiles = y.in / y.bn_dx; g.k_splits = 1;
     g.kb_total = (k_width + 63) / 64; g.kb_per_split = g.kb_total;
-    g.colsum = yp.colsum; g.colsum_ld = yp.colsum_ld;
+    g.colsum = colsum; g.colsum_ld = colsum_ld;
     g.counters = c->counters;
     int grid = 0;
-    const int realK = (l == L) ? y.out : k_width;
-    ProfScope ps(c, s, l == L ? "dX_head" : "dX_hidden", 2.0 * n * realK * y.in,
+    const int realK = is_head ? y.out : k_width;
+    ProfScope ps(c, s, is_head ? "dX_head" : "dX_hidden", 2.0 * n * realK * y.in,
                  2.0 * n * (k_width + 2.0 * y.in) + 2.0 * y.in * k_width);
     srl_status st = gemm(y.bn_dx, false, true, EPI_DTANH, y.cg_dx, ta, tb, to, ty, g, sms, s, &grid);
-    colsum_parts[l - 1] = grid;
+    if (is_head) dz_parts = grid;
+    else colsum_parts[c->hidx(y.t, y.l - 1)] = grid;
     return st;
   };
   // a6 through NVLink peer memory: finalise and extras write this rank's bucket into its
@@ -830,9 +945,9 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   const unsigned long long epoch = p2p ? c->epoch + 1 : 0;
   const int64_t xoff = (int64_t)(epoch & 1ull) * c->xstride();
   float* bk = p2p ? c->xbuf + xoff : c->grads;
-  // finalise (1/N-scaled split/column-sum reduction into the bucket) layers [lo, hi]
+  // finalise (1/N-scaled split/column-sum reduction into the bucket) layers [lo, hi] (T = 1)
   auto finalize_layers = [&](int lo, int hi) -> srl_status {
-    SegTable all = make_segs(c, splits, colsum_parts), t{};
+    SegTable all = make_segs(c, splits, colsum_parts, dz_parts), t{};
     double rd = 0;
     for (int l = lo; l <= hi; ++l) {
       t.s[t.n++] = all.s[2 * l];
@@ -845,10 +960,10 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   };
   // a6 overlap: once dW of layer 1 is done, layers 1..L (a contiguous bucket tail) are final;
   // their allreduce runs on comm_stream during layer 0's dX/dW.
-  // Opt-in (SRL_AR_OVERLAP=1): measured slower on 2-4 B200 for the Atari-shaped step, because
-  // NCCL's kernel takes SMs from the persistent one-CTA-per-SM GEMMs running beside it.
-  const bool overlap = apply && c->world > 1 && ar_overlap();
-  const int64_t split_off = c->lay[1].w_off;          // bucket [split_off, P) = layers 1..L
+  // Opt-in (SRL_AR_OVERLAP=1, shared trunk only): measured slower on 2-4 B200 for the
+  // Atari-shaped step, because NCCL's kernel takes SMs from the persistent GEMMs beside it.
+  const bool overlap = apply && c->world > 1 && ar_overlap() && T == 1;
+  const int64_t split_off = c->lay[std::min(1, L)].w_off;   // bucket [split_off, P) = layers 1..L
   auto early_reduce = [&]() -> srl_status {
     if (srl_status st = finalize_layers(1, L)) return st;
     CK(cudaEventRecord(c->ev_early, s));
@@ -858,67 +973,102 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
                       ncclFloat, ncclSum, c->comm, c->comm_stream));
     return SRL_OK;
   };
-  if (srl_status st = dW(L, c->Y[L - 1], hd.in, c->G16, kHeadCols)) return st;
+  if (!fused) {
+    if (srl_status st = dW(HI, c->Y[L - 1], hd.in, c->G16, kHeadCols)) return st;
+  }
   if (overlap && L == 1) if (srl_status st = early_reduce()) return st;
-  int cur = 0;
-  if (srl_status st = dX(L, c->G16, kHeadCols, c->dZ[cur])) return st;
+  if (!fused) {
+    if (srl_status st = dX(HI, c->G16, kHeadCols, kHeadCols, c->dZ[cur], c->Y[L - 1], hd.in,
+                           hd.dz_colsum, hd.in)) return st;
+  }
   for (int l = L - 1; l >= 0; --l) {
-    const Lay& y = c->lay[l];
-    const __half* Xl = l == 0 ? X0 : c->Y[l - 1];
-    const int ldx = l == 0 ? ld_obs : y.in;
-    if (srl_status st = dW(l, c->dZ[cur], y.out, Xl, ldx)) return st;
+    for (int tr = 0; tr < T; ++tr) {
+      const Lay& y = c->hid(tr, l);
+      const __half* Xl = l == 0 ? X0 : c->Y[l - 1] + (size_t)tr * y.in;
+      const int ldx = l == 0 ? ld_obs : T * y.in;
+      if (srl_status st = dW(c->hidx(tr, l), c->dZ[cur] + (size_t)tr * y.out, T * y.out, Xl, ldx)) return st;
+    }
     if (overlap && l == 1) if (srl_status st = early_reduce()) return st;
     if (l > 0) {
-      if (srl_status st = dX(l, c->dZ[cur], y.out, c->dZ[cur ^ 1])) return st;
+      for (int tr = 0; tr < T; ++tr) {
+        const Lay& y = c->hid(tr, l);
+        const Lay& yp = c->hid(tr, l - 1);
+        if (srl_status st = dX(c->hidx(tr, l), c->dZ[cur] + (size_t)tr * y.out, y.out, T * y.out,
+                               c->dZ[cur ^ 1] + (size_t)tr * y.in, c->Y[l - 1] + (size_t)tr * y.in,
+                               T * y.in, yp.colsum, yp.colsum_ld)) return st;
+      }
       cur ^= 1;
     }
   }
-  SegTable segs = make_segs(c, splits, colsum_parts);
-  if (srl_status st = overlap ? finalize_layers(0, 0) : finalize_layers(0, L)) return st;
-  CK(launch_extras(c->P, inv_n, c->stats_part, grid_loss, c->counters, bk, s));
-  if (apply) {
-    // ---------------- a6: gradient allreduce (bucket already scaled by 1/N_global)
-    if (overlap) {
-      // layer 0 + the 8 statistics, on the same comm stream (NCCL calls stay in one order)
-      CK(cudaEventRecord(c->ev_late, s));
-      CK(cudaStreamWaitEvent(c->comm_stream, c->ev_late, 0));
-      {
-        ProfScope ps(c, c->comm_stream, "allreduce", 0.0, 4.0 * (split_off + 8));
-        CKN(ncclGroupStart());
-        CKN(ncclAllReduce(c->grads, c->grads, (size_t)split_off, ncclFloat, ncclSum, c->comm, c->comm_stream));
-        CKN(ncclAllReduce(c->grads + c->P, c->grads + c->P, 8, ncclFloat, ncclSum, c->comm, c->comm_stream));
-        CKN(ncclGroupEnd());
+  SegTable segs = make_segs(c, splits, colsum_parts, dz_parts);
+  const bool gclip = apply && c->cfg.max_grad_norm > 0.f;
+  double part_bytes = 4.0 * dz_parts * hd.in;
+  for (int i = 0; i <= HI; ++i)
+    part_bytes += 4.0 * splits[i] * c->lay[i].out * c->lay[i].in + 4.0 * colsum_parts[i] * c->lay[i].colsum_ld;
+  // the fused finalise -> [grad norm] -> Adam launch (update_kernel)
+  auto update = [&](bool finalize, bool adam, float* bucket) -> srl_status {
+    UpdateArgs u{};
+    u.t = segs; u.P = c->P; u.inv_n = inv_n; u.bucket = bucket; u.counters = c->counters;
+    u.stats_part = c->stats_part; u.nstats = grid_loss;
+    u.finalize = finalize; u.adam = adam;
+    u.g = c->grads; u.p = c->params; u.m = c->m; u.v = c->v; u.t_dev = c->t_dev;
+    u.lr = c->cfg.lr; u.b1 = c->cfg.beta1; u.b2 = c->cfg.beta2; u.eps = c->cfg.adam_eps;
+    u.max_norm = gclip ? c->cfg.max_grad_norm : 0.f;
+    u.gn_part = c->gn; u.gn_norm = c->gn_norm(); u.gn_coef = c->gn_coef();
+    u.comm_err = c->world > 1 ? c->cc.err_dev : nullptr;
+    u.bar = c->gbar;
+    ProfScope ps(c, s, finalize ? (adam ? "grad_update" : "grad_finalize") : "adam",
+                 0.0, (finalize ? part_bytes : 0.0) + (adam ? 30.0 * c->P : 0.0));
+    CK(launch_update(u, s));
+    return SRL_OK;
+  };
+  if (!overlap) {
+    // world 1: ONE launch from the partials to the updated parameters; world > 1: finalise
+    // into the bucket the exchange reads, exchange, then the norm + Adam launch
+    const bool one = apply && c->world == 1;
+    if (srl_status st = update(true, one, bk)) return st;
+    if (apply && c->world > 1) {
+      if (p2p) {
+        ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8) * 2.0 * (c->world - 1) / c->world);
+        c->epoch = epoch;
+        CK(launch_p2p_allreduce(c->peers, c->world, c->rank, xoff, c->P + 8, epoch, 1.f, c->grads,
+                                c->cc, 3, s));
+      } else {
+        ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8));
+        CKN(ncclAllReduce(c->grads, c->grads, (size_t)(c->P + 8), ncclFloat, ncclSum, c->comm, s));
       }
-      CK(cudaEventRecord(c->ev_comm, c->comm_stream));
-      CK(cudaStreamWaitEvent(s, c->ev_comm, 0));
+      if (srl_status st = update(false, true, c->grads)) return st;
     }
-    else if (p2p) {
-      ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8) * c->world);
-      c->epoch = epoch;
-      CK(launch_p2p_allreduce(c->peers, c->world, c->rank, xoff, c->P + 8, epoch, 1.f, c->grads,
-                              c->cc, 3, s));
+  } else {
+    // opt-in NCCL overlap path (SRL_AR_OVERLAP=1): layers 1..L were finalised and their
+    // allreduce started during the backward; layer 0 + the statistics now
+    if (srl_status st = finalize_layers(0, 0)) return st;
+    CK(launch_extras(c->P, inv_n, c->stats_part, grid_loss, c->counters, bk, s));
+    CK(cudaEventRecord(c->ev_late, s));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_late, 0));
+    {
+      ProfScope ps(c, c->comm_stream, "allreduce", 0.0, 4.0 * (split_off + 8));
+      CKN(ncclGroupStart());
+      CKN(ncclAllReduce(c->grads, c->grads, (size_t)split_off, ncclFloat, ncclSum, c->comm, c->comm_stream));
+      CKN(ncclAllReduce(c->grads + c->P, c->grads + c->P, 8, ncclFloat, ncclSum, c->comm, c->comm_stream));
+      CKN(ncclGroupEnd());
     }
-    else if (c->world > 1) {
-      ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8));
-      CKN(ncclAllReduce(c->grads, c->grads, (size_t)(c->P + 8), ncclFloat, ncclSum, c->comm, s));
-    }
-    // ---------------- NEXT-3: global gradient-norm clipping of the reduced bucket
-    const bool gclip = c->cfg.max_grad_norm > 0.f;
+    CK(cudaEventRecord(c->ev_comm, c->comm_stream));
+    CK(cudaStreamWaitEvent(s, c->ev_comm, 0));
     if (gclip) {
       ProfScope ps(c, s, "grad_norm", 0.0, 4.0 * c->P);
       CK(launch_gradnorm(c->grads, c->P, c->gn, c->gn_counter, c->cfg.max_grad_norm,
                          c->gn_norm(), c->gn_coef(), s));
     }
-    // ---------------- a7: Adam + fp16 shadow refresh
     ProfScope ps(c, s, "adam", 0.0, 30.0 * c->P);
     CK(launch_adam(segs, c->P, c->params, c->m, c->v, c->grads, c->t_dev, c->cfg.lr,
                    c->cfg.beta1, c->cfg.beta2, c->cfg.adam_eps, s, gclip ? c->gn_coef() : nullptr,
-                   c->world > 1 ? c->cc.err_dev : nullptr));
+                   c->cc.err_dev));
   }
+  ProfScope ps_stats(c, s, "stats", 0.0, 0.0);
   CK(launch_stats(c->grads, c->P, adv_mean_std, n_global, c->cfg.value_coef, c->cfg.entropy_coef,
                   c->t_dev, apply, stats_out, s, c->counters,
-                  (apply && c->cfg.max_grad_norm > 0.f) ? c->gn_norm() : nullptr,
-                  c->world > 1 ? c->cc.err_dev : nullptr));
+                  gclip ? c->gn_norm() : nullptr, c->world > 1 ? c->cc.err_dev : nullptr));
   return SRL_OK;
 }
 
@@ -999,7 +1149,7 @@ extern "C" srl_status srl_policy_rollout(srl_ctx* c, int64_t n, const uint16_t* 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int nn = (int)n;
   if (srl_status st = forward_hidden(c, nn, reinterpret_cast<const __half*>(obs), s)) return st;
-  const Lay& hd = c->lay[c->L];
+  const Lay& hd = c->head();
   CUtensorMap ta, tb;
   TMC(ta, c->Y[c->L - 1], hd.in, nn, (uint64_t)hd.in * 2, 64, 128);
   TMC(tb, hd.w16, hd.in, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
@@ -1007,7 +1157,7 @@ extern "C" srl_status srl_policy_rollout(srl_ctx* c, int64_t n, const uint16_t* 
   g.M = nn; g.N = kHeadCols;
   g.m_tiles = (nn + 127) / 128; g.n_tiles = 1; g.k_splits = 1;
   g.kb_total = (hd.in + 63) / 64; g.kb_per_split = g.kb_total;
-  g.bias = c->params + hd.b_off;
+  g.bias = c->T == 1 ? c->params + hd.b_off : c->hbias;
   g.n_heads = (int)c->heads.size(); g.A = c->A;
   for (int h = 0; h < g.n_heads; ++h) g.head_size[h] = c->heads[h];
   g.seed = seed; g.keys = reinterpret_cast<const unsigned long long*>(keys);

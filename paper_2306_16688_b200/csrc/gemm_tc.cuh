@@ -361,6 +361,26 @@ struct OutStage {
   }
 };
 
+// one staging tile per warp: reused once the previous TMA store has read it
+struct OutStage1 {
+  uint8_t* buf;
+  int k;
+  __device__ __forceinline__ uint8_t* acquire() {
+    if (k > 0 && lane_id() == 0) bulk_wait_read<0>();
+    __syncwarp();
+    return buf;
+  }
+  __device__ __forceinline__ void release(uint8_t* t, const CUtensorMap* map, int col, int row) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane_id() == 0) {
+      tma_store_2d(map, t, col, row);
+      bulk_commit();
+    }
+    ++k;
+  }
+};
+
 // ---------------------------------------------------------------------------------------
 template <int BN, bool A_MN, bool B_MN, int EPI_KIND, int CG>
 __global__ void __launch_bounds__(kThreads, 1)

@@ -81,6 +81,13 @@ cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUt
                         const CUtensorMap& tb, const CUtensorMap& to, const CUtensorMap& ty,
                         const GemmArgs& args, int grid, cudaStream_t s);
 
+// ---- a4 + head part of a5 in one kernel (head_fused.cu): loss, dZ_L (+ db_L column sums into
+// colsum_y [grid][hL]) and dW_h^T partials [grid][hL][64] (args.part); hL % 128 == 0, <= 512
+size_t head_fused_smem(int hL, int zcols);
+cudaError_t launch_head_fused(const CUtensorMap& tmY, const CUtensorMap& tmW, const CUtensorMap& tmO,
+                              const GemmArgs& args, int hL, float* colsum_y, int grid,
+                              cudaStream_t s);
+
 // ---- parameter segments (misc.cu): one weight matrix or bias vector of the flat layout
 struct Segment {
   int64_t off;          // offset in the flat parameter / gradient vector
@@ -96,7 +103,9 @@ struct Segment {
   // fp16 shadow (weights only)
   __half* w16;
   int w16_ld;
+  float* b32;           // bias only, nullable: fp32 mirror the GEMM epilogue reads (R-AC head)
   int64_t item0;        // finalize: first work item (4 partial-buffer entries) of this segment
+  int warp;             // finalize: 1 = many splits, one WARP per item (lanes stride the splits)
 };
 constexpr int kMaxSegs = 20;
 struct SegTable {
@@ -112,6 +121,29 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
                         float b2, float eps, cudaStream_t s, const float* coef = nullptr,
                         const int* comm_err = nullptr);
 constexpr int kGradNormBlocks = 296;   // 2 x 148 SMs
+// a5 tail + a7 in one persistent launch (misc.cu update_kernel): finalise (if `finalize`) the
+// partials into `bucket` with the loss statistics, then (if `adam`) the optional global-norm
+// clip and Adam + fp16 shadow reading `g` (== bucket at world 1, the reduced bucket otherwise)
+struct UpdateArgs {
+  SegTable t;
+  int64_t P, items, witems, nbias;
+  float inv_n;
+  float* bucket;
+  unsigned long long* counters;
+  const double* stats_part;
+  int nstats;
+  int finalize, adam;
+  const float* g;
+  float *p, *m, *v;
+  const int64_t* t_dev;
+  float lr, b1, b2, eps, max_norm;
+  double* gn_part;          // [>= #SMs]
+  double* gn_norm;
+  float* gn_coef;
+  const int* comm_err;
+  unsigned* bar;            // grid barrier words [2], zero-initialised
+};
+cudaError_t launch_update(UpdateArgs u, cudaStream_t s);
 // a6 over NVLink peer memory (world <= 8 on one node): every rank's exposed bucket (double
 // buffered by step parity) and flag array, mapped into this process with CUDA IPC
 constexpr int kMaxPeers = 8;

@@ -24,32 +24,31 @@ __device__ __forceinline__ int find_seg(const SegTable& t, int64_t p) {
 // 4 consecutive entries along the partial buffer's contiguous dimension (float4 loads of every
 // split, coalesced across threads): W[r][c..c+3] for hidden layers; for the head, whose
 // partial holds dW^T[in][64], entries [i][j..j+3] written to W[j..j+3][i].
-__global__ void __launch_bounds__(256) finalize_w_kernel(const SegTable t, int64_t items,
-                                                         float inv_n, float* __restrict__ bucket,
-                                                         unsigned long long* counters) {
-  griddep_wait();
-  griddep_launch();
+__device__ __forceinline__ uint32_t finalize_w_body(const SegTable& t, int64_t items, float inv_n,
+                                                    float* __restrict__ bucket, int64_t q0,
+                                                    int64_t qstride) {
   uint32_t bad = 0;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < items;
-       q += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t q = q0; q < items; q += qstride) {
     int k = 0;
     for (int i = 0; i < t.n; ++i)
-      if (!t.s[i].is_bias && q >= t.s[i].item0) k = i;
+      if (!t.s[i].is_bias && !t.s[i].warp && q >= t.s[i].item0) k = i;
     const Segment& s = t.s[k];
-    const int prow_len = s.transposed ? (int)s.ld_part : s.cols;   // contiguous extent
+    // contiguous extent of a partial row; a transposed (head) partial holds dW^T [in][64] of
+    // which this segment's `rows` columns are used
+    const int prow_len = s.transposed ? min((int)s.ld_part, s.rows) : s.cols;
     const int per_row = (prow_len + 3) / 4;                        // work items per row
     const int64_t qi = q - s.item0;
     const int pr = (int)(qi / per_row), pc = 4 * (int)(qi % per_row);
     const float* src = s.part + (int64_t)pr * s.ld_part + pc;
     float a[4] = {0.f, 0.f, 0.f, 0.f};
-    if ((s.ld_part & 3) == 0 && pc + 4 <= prow_len) {
+    if ((s.ld_part & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pc + 4 <= prow_len) {
       const float4* s4 = reinterpret_cast<const float4*>(src);
       const int64_t st4 = s.split_stride / 4;
       for (int k0 = 0; k0 < s.splits; k0 += 16) {   // 16 loads in flight, summed in split order
         float4 x[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (k0 + j < s.splits) x[j] = __ldg(s4 + (int64_t)(k0 + j) * st4);
+          if (k0 + j < s.splits) x[j] = __ldcs(s4 + (int64_t)(k0 + j) * st4);
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           if (k0 + j < s.splits) { a[0] += x[j].x; a[1] += x[j].y; a[2] += x[j].z; a[3] += x[j].w; }
@@ -74,6 +73,83 @@ __global__ void __launch_bounds__(256) finalize_w_kernel(const SegTable t, int64
       bucket[p] = g;
     }
   }
+  return bad;
+}
+
+// the same for segments with many partials (the fused head kernel's one per CTA): one warp per
+// item, lane l sums splits l, l+32, ... in order, then a fixed butterfly (deterministic)
+__device__ __forceinline__ uint32_t finalize_w_warp_body(const SegTable& t, int64_t witems,
+                                                         float inv_n, float* __restrict__ bucket,
+                                                         int64_t w0, int64_t wstride) {
+  const int lane = threadIdx.x & 31;
+  uint32_t bad = 0;
+  for (int64_t q = w0; q < witems; q += wstride) {
+    int k = -1;
+    for (int i = 0; i < t.n; ++i)
+      if (!t.s[i].is_bias && t.s[i].warp && q >= t.s[i].item0) k = i;
+    if (k < 0) continue;
+    const Segment& s = t.s[k];
+    const int prow_len = s.transposed ? min((int)s.ld_part, s.rows) : s.cols;
+    const int per_row = (prow_len + 3) / 4;
+    const int64_t qi = q - s.item0;
+    const int pr = (int)(qi / per_row), pc = 4 * (int)(qi % per_row);
+    const float* src = s.part + (int64_t)pr * s.ld_part + pc;
+    const int cnt = min(4, prow_len - pc);
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    if ((s.ld_part & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && cnt == 4) {
+      for (int sp = lane; sp < s.splits; sp += 32) {
+        const float4 x = __ldcs(reinterpret_cast<const float4*>(src + (int64_t)sp * s.split_stride));
+        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+      }
+    } else {
+      for (int sp = lane; sp < s.splits; sp += 32)
+        for (int e = 0; e < cnt; ++e) a[e] += __ldg(src + (int64_t)sp * s.split_stride + e);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) a[e] += __shfl_xor_sync(0xffffffffu, a[e], o);
+    if (lane == 0)
+      for (int e = 0; e < cnt; ++e) {
+        const int c = pc + e;
+        if (s.transposed && c >= s.rows) break;
+        const int64_t p = s.transposed ? s.off + (int64_t)c * s.cols + pr : s.off + (int64_t)pr * s.cols + c;
+        const float g = a[e] * inv_n;
+        if (!isfinite(g)) ++bad;
+        bucket[p] = g;
+      }
+  }
+  return bad;
+}
+
+// bias element e of the bias segments (warp-wide): (1/N) * sum of the per-CTA column sums,
+// lane-strided partials then a fixed butterfly (deterministic)
+__device__ __forceinline__ uint32_t finalize_b_one(const SegTable& t, int e, float inv_n,
+                                                   float* __restrict__ bucket) {
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < t.n; ++i) {
+    const Segment& s = t.s[i];
+    if (!s.is_bias) continue;
+    if (e >= s.cols) { e -= s.cols; continue; }
+    float acc = 0.f;
+    for (int k = lane; k < s.nparts; k += 32) acc += __ldg(s.colsum + (int64_t)k * s.colsum_ld + e);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const float g = acc * inv_n;
+    if (lane == 0) bucket[s.off + e] = g;
+    return isfinite(g) ? 0u : 1u;
+  }
+  return 0u;
+}
+
+__global__ void __launch_bounds__(256) finalize_w_kernel(const SegTable t, int64_t items,
+                                                         float inv_n, float* __restrict__ bucket,
+                                                         unsigned long long* counters) {
+  griddep_wait();
+  griddep_launch();
+  const uint32_t bad = finalize_w_body(t, items, inv_n, bucket,
+                                       blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                                       (int64_t)gridDim.x * blockDim.x);
   const uint32_t tot = __reduce_add_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0 && tot) atomicAdd(counters, (unsigned long long)tot);
 }
@@ -86,39 +162,35 @@ __global__ void __launch_bounds__(256) finalize_b_kernel(const SegTable t, float
   griddep_wait();
   griddep_launch();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  int e = warp;
+  if (finalize_b_one(t, warp, inv_n, bucket) && (threadIdx.x & 31) == 0) atomicAdd(counters, 1ull);
+}
+
+// work items of the weight segments (4 partial-buffer entries each); sets item0.  witems
+// non-null: segments with more than 32 splits get warp items (their own index space)
+static int64_t finalize_items(SegTable& t, int* nbias, int64_t* witems = nullptr) {
+  int64_t items = 0, wit = 0;
+  int nb = 0;
   for (int i = 0; i < t.n; ++i) {
-    const Segment& s = t.s[i];
-    if (!s.is_bias) continue;
-    if (e >= s.cols) { e -= s.cols; continue; }
-    float acc = 0.f;
-    for (int k = lane; k < s.nparts; k += 32) acc += __ldg(s.colsum + (int64_t)k * s.colsum_ld + e);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      const float g = acc * inv_n;
-      bucket[s.off + e] = g;
-      if (!isfinite(g)) atomicAdd(counters, 1ull);
-    }
-    return;
+    Segment& g = t.s[i];
+    if (g.is_bias) { nb += g.cols; continue; }
+    const int64_t prow = g.transposed ? std::min<int64_t>(g.ld_part, g.rows) : g.cols;
+    const int64_t nrow = g.transposed ? g.cols : g.rows;      // head partial: [in][64]
+    const int64_t cnt = nrow * ((prow + 3) / 4);
+    g.warp = (witems && g.splits > 32) ? 1 : 0;
+    if (g.warp) { g.item0 = wit; wit += cnt; }
+    else { g.item0 = items; items += cnt; }
   }
+  if (nbias) *nbias = nb;
+  if (witems) *witems = wit;
+  return items;
 }
 
 cudaError_t launch_finalize_grads(const SegTable& t0, int64_t P, float inv_n, float* bucket,
                                   unsigned long long* counters, cudaStream_t s) {
   (void)P;
   SegTable t = t0;
-  int64_t items = 0;
   int nb = 0;
-  for (int i = 0; i < t.n; ++i) {
-    Segment& g = t.s[i];
-    if (g.is_bias) { nb += g.cols; continue; }
-    g.item0 = items;
-    const int64_t prow = g.transposed ? g.ld_part : g.cols;   // contiguous extent
-    const int64_t nrow = g.transposed ? g.cols : g.rows;      // head partial: [in][64]
-    items += nrow * ((prow + 3) / 4);
-  }
+  const int64_t items = finalize_items(t, &nb);
   int64_t blocks = (items + 255) / 256;
   if (blocks > 16 * num_sms()) blocks = 16 * num_sms();
   if (blocks < 1) blocks = 1;
@@ -164,32 +236,26 @@ __device__ __forceinline__ float adam_one(float& p, float& m, float& v, float g,
   return p;
 }
 
-__global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
-                                                   float* __restrict__ p, float* __restrict__ m,
-                                                   float* __restrict__ v,
-                                                   const float* __restrict__ g,
-                                                   const int64_t* __restrict__ t_dev, float lr,
-                                                   float b1, float b2, float eps,
-                                                   const float* __restrict__ coef,
-                                                   const int* __restrict__ comm_err) {
-  griddep_wait();
-  griddep_launch();
-  if (g[P + 5] > 0.f || (comm_err && *comm_err)) return;
-  const float cf = coef ? *coef : 1.f;           // NEXT-3 global-norm clip coefficient
-  const Segment& s = t.s[blockIdx.y];            // one segment per grid row
+// Adam over segment s for quads q = q0, q0 + qstride, ...; step = t + 1 (bias corrections)
+__device__ __forceinline__ void adam_seg_body(const Segment& s, float* __restrict__ p,
+                                              float* __restrict__ m, float* __restrict__ v,
+                                              const float* __restrict__ g, double step, float lr,
+                                              float b1, float b2, float eps, float cf, int64_t q0,
+                                              int64_t qstride) {
   const int cnt = s.rows * s.cols;
-  const int nq = (cnt + 3) >> 2;
-  int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nq) return;
-  const double step = (double)(t_dev[0] + 1);
+  const int64_t nq = (cnt + 3) >> 2;
+  if (q0 >= nq) return;
   const float bc1 = (float)(1.0 - pow((double)b1, step));
   const float bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, step));
   const float step_size = lr / bc1;
   const bool vec_w16 = !s.is_bias && (s.cols & 3) == 0 && (s.w16_ld & 3) == 0;
-  for (; q < nq; q += gridDim.x * blockDim.x) {
-    const int e0 = 4 * q;
+  // float4 only where the segment starts 16-byte aligned (every segment of the shared layout;
+  // the separate-trunk layout (R-AC) puts the critic after b_pi[A], A arbitrary)
+  const bool vec = (s.off & 3) == 0;
+  for (int64_t q = q0; q < nq; q += qstride) {
+    const int e0 = 4 * (int)q;
     const int64_t i0 = s.off + e0;
-    if (e0 + 4 <= cnt) {
+    if (vec && e0 + 4 <= cnt) {
       float4 pp = *reinterpret_cast<const float4*>(p + i0);
       float4 mm = *reinterpret_cast<const float4*>(m + i0);
       float4 vv = *reinterpret_cast<const float4*>(v + i0);
@@ -202,6 +268,9 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
       *reinterpret_cast<float4*>(p + i0) = pp;
       *reinterpret_cast<float4*>(m + i0) = mm;
       *reinterpret_cast<float4*>(v + i0) = vv;
+      if (s.b32) {
+        s.b32[e0] = pp.x; s.b32[e0 + 1] = pp.y; s.b32[e0 + 2] = pp.z; s.b32[e0 + 3] = pp.w;
+      }
       if (vec_w16) {                              // 4 entries of one row of the fp16 shadow
         const int r = e0 / s.cols, c = e0 - r * s.cols;
         __half2 h0 = __floats2half2_rn(pp.x, pp.y), h1 = __floats2half2_rn(pp.z, pp.w);
@@ -217,11 +286,12 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
         }
       }
     } else {
-      for (int e = e0; e < cnt; ++e) {
+      for (int e = e0; e < min(e0 + 4, cnt); ++e) {
         const int64_t i = s.off + e;
         float pi = p[i], mi = m[i], vi = v[i];
         adam_one(pi, mi, vi, g[i] * cf, b1, b2, step_size, bc2_sqrt, eps);
         p[i] = pi; m[i] = mi; v[i] = vi;
+        if (s.b32) s.b32[e] = pi;
         if (!s.is_bias) {
           const int r = e / s.cols, c = e - r * s.cols;
           s.w16[(int64_t)r * s.w16_ld + c] = __float2half_rn(pi);
@@ -229,6 +299,22 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
+                                                   float* __restrict__ p, float* __restrict__ m,
+                                                   float* __restrict__ v,
+                                                   const float* __restrict__ g,
+                                                   const int64_t* __restrict__ t_dev, float lr,
+                                                   float b1, float b2, float eps,
+                                                   const float* __restrict__ coef,
+                                                   const int* __restrict__ comm_err) {
+  griddep_wait();
+  griddep_launch();
+  if (g[P + 5] > 0.f || (comm_err && *comm_err)) return;
+  const float cf = coef ? *coef : 1.f;           // NEXT-3 global-norm clip coefficient
+  adam_seg_body(t.s[blockIdx.y], p, m, v, g, (double)(t_dev[0] + 1), lr, b1, b2, eps, cf,
+                blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
 cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float* v,
@@ -240,6 +326,111 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
   if (bx > 4 * num_sms()) bx = 4 * num_sms();
   return launch_k(adam_kernel, dim3((unsigned)bx, (unsigned)t.n), dim3(256), 0, s, 1, t, P, p, m,
                   v, bucket, t_dev, lr, b1, b2, eps, coef, comm_err);
+}
+
+// ---------------------------------------------------------------------------------------
+// a5 tail + a7 in ONE persistent launch (grid = #SMs, all blocks co-resident): finalise the
+// split-K / per-CTA partials into the 1/N-scaled bucket, the loss statistics into its 8 extra
+// slots, then (optionally) the global gradient norm (NEXT-3 R-G) and Adam with the fp16
+// shadow refresh.  Grid-wide barriers separate the phases, so the skip-on-non-finite rule of
+// a7 sees the whole bucket, exactly as the separate kernels did.
+// The block partials of the norm are summed in block order: deterministic.
+// The blocks call griddepcontrol.launch_dependents first, so the next grid (PDL) can only
+// start once every block of this one is resident: the spin barrier cannot starve.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
+  griddep_launch();
+  griddep_wait();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double step = (double)(u.t_dev[0] + 1);   // read before anyone can advance it
+  __shared__ double red[16];
+  if (u.finalize) {
+    uint32_t bad = finalize_w_body(u.t, u.items, u.inv_n, u.bucket, tid, nthr);
+    const int64_t gw = tid >> 5, nw = nthr >> 5;
+    bad += finalize_w_warp_body(u.t, u.witems, u.inv_n, u.bucket, gw, nw) * (lane == 0);
+    for (int64_t e = gw; e < u.nbias; e += nw) bad += finalize_b_one(u.t, (int)e, u.inv_n, u.bucket) && lane == 0;
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, bad);
+    if (lane == 0 && tot) atomicAdd(u.counters, (unsigned long long)tot);
+    if (blockIdx.x == 0 && warp < 5) {             // loss statistics / N
+      double x = 0.0;
+      for (int g = lane; g < u.nstats; g += 32) x += u.stats_part[(int64_t)g * 8 + warp];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) u.bucket[u.P + warp] = (float)(x * (double)u.inv_n);
+    }
+    grid_barrier(u.bar);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      u.bucket[u.P + 5] = (float)u.counters[0];
+      u.bucket[u.P + 6] = (float)u.counters[1];
+      u.bucket[u.P + 7] = 0.f;
+    }
+  }
+  if (!u.adam) return;
+  const float* g = u.g;
+  const bool skip = (u.finalize ? (*reinterpret_cast<volatile unsigned long long*>(u.counters) > 0)
+                                : (g[u.P + 5] > 0.f)) || (u.comm_err && *u.comm_err);
+  float cf = 1.f;
+  if (u.max_norm > 0.f) {                          // NEXT-3: global norm of the (reduced) bucket
+    double acc = 0.0;
+    const int64_t nq = u.P >> 2;
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    for (int64_t q = tid; q < nq; q += nthr) {
+      const float4 x = g4[q];
+      acc += (double)x.x * x.x + (double)x.y * x.y + (double)x.z * x.z + (double)x.w * x.w;
+    }
+    if (blockIdx.x == 0)
+      for (int64_t i = 4 * nq + threadIdx.x; i < u.P; i += blockDim.x) acc += (double)g[i] * g[i];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += red[w];
+      u.gn_part[blockIdx.x] = b;
+    }
+    grid_barrier(u.bar);
+    double x = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) x += __ldcg(u.gn_part + b);   // block order
+    const double norm = sqrt(x);
+    const double c = (double)u.max_norm / (norm + 1e-6);
+    cf = c < 1.0 ? (float)c : 1.f;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *u.gn_norm = norm;
+      *u.gn_coef = cf;
+    }
+  }
+  if (skip) return;
+  for (int i = 0; i < u.t.n; ++i)
+    adam_seg_body(u.t.s[i], u.p, u.m, u.v, g, step, u.lr, u.b1, u.b2, u.eps, cf, tid, nthr);
+}
+
+cudaError_t launch_update(UpdateArgs u, cudaStream_t s) {
+  int nb = 0;
+  int64_t wit = 0;
+  u.items = finalize_items(u.t, &nb, &wit);
+  u.witems = wit;
+  u.nbias = nb;
+  return launch_k(update_kernel, dim3(num_sms()), dim3(512), 0, s, 1, u);
 }
 
 // NEXT-3 global gradient-norm clipping (reading R-G, PyTorch clip_grad_norm_ semantics):
@@ -403,10 +594,13 @@ __global__ void shadow_kernel(const SegTable t, const float* __restrict__ p) {
   griddep_launch();
   for (int k = 0; k < t.n; ++k) {
     const Segment& s = t.s[k];
-    if (s.is_bias) continue;
     const int64_t cnt = (int64_t)s.rows * s.cols;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
          i += (int64_t)gridDim.x * blockDim.x) {
+      if (s.is_bias) {
+        if (s.b32) s.b32[i] = p[s.off + i];
+        continue;
+      }
       const int r = (int)(i / s.cols), c = (int)(i % s.cols);
       s.w16[(int64_t)r * s.w16_ld + c] = __float2half_rn(p[s.off + i]);
     }

@@ -41,7 +41,7 @@ class PPOConfigC(C.Structure):
                 ("max_local_n", C.c_int64), ("precision", C.c_int),
                 # NEXT-3 PPO variants
                 ("value_clip", C.c_float), ("max_grad_norm", C.c_float),
-                ("epochs", C.c_int), ("minibatches", C.c_int)]
+                ("epochs", C.c_int), ("minibatches", C.c_int), ("separate_critic", C.c_int)]
 
 
 class PPOStatsC(C.Structure):
@@ -214,12 +214,14 @@ class NetSpec:
     max_grad_norm: float = 0.0
     epochs: int = 1
     minibatches: int = 1
+    separate_critic: int = 0      # NEXT-3 R-AC
 
     @classmethod
     def from_config(cls, cfg):
         return cls(cfg.obs_dim, tuple(cfg.hidden), tuple(cfg.heads), cfg.ld_obs, cfg.clip_eps,
                    cfg.value_coef, cfg.entropy_coef, cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps,
-                   1e-8, cfg.gamma, cfg.lam, 0)
+                   1e-8, cfg.gamma, cfg.lam, 0,
+                   separate_critic=int(bool(getattr(cfg, "separate_critic", False))))
 
 
 class PPOContext:
@@ -239,7 +241,7 @@ class PPOContext:
                               spec.lr, spec.beta1, spec.beta2, spec.adam_eps, spec.adv_eps,
                               spec.gamma, spec.gae_lambda, int(spec.adv_unbiased),
                               int(max_local_n), 0, spec.value_clip, spec.max_grad_norm,
-                              int(spec.epochs), int(spec.minibatches))
+                              int(spec.epochs), int(spec.minibatches), int(spec.separate_critic))
         h = C.c_void_p()
         _check(lib().srl_ppo_create(C.byref(self.cfg), rank, world, nccl_id, self.device,
                                     C.byref(h)))

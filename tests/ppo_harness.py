@@ -117,7 +117,7 @@ def near_kink(cfg, params, obs, actions, logp_old, margin=KINK_MARGIN / 2, v_old
     for k in (np.log(1 + cfg.clip_eps), np.log(1 - cfg.clip_eps)):
         near |= np.abs(xi - k) < margin
     if value_clip > 0:
-        V = oracle.forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, obs)[:, -1]
+        V = oracle.forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, obs, separate=oracle.sep(cfg))[:, -1]
         vo = np.asarray(v_old, np.float64)
         R = np.asarray(ret, np.float64)
         d = V - vo
@@ -133,7 +133,7 @@ def value_kink_free(cfg, params, b, value_clip, margin=KINK_MARGIN, rounds=20):
     b = dict(b)
     vals = np.array(b["values"], np.float32)
     T, Bk = vals.shape[0] - 1, vals.shape[1]
-    V = oracle.forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, b["obs"])[:, -1]
+    V = oracle.forward(cfg.obs_dim, cfg.hidden, cfg.heads, params, b["obs"], separate=oracle.sep(cfg))[:, -1]
     for _ in range(rounds):
         _, r = oracle.gae(b["rewards"], vals, b["dones"], cfg.gamma, cfg.lam)
         vo = vals[:-1].reshape(-1).astype(np.float64)

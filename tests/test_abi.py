@@ -62,7 +62,7 @@ def test_create_rejects_bad_config(L):
     hid = (C.c_int * 1)(100)      # not a multiple of 64
     heads = (C.c_int * 1)(2)
     cfg = S.PPOConfigC(4, 8, 1, hid, 1, heads, 0.2, 0.5, 0.01, 3e-4, 0.9, 0.999, 1e-8, 1e-8,
-                       0.99, 0.95, 0, 32, 0, 0.0, 0.0, 1, 1)
+                       0.99, 0.95, 0, 32, 0, 0.0, 0.0, 1, 1, 0)
     h = C.c_void_p()
     assert L.srl_ppo_create(C.byref(cfg), 0, 1, None, 0, C.byref(h)) == 1
     assert b"hidden" in L.srl_last_error()

@@ -241,3 +241,18 @@ def test_prefetch_slots_against_oracle():
         mg = c.adam_state()[0].cpu().numpy().astype(np.float64)
         assert np.abs(mg - m).max() <= 1e-6 * np.abs(m).max()
         assert st["step"] == k + 1
+
+
+@pytest.mark.parametrize("name", ["atari", "gfootball", "hns"])
+def test_step_is_deterministic(name):
+    """Two contexts, same inputs, two chained steps each: bit-identical gradients, parameters
+    and Adam moments (fixed-order split/partial sums in the fused update kernel, no atomics
+    on floating-point values)."""
+    cfg = synth.get_config(name).with_(B=REDUCED[name] * synth.get_config(name).agents)
+    params, b = make_inputs(cfg, seed=23)
+    outs = []
+    for _ in range(2):
+        g = gpu_step(cfg, params, [b], apply=True, n_steps=2)
+        outs.append(g)
+    for k in ("bucket", "params", "m", "v"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k

@@ -75,9 +75,9 @@ def test_kshard_opposite_grads_cancel():
 def test_all_core_driver_equals_single_thread(threads):
     """bench.py's all-core cpu_baseline driver (oracle_loss_and_grad_mt) computes the same
     gradient and loss sums as oracle_loss_and_grad, up to the order of the block sums."""
-    cfg = synth.get_config("gfootball").with_(B=6)
+    cfg = synth.get_config("gfootball").with_(B=24)            # 4800 rows: the driver path
     params, b = make_inputs(cfg, seed=2)
-    o1 = oracle.ppo_step(cfg, params, [b], apply=True)
+    o1 = oracle.ppo_step(cfg, params, [b], apply=True, threads=1)
     oT = oracle.ppo_step(cfg, params, [b], apply=True, threads=threads)
     assert np.linalg.norm(oT["grad"] - o1["grad"]) <= 1e-12 * np.linalg.norm(o1["grad"])
     assert np.allclose(oT["sums"], o1["sums"], rtol=1e-12, atol=1e-12)

@@ -1,0 +1,184 @@
+"""CPU model of head_fused_kernel's mbarrier protocol (head_fused.cu): every warp role is a
+generator that yields the waits the kernel makes, in the kernel's order, and performs the
+same arrivals / commits.  Asynchronous completions (TMA bytes, tcgen05.commit) are modelled as
+immediate.  A run that cannot make progress is a protocol deadlock; a barrier that completes a
+phase twice before a waiter observed it is a parity aliasing error.  Run before a GPU test:
+
+    python tools/hf_protocol_sim.py
+"""
+import itertools
+import sys
+
+R, KDY = 6, 3
+
+
+class Bar:
+    def __init__(self, name, count):
+        self.name, self.count, self.pending, self.phase, self.completions = name, count, 0, 0, 0
+
+    def arrive(self, n=1):
+        self.pending += n
+        assert self.pending <= self.count, f"{self.name}: too many arrivals"
+        if self.pending == self.count:
+            self.pending = 0
+            self.phase ^= 1
+            self.completions += 1
+
+    def ready(self, parity):
+        return self.phase != parity
+
+
+def pos_a(j, KB):
+    return 0 if j == 0 else KB * (2 * j - 1)
+
+
+def pos_b(j, KB, m):
+    return KB * (2 * j + 2 if j + 1 < m else 2 * j + 1)
+
+
+def simulate(m, KB, verbose=False):
+    NP = KB // 2
+    B = {}
+    mk = lambda n, c: B.setdefault(n, Bar(n, c))
+    full = [mk(f"full{s}", 1) for s in range(R)]
+    empty = [mk(f"empty{s}", 1) for s in range(R)]
+    dfull = [mk(f"dfull{b}", 1) for b in range(KDY)]
+    dempty = [mk(f"dempty{b}", 8) for b in range(KDY)]
+    m3 = [mk(f"m3done{b}", 1) for b in range(2)]
+    gfull = [mk(f"gfull{b}", 4) for b in range(2)]
+    gempty = [mk(f"gempty{b}", 1) for b in range(2)]
+    wfull, lfull, lempty, dwdone = mk("wfull", 1), mk("lfull", 1), mk("lempty", 4), mk("dwdone", 1)
+    ring_owner = {}                      # slot -> position loaded (for overwrite checks)
+    named = {"n2": [0, 0]}               # dtanh named barrier: [arrived, generation]
+
+    def producer():
+        wfull.arrive()
+        w = 0
+        for j in range(m + 1):
+            groups = []
+            if j < m:
+                groups.append(("A", j))
+            if j >= 1:
+                groups.append(("B", j - 1))
+            for g in groups:
+                for kb in range(KB):
+                    s = w % R
+                    yield (empty[s], ((w // R) & 1) ^ 1)
+                    ring_owner[s] = (g, kb, w)
+                    full[s].arrive()
+                    w += 1
+
+    def mma():
+        yield (wfull, 0)
+        dyc = u3 = 0
+        for j in range(m + 1):
+            if j < m:
+                yield (lempty, (j & 1) ^ 1)
+                p0 = pos_a(j, KB)
+                for kb in range(KB):
+                    w = p0 + kb
+                    s = w % R
+                    yield (full[s], (w // R) & 1)
+                    assert ring_owner[s] == (("A", j), kb, w), ("MMA1 reads wrong slot", s, ring_owner[s], j, kb)
+                    empty[s].arrive()
+                lfull.arrive()
+            if j >= 1:
+                jb = j - 1
+                gb = jb & 1
+                yield (gfull[gb], (jb >> 1) & 1)
+                p0 = pos_b(jb, KB, m)
+                for c in range(NP):
+                    for h in range(2):
+                        b = dyc % KDY
+                        yield (dempty[b], ((dyc // KDY) & 1) ^ 1)
+                        dfull[b].arrive()
+                        dyc += 1
+                    w = p0 + 2 * c
+                    s = w % R
+                    assert s % 2 == 0 and s + 1 < R
+                    yield (full[s], (w // R) & 1)
+                    yield (full[s + 1], ((w + 1) // R) & 1)
+                    assert ring_owner[s] == (("B", jb), 2 * c, w) and ring_owner[s + 1] == (("B", jb), 2 * c + 1, w + 1)
+                    m3[u3 & 1].arrive()
+                    u3 += 1
+                gempty[gb].arrive()
+        dwdone.arrive()
+
+    def loss(lw):
+        for j in range(m):
+            yield (lfull, j & 1)
+            lempty.arrive()
+            gb = j & 1
+            yield (gempty[gb], ((j >> 1) & 1) ^ 1)
+            gfull[gb].arrive()
+
+    def dtanh(dw):
+        dyc = u3 = 0
+        for j in range(m):
+            p0 = pos_b(j, KB, m)
+            for c in range(NP):
+                for h in range(2):
+                    kb = 2 * c + h
+                    b = dyc % KDY
+                    wk = p0 + kb
+                    yield (dfull[b], (dyc // KDY) & 1)
+                    dempty[b].arrive()
+                    s = wk % R
+                    yield (full[s], (wk // R) & 1)
+                    assert ring_owner[s] == (("B", j), kb, wk), ("dtanh reads wrong slot", dw, s, ring_owner[s], j, kb)
+                    dyc += 1
+                # named barrier over the 8 dtanh warps
+                gen = named["n2"][1]
+                named["n2"][0] += 1
+                if named["n2"][0] == 8:
+                    named["n2"] = [0, gen + 1]
+                yield ("named", gen)
+                if dw == 0:
+                    yield (m3[u3 & 1], (u3 >> 1) & 1)
+                    s = (p0 + 2 * c) % R
+                    empty[s].arrive()
+                    empty[s + 1].arrive()
+                u3 += 1
+        yield (dwdone, 0)
+
+    roles = {"producer": producer(), "mma": mma()}
+    for i in range(4):
+        roles[f"loss{i}"] = loss(i)
+    for i in range(8):
+        roles[f"dtanh{i}"] = dtanh(i)
+    waiting = {k: None for k in roles}
+    done = set()
+    steps = 0
+    while len(done) < len(roles):
+        progress = False
+        for name, g in roles.items():
+            if name in done:
+                continue
+            while True:
+                w = waiting[name]
+                if w is not None:
+                    if w[0] == "named":
+                        if named["n2"][1] <= w[1]:
+                            break
+                    elif not w[0].ready(w[1]):
+                        break
+                try:
+                    waiting[name] = next(g)
+                    progress = True
+                    steps += 1
+                except StopIteration:
+                    done.add(name)
+                    progress = True
+                    break
+        if not progress:
+            blocked = {k: (v[0].name if v and v[0] != "named" else "named", v[1] if v else None)
+                       for k, v in waiting.items() if k not in done}
+            raise RuntimeError(f"deadlock m={m} KB={KB}: {blocked}")
+    return steps
+
+
+if __name__ == "__main__":
+    for KB, m in itertools.product((2, 4, 8), (1, 2, 3, 4, 7, 8)):
+        simulate(m, KB)
+    print("protocol ok for KB in {2,4,8}, m in {1,2,3,4,7,8}")
+    sys.exit(0)

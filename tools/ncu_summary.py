@@ -18,9 +18,25 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
 
-# launch order of one srl_ppo_train_step for an L=2 MLP (see api.cu)
-STEP_ORDER = ["gae_scan", "fwd_l1", "fwd_hidden", "head_loss", "dW_head", "dX_head", "dW_hidden",
-              "dX_hidden", "dW_l1", "finalize_w", "finalize_b", "extras", "adam", "stats"]
+def label(kernel):
+    """Short name of one of our launches from ncu's (demangled) kernel name."""
+    k = kernel
+    if "gae_kernel" in k:
+        return "gae_scan"
+    if "head_fused" in k:
+        return "head_fused"
+    if "update_kernel" in k:
+        return "grad_update"
+    if "stats_kernel" in k:
+        return "stats"
+    if "p2p_allreduce" in k:
+        return "allreduce"
+    if "p2p_moments" in k:
+        return "adv_norm"
+    if "gemm_tc_kernel" in k:
+        epi = k.split("gemm_tc_kernel<")[1].split(">")[0].split(",")[3].strip()
+        return {"0": "fwd", "4": "fwd", "1": "dX", "2": "dW", "3": "head_loss", "5": "head_sample"}.get(epi, "gemm")
+    return k.split("(")[0].split("::")[-1][:40]
 
 
 def launches(path, rnd, config="atari"):
@@ -35,28 +51,33 @@ def launches(path, rnd, config="atari"):
             r["Metric Value"].replace(",", ""))
     recs = list(by.values())
     starts = [i for i, r in enumerate(recs) if ("gae_kernel" in r["kernel"])]
-    start = starts[min(3, len(starts) - 1)]          # the first step after 3 warm-up steps
-    step = recs[start:start + len(STEP_ORDER)]
+    k0 = min(3, len(starts) - 1)                       # the first step after 3 warm-up steps
+    start = starts[k0]
+    end = starts[k0 + 1] if k0 + 1 < len(starts) else len(recs)
+    step = recs[start:end]
     tot = sum(r["gpu__time_duration.sum"] for r in step)
     lines = [f"# {rnd}: ncu launch list, one `srl_ppo_train_step` ({config}-shaped, 1 x B200)", "",
              "Cold-cache, serialised per-launch durations (`--metrics gpu__time_duration.sum,"
              "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none`); compare shares.", "",
              "| kernel | ncu name | us | share | DRAM read MB | DRAM write MB |",
              "|---|---|---|---|---|---|"]
-    traffic = {}
-    for name, r in zip(STEP_ORDER, step):
+    traffic = {"launches": [], "dram_bytes": []}     # in launch order (bench.py matches by position)
+    seen = collections.Counter()
+    for r in step:
+        name = label(r["kernel"])
+        seen[name] += 1
         t = r["gpu__time_duration.sum"] / 1e3
         rd, wr = r.get("dram__bytes_read.sum", 0.0), r.get("dram__bytes_write.sum", 0.0)
-        traffic[name] = rd + wr
-        lines.append(f"| {name} | `{r['kernel'][:60]}` | {t:.1f} | {100 * t * 1e3 / tot:.1f}% | "
+        traffic["launches"].append(name)
+        traffic["dram_bytes"].append(rd + wr)
+        lines.append(f"| {name}#{seen[name]} | `{r['kernel'][:60]}` | {t:.1f} | {100 * t * 1e3 / tot:.1f}% | "
                      f"{rd / 1e6:.1f} | {wr / 1e6:.1f} |")
     lines.append(f"| **step** | | {tot / 1e3:.1f} | 100% | | |")
-    traffic["grad_finalize"] = traffic["finalize_w"] + traffic["finalize_b"] + traffic["extras"]
-    open(os.path.join(PROF, f"{rnd}_launches.md"), "w").write("\n".join(lines) + "\n")
     jp = os.path.join(PROF, "ncu_traffic.json")
     data = json.load(open(jp)) if os.path.exists(jp) else {}
-    data.setdefault(config, {}).update(traffic)
-    data.setdefault("_source", {})[config] = f"profiles/{rnd}_launches.csv"
+    data[config] = traffic
+    data.setdefault("_source", {})[config] = f"{rnd}_launches.csv"
+    open(os.path.join(PROF, f"{rnd}_launches.md"), "w").write("\n".join(lines) + "\n")
     json.dump(data, open(jp, "w"), indent=1)
     print("\n".join(lines))
 
