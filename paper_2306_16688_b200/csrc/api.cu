@@ -832,7 +832,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   const int hL = hd.in;                                 // T * h_L: both trunks' last layer
   const float* hbias = T == 1 ? c->params + hd.b_off : c->hbias;
   const int zcols = c->A + 1 + (int)c->heads.size();
-  const bool fused = head_fused_enabled() && hL % 128 == 0 && hL <= 512 &&
+  const bool fused = head_fused_enabled() && hL % 128 == 0 && hL <= 512 && c->A + 1 <= 32 &&
                      head_fused_smem(hL, zcols) + 512 <= kSmemLimit;
   std::vector<int> splits(HI + 1, 1), colsum_parts(HI + 1, 0);
   int cur = 0;
@@ -853,7 +853,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     // a4 + the head's a5 in one kernel: loss, dZ_L, db_L / db_h column sums, dW_h^T partials
     CUtensorMap ty, tw, to;
     TMC(ty, c->Y[L - 1], hL, n, (uint64_t)hL * 2, 64, 128);
-    TMC(tw, hd.w16, hL, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 64);
+    TMC(tw, hd.w16, hL, kHeadCols, (uint64_t)hd.w16_ld * 2, 64, 32);   // the 32 real head rows
     TMC(to, c->dZ[cur], hL, n, (uint64_t)hL * 2, 32, 32, 64);
     GemmArgs g{};
     g.M = n; g.N = kHeadCols;
@@ -1192,12 +1192,21 @@ extern "C" srl_status srl_batch_upload(srl_ctx* c, int slot, int T, int B, const
     if ((st = dalloc(c, &sl.logp_old, sizeof(float) * n))) return st;
     CK(cudaEventCreateWithFlags(&sl.uploaded, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sl.released, cudaEventDisableTiming));
+    CK(cudaDeviceSynchronize());                   // the zeroing memsets (see below)
     CK(cudaEventRecord(sl.released, c->copy_stream));
   }
-  if (trunc_values && !sl.trunc_values)
+  bool fresh = false;
+  if (trunc_values && !sl.trunc_values) {
     if (srl_status st = dalloc(c, &sl.trunc_values, sizeof(float) * n)) return st;
-  if (valid && !sl.valid)
+    fresh = true;
+  }
+  if (valid && !sl.valid) {
     if (srl_status st = dalloc(c, &sl.valid, n)) return st;
+    fresh = true;
+  }
+  // dalloc zeroes new buffers with cudaMemset on the legacy stream, which the non-blocking copy
+  // stream does not wait for: finish the zeroing before the first upload into them
+  if (fresh) CK(cudaDeviceSynchronize());
   const int64_t m = (int64_t)T * B;
   cudaStream_t cs = c->copy_stream;
   CK(cudaStreamWaitEvent(cs, sl.released, 0));      // the last step on this slot is done with it

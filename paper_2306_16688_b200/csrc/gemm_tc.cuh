@@ -128,16 +128,13 @@ struct GemmCfg {
 };
 
 __device__ __forceinline__ void wait_bounded(uint64_t* bar, uint32_t parity) {
-  // bounded spin: a lost arrival traps (error surfaced to the host) instead of hanging
-  uint32_t it = 0;
-  long long t0 = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if (((++it) & 1023) == 0) {
-      long long now = clock64();
-      if (t0 == 0) t0 = now;
-      else if (now - t0 > (1ll << 35)) __trap();
-    }
-  }
+  // the thread sleeps in try_wait (suspend-time hint) instead of spinning and stealing issue
+  // slots from working warps; bounded: a lost arrival (a kernel bug, never another rank)
+  // traps after ~17 s so the error reaches the host instead of a hang
+  if (mbar_try_wait_sleep(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait_sleep(bar, parity))
+    if (clock64() - t0 > (1ll << 35)) __trap();
 }
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
@@ -656,6 +653,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           uint8_t* t = ost.acquire();
           stile_write_row(t, (int)lane, v);
           ost.release(t, &tmO, col0, row0);
+          // db column sums of the fp32 values (summing the fp16-rounded tile on the tensor
+          // core was measured too imprecise for some bias tensors, and slower)
           const float s = transpose_reduce32(v);
           my_colsum[col0 + lane] += s;
         };

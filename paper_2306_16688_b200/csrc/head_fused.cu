@@ -11,11 +11,12 @@
 // L2), dZ_L written once.
 //
 // Per tile, two passes over the tile's hL/64 column blocks of Y_L through one TMA ring:
-//   pass A: MMA1  logits[128][64]  += Y_kb . W_h[:, kb]^T          (A K-major, B K-major)
-//   pass B: MMA2  dY_kb[128][64]    = g . W_h[:, kb]                (A K-major, B MN-major)
+//   pass A: MMA1  logits[128][32]  += Y_kb . W_h[:, kb]^T          (A K-major, B K-major)
+//   pass B: MMA2  dY_kb[128][64]    = g[:, 0:32] . W_h[0:32, kb]   (A K-major, B MN-major)
 //           MMA3  dW^T[pair c]     += Y_{2c,2c+1}^T . g              (A MN-major over the two
 //                                     ring slots of the pair, B MN-major)
-// One smem copy of W_h ([64 head rows][hL], 64-column boxes) serves as the K-major B of
+// The head has A + 1 <= 32 real rows (the host checks), so W_h lives in smem as 32-row boxes.
+// One smem copy of W_h ([32 head rows][hL], 64-column boxes) serves as the K-major B of
 // MMA1 and the MN-major B of MMA2; the g tile serves as the K-major A of MMA2 and the
 // MN-major B of MMA3; a Y ring slot serves as the K-major A of MMA1 and the MN-major A of MMA3.
 //
@@ -34,7 +35,8 @@ namespace srl {
 namespace hf {
 constexpr int kRing = 6;                      // Y ring slots (even: an MMA3 pair is adjacent)
 constexpr int kSlot = 128 * 64 * 2;           // one [128 rows][64 cols] fp16 block, 16 KB
-constexpr int kWBox = 64 * 64 * 2;            // one [64 head rows][64 cols] W_h box, 8 KB
+constexpr int kWRows = 32;                    // head rows kept (A + 1 <= 32)
+constexpr int kWBox = kWRows * 64 * 2;        // one [32 head rows][64 cols] W_h box, 4 KB
 constexpr int kGBytes = 128 * 64 * 2;         // g tile [128][64] fp16
 constexpr int kDy = 3;                        // dY buffers
 constexpr int kThreads = 512;
@@ -42,7 +44,7 @@ constexpr int kLossWarps = 4, kDtWarps = 8;
 constexpr uint32_t kColLogits = 256, kColDy = 320;
 
 struct Layout {
-  uint32_t ring, w, g, ostage, zbuf, cs_h, bias, bars, total;
+  uint32_t ring, w, g, ostage, zbuf, cs_y, cs_h, bias, bars, total;
 };
 __host__ __device__ inline Layout layout(int hL, int zcols) {
   Layout L;
@@ -51,7 +53,8 @@ __host__ __device__ inline Layout layout(int hL, int zcols) {
   L.g = L.w + (hL / 64) * kWBox;
   L.ostage = L.g + 2 * kGBytes;
   L.zbuf = L.ostage + kDtWarps * kStageTile;
-  L.cs_h = L.zbuf + kLossWarps * zcols * kZPitch * 4;
+  L.cs_y = L.zbuf + kLossWarps * zcols * kZPitch * 4;
+  L.cs_h = L.cs_y + kDtWarps * (hL / 2) * 4;       // per dtanh warp: its hL / 2 columns
   L.bias = L.cs_h + kLossWarps * 64 * 4;
   L.bars = L.bias + 64 * 4;
   L.total = L.bars + 512;
@@ -154,7 +157,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     }
   } else if (warp == 1) {
     // ============================ MMA issuer (same stream order as the producer)
-    constexpr uint32_t ID1 = umma_idesc_f16(128, 64, false, false);
+    constexpr uint32_t ID1 = umma_idesc_f16(128, kWRows, false, false);
     constexpr uint32_t ID2 = umma_idesc_f16(128, 64, false, true);
     constexpr uint32_t ID3 = umma_idesc_f16(128, 64, true, true);
     const uint32_t ring0 = smem_u32(smem + SL.ring), w0 = smem_u32(smem + SL.w);
@@ -200,7 +203,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
             if (lane == 0) {
               const uint32_t wb = w0 + kb * kWBox;
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
+              for (int k = 0; k < kWRows / 16; ++k)      // K = the 32 real head columns of g
                 tc_mma_f16_cg<1>(tmem_base + kColDy + 64 * b, umma_desc_sw128(g0 + k * 32, 16, 1024),
                                  umma_desc_sw128(wb + k * 2048, 8192, 1024), ID2, k > 0 ? 1u : 0u);
               tc_commit_cg<1>(&dfull[b]);
@@ -257,16 +260,15 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
       wait_bounded(lfull, j & 1);
       tc_fence_after();
       {
-        float z[64];
+        float z[32];                                 // the A + 1 <= 32 head outputs
         const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + kColLogits;
         tmem_ld32(ta, z);
-        tmem_ld32(ta + 32, z + 32);
         tc_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(lempty);         // MMA1 of the next tile may overwrite
 #pragma unroll
-        for (int jj = 0; jj < 64; ++jj)
+        for (int jj = 0; jj < 32; ++jj)
           if (jj <= args.A) zb[jj * kZPitch + lane] = z[jj] + bias_s[jj];
       }
       if (args.mean_std) {
@@ -331,9 +333,9 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
   } else if (warp >= 8) {
     // ============================ dtanh epilogue: dZ_L = dY .* (1 - Y^2), db_L column sums
     const int dw = warp - 8, grp = dw >> 2, quad = warp & 3;
-    float cs[KB];                                    // column kb*64 + 32 grp + lane, my rows
-#pragma unroll
-    for (int kb = 0; kb < KB; ++kb) cs[kb] = 0.f;
+    float* my_cs = reinterpret_cast<float*>(smem + SL.cs_y) + dw * (hL / 2);   // col kb*32 + c
+    for (int i = lane; i < hL / 2; i += 32) my_cs[i] = 0.f;
+    __syncwarp();
     OutStage1 ost{smem + SL.ostage + dw * kStageTile, 0};
     uint32_t nsat = 0;
     uint32_t dyc = 0, u3 = 0;
@@ -381,7 +383,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
           uint8_t* tl = ost.acquire();
           stile_write_row(tl, (int)lane, v);
           ost.release(tl, &tmO, kb * 64 + 32 * grp, t * 128 + quad * 32);
-          cs[kb] += transpose_reduce32(v);
+          my_cs[kb * 32 + lane] += transpose_reduce32(v);   // db_L: fp32 column sums
         }
         // both blocks of the pair read by all 8 dtanh warps: once MMA3 of the pair is done too,
         // the two ring slots go back to the producer
@@ -397,17 +399,13 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
     if (args.counters) count_warp(args.counters + 1, nsat);
-    // column sums: the four row quadrants of each half, in quadrant order, through the (now
-    // idle) ring; the producer finished all its loads before the last pair was released
+    // per-CTA column sums: the four row quadrants of each half, in quadrant order
     named_bar_sync(2, 256);
-    float* red = reinterpret_cast<float*>(smem + SL.ring);   // [8 warps][KB][32]
-#pragma unroll
-    for (int kb = 0; kb < KB; ++kb) red[(dw * KB + kb) * 32 + lane] = cs[kb];
-    named_bar_sync(2, 256);
+    const float* cs0 = reinterpret_cast<const float*>(smem + SL.cs_y);
     for (int i = dw * 32 + lane; i < hL; i += 256) {
-      const int kb = i / 64, g2 = (i % 64) / 32, ln = i % 32;
+      const int kb = i / 64, g2 = (i % 64) / 32, c = i % 32;
       float x = 0.f;
-      for (int q = 0; q < 4; ++q) x += red[((g2 * 4 + q) * KB + kb) * 32 + ln];
+      for (int q = 0; q < 4; ++q) x += cs0[(g2 * 4 + q) * (hL / 2) + kb * 32 + c];
       colsum_y[(int64_t)blockIdx.x * hL + i] = x;
     }
     // dW_h^T of this CTA -> partial [blockIdx][hL][64] (the transposed split-K layout of the
@@ -458,6 +456,7 @@ static cudaError_t launch_kb(const CUtensorMap& tmY, const CUtensorMap& tmW, con
 cudaError_t launch_head_fused(const CUtensorMap& tmY, const CUtensorMap& tmW, const CUtensorMap& tmO,
                               const GemmArgs& args, int hL, float* colsum_y, int grid,
                               cudaStream_t s) {
+  if (args.A + 1 > hf::kWRows) return cudaErrorInvalidValue;
   const int zcols = args.A + 1 + args.n_heads;
   const size_t smem = head_fused_smem(hL, zcols);
   if (smem + 512 > kSmemLimit) return cudaErrorInvalidConfiguration;

@@ -44,13 +44,13 @@ __device__ __forceinline__ uint32_t finalize_w_body(const SegTable& t, int64_t i
     if ((s.ld_part & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pc + 4 <= prow_len) {
       const float4* s4 = reinterpret_cast<const float4*>(src);
       const int64_t st4 = s.split_stride / 4;
-      for (int k0 = 0; k0 < s.splits; k0 += 16) {   // 16 loads in flight, summed in split order
-        float4 x[16];
+      for (int k0 = 0; k0 < s.splits; k0 += 20) {   // 20 loads in flight, summed in split order
+        float4 x[20];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < 20; ++j)
           if (k0 + j < s.splits) x[j] = __ldcs(s4 + (int64_t)(k0 + j) * st4);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < 20; ++j)
           if (k0 + j < s.splits) { a[0] += x[j].x; a[1] += x[j].y; a[2] += x[j].z; a[3] += x[j].w; }
       }
     } else {
@@ -97,9 +97,16 @@ __device__ __forceinline__ uint32_t finalize_w_warp_body(const SegTable& t, int6
     const int cnt = min(4, prow_len - pc);
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     if ((s.ld_part & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && cnt == 4) {
-      for (int sp = lane; sp < s.splits; sp += 32) {
-        const float4 x = __ldcs(reinterpret_cast<const float4*>(src + (int64_t)sp * s.split_stride));
-        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+      for (int sp0 = lane; sp0 < s.splits; sp0 += 256) {     // 8 loads in flight per lane
+        float4 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int sp = sp0 + 32 * j;
+          x[j] = sp < s.splits ? __ldcs(reinterpret_cast<const float4*>(src + (int64_t)sp * s.split_stride))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { a[0] += x[j].x; a[1] += x[j].y; a[2] += x[j].z; a[3] += x[j].w; }
       }
     } else {
       for (int sp = lane; sp < s.splits; sp += 32)
@@ -132,7 +139,16 @@ __device__ __forceinline__ uint32_t finalize_b_one(const SegTable& t, int e, flo
     if (!s.is_bias) continue;
     if (e >= s.cols) { e -= s.cols; continue; }
     float acc = 0.f;
-    for (int k = lane; k < s.nparts; k += 32) acc += __ldg(s.colsum + (int64_t)k * s.colsum_ld + e);
+    for (int k0 = lane; k0 < s.nparts; k0 += 256) {           // 8 loads in flight per lane
+      float x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0 + 32 * j;
+        x[j] = k < s.nparts ? __ldg(s.colsum + (int64_t)k * s.colsum_ld + e) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += x[j];
+    }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     const float g = acc * inv_n;
