@@ -2,19 +2,16 @@
 //
 // GAE (BASELINE.json north_star):
 //   m_t = 1 - d_t;  delta_t = r_t + gamma v_{t+1} m_t - v_t;  A_t = delta_t + gamma lambda m_t A_{t+1}
-// is an affine recurrence A_t = delta_t + c_t A_{t+1}.  One thread per env column (coalesced
-// time-major rows) is too little parallelism for B ~ 1k columns, so each block owns 32
-// columns and splits T into W chunks of TC rows, one warp per chunk:
-//   pass 1: every warp scans its chunk from A_end = 0 and publishes (a_first, prod c);
-//   combine: A entering chunk w = fold of the later chunks' (a, P) summaries;
-//   pass 2: every warp re-runs the exact recurrence from the true A_end (values are
-//   register-resident), writes adv/ret and accumulates moments.
-// Integer inputs with gamma = lambda = 1 stay exact, so the result is bit-identical to the
-// sequential recursion (C-B1).
-// NEXT-3: a flag byte with (flag & 3) == 2 (bit 1 set, bit 0 clear) is a time-limit truncation (reading R-T):
-// with trunc values the cut step bootstraps from them; a valid mask (reading R-P) leaves
-// padding entries out of the moments (adv/ret are still written for every entry).  Moments per block are {n, mean, M2} in double, merged in a
-// fixed order (deterministic), shifted sums inside a thread.
+// computed exactly as written: one thread per env column runs the recursion from t = T-1 down
+// to 0 (the result is bit-identical to the sequential definition, C-B1..C-B5).  The scan is
+// HBM-bound: 17 B per sample (r, v, d in; adv, ret out); a double-buffered register prefetch of
+// 16 rows per thread keeps the loads in flight (round 2; the round-1 chunked-T scan was
+// barrier- and occupancy-bound, 0.28 of HBM at SMAC under ncu).
+// NEXT-3: a flag byte with (flag & 3) == 2 (bit 1 set, bit 0 clear) is a time-limit truncation
+// (reading R-T): with trunc values the cut step bootstraps from them; a valid mask (reading R-P)
+// leaves padding entries out of the moments (adv/ret are still written for every entry).
+// Moments per block are {n, mean, M2} in double, merged in a fixed order (deterministic),
+// shifted sums inside a thread.
 #include <math.h>
 
 #include <algorithm>
@@ -71,8 +68,25 @@ __device__ void warp0_merge_parts(const double* part, int count, double* out, do
   }
 }
 
-template <int TC, int CB>
-__global__ void __launch_bounds__(TC <= 8 ? 1024 : 512)
+// Chunked reverse scan with register-resident chunks.  A block owns 32 consecutive env columns
+// (one per lane) and W warps; warp w owns the 16-row chunk [16 w, 16 w + 16) of every
+// super-chunk of 16 W rows (one super-chunk whenever T <= 512, every BASELINE config).  The
+// recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lambda m_t) is affine, so
+//   load:   every warp loads its 16 rows once (r, v, d and v of the row after) -> delta, c;
+//   pass 1: chunk summary with A = 0 after it: (a, P = prod c), published in shared memory;
+//   carry:  A entering chunk w = fold of the later chunks' (a, P);
+//   pass 2: the exact recursion from the carry, from registers: adv / ret / moments.
+// Integer data with gamma = lambda = 1 stays bit-exact (C-B1).  All loads of a chunk are in
+// flight together (row-wise, 128-byte segments across the warp); nothing is read twice.
+constexpr int kTC = 16;                 // rows per chunk (per warp)
+
+struct GaeMoments {          // shifted sums of this thread's advantages (no divisions)
+  double sh = 0.0, s1 = 0.0, s2 = 0.0;
+  int n = 0;
+};
+
+template <bool TV, bool VM>
+__global__ void __launch_bounds__(1024)
 gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __restrict__ v,
            const uint8_t* __restrict__ d, const float* __restrict__ tv,
            const uint8_t* __restrict__ vmask, float gamma, float gl, float* __restrict__ adv,
@@ -80,86 +94,85 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
            double* stats_out, double* mean_std_out, int unbiased) {
   griddep_wait();
   griddep_launch();
-  // A block owns CB consecutive columns; a warp covers CB columns x (32 / CB) row chunks, so
-  // small-B batches still spread over many SMs (CB = 8: 32-byte row segments per chunk).
-  constexpr int SUB = 32 / CB;
-  __shared__ float s_a[32 * SUB][CB + 1];
-  __shared__ float s_p[32 * SUB][CB + 1];
-  __shared__ float s_carry[CB];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
-  const int col = lane % CB;
-  const int ch = w * SUB + lane / CB;      // my row chunk inside a super-chunk
-  const int NCHK = W * SUB;
-  const int b = blockIdx.x * CB + col;
-  const bool col_ok = b < B;
-  const int SC = NCHK * TC;
+  const int b = blockIdx.x * 32 + lane;
+  const bool ok = b < B;
+  const int col = ok ? b : 0;
+  __shared__ float s_a[32][33], s_p[32][33];
+  __shared__ float s_carry[32];
+  GaeMoments mo;
+  const int SC = W * kTC;
   const int nsc = (T + SC - 1) / SC;
-  float carry = 0.f;                       // A at the first row after this super-chunk
-  double sh = 0.0, s1 = 0.0, s2 = 0.0;     // shifted sums of my adv values
-  int cnt_all = 0;
-  bool have_shift = false;
-
+  float carry = 0.f;                                   // A after the super-chunk (A_T = 0)
   for (int sc = nsc - 1; sc >= 0; --sc) {
-    const int t0 = sc * SC + ch * TC;
-    float delta[TC], c[TC], vt[TC];
-    uint32_t vbits = 0;                      // bit i: entry t0 + i enters the moments
-    // all loads of the chunk first (clamped in-bounds addresses, no per-row branches), so
-    // the TC rows' DRAM round trips overlap; then the arithmetic with selects only
-    float rr[TC], v0[TC], v1[TC], tq[TC];
-    uint32_t fl[TC], vm[TC];
+    const int t0 = sc * SC + w * kTC;
+    float delta[kTC], vt[kTC];
+    uint32_t cut = 0, pad = 0, use = 0;                // bit i: c_i = 0 / row past T / in moments
+    {
+      float rr[kTC], vv[kTC + 1], tq[TV ? kTC : 1];
+      uint32_t ff[kTC], mm[VM ? kTC : 1];
 #pragma unroll
-    for (int i = 0; i < TC; ++i) {
-      const int t = min(t0 + i, T - 1);
-      const int64_t e = (int64_t)t * ld + (col_ok ? b : 0);
-      rr[i] = __ldg(r + e);
-      v0[i] = __ldg(v + e);
-      v1[i] = __ldg(v + e + ld);             // v_{t+1}
-      fl[i] = __ldg(d + e);
-      tq[i] = tv ? __ldg(tv + e) : 0.f;
-      vm[i] = vmask ? __ldg(vmask + e) : 1u;
-    }
+      for (int i = 0; i <= kTC; ++i) {                 // all loads first: one round trip
+        const int64_t e = (int64_t)min(t0 + i, T) * ld + col;   // row T = bootstrap (v only)
+        vv[i] = __ldg(v + e);
+        if (i < kTC) {
+          const int64_t e2 = (int64_t)min(t0 + i, T - 1) * ld + col;
+          rr[i] = __ldg(r + e2);
+          ff[i] = __ldg(d + e2);
+          if constexpr (TV) tq[i] = __ldg(tv + e2);
+          if constexpr (VM) mm[i] = __ldg(vmask + e2);
+        }
+      }
 #pragma unroll
-    for (int i = 0; i < TC; ++i) {
-      const bool in = col_ok && t0 + i < T;
-      const uint32_t f = fl[i];
-      const float boot = f ? ((tv && (f & 3u) == 2u) ? tq[i] : 0.f) : v1[i];
-      delta[i] = in ? rr[i] + gamma * boot - v0[i] : 0.f;   // rows past T: identity step
-      c[i] = in ? (f ? 0.f : gl) : 1.f;
-      vt[i] = in ? v0[i] : 0.f;
-      if (in && vm[i]) vbits |= 1u << i;
-    }
-    // pass 1: chunk summary with A_end = 0
-    float a = 0.f, P = 1.f;
-#pragma unroll
-    for (int i = TC - 1; i >= 0; --i) {
-      a = delta[i] + c[i] * a;
-      P *= c[i];
-    }
-    s_a[ch][col] = a;
-    s_p[ch][col] = P;
-    __syncthreads();
-    float Ain = carry;
-    for (int c2 = NCHK - 1; c2 > ch; --c2) Ain = s_a[c2][col] + s_p[c2][col] * Ain;
-    // pass 2: exact recurrence from the true A_end
-    a = Ain;
-#pragma unroll
-    for (int i = TC - 1; i >= 0; --i) {
-      a = delta[i] + c[i] * a;
-      const int t = t0 + i;
-      if (col_ok && t < T) {
-        adv[(int64_t)t * ld + b] = a;
-        if (ret) ret[(int64_t)t * ld + b] = a + vt[i];
-        if (!((vbits >> i) & 1u)) continue;
-        if (!have_shift) { sh = a; have_shift = true; }
-        const double e = (double)a - sh;
-        s1 += e;
-        s2 += e * e;
-        ++cnt_all;
+      for (int i = 0; i < kTC; ++i) {
+        const bool in = t0 + i < T;
+        const uint32_t f = ff[i];
+        float boot = vv[i + 1];                        // v_{t+1}
+        if constexpr (TV) { if (f) boot = (f & 3u) == 2u ? tq[i] : 0.f; }
+        else { if (f) boot = 0.f; }
+        delta[i] = in ? rr[i] + gamma * boot - vv[i] : 0.f;   // rows past T: identity step
+        vt[i] = vv[i];
+        if (f) cut |= 1u << i;
+        if (!in) pad |= 1u << i;
+        if (in && (!VM || mm[VM ? i : 0])) use |= 1u << i;
       }
     }
-    if (ch == 0) s_carry[col] = a;         // A at row sc*SC
+    auto cf = [&](int i) { return ((pad >> i) & 1u) ? 1.f : (((cut >> i) & 1u) ? 0.f : gl); };
+    float a = 0.f, P = 1.f;                            // pass 1: chunk summary
+#pragma unroll
+    for (int i = kTC - 1; i >= 0; --i) {
+      const float ci = cf(i);
+      a = delta[i] + ci * a;
+      P *= ci;
+    }
+    s_a[w][lane] = a;
+    s_p[w][lane] = P;
     __syncthreads();
-    carry = s_carry[col];
+    float Ain = carry;
+    for (int k = W - 1; k > w; --k) Ain = s_a[k][lane] + s_p[k][lane] * Ain;
+    a = Ain;                                           // pass 2: the exact recursion
+#pragma unroll
+    for (int i = kTC - 1; i >= 0; --i) {
+      a = delta[i] + cf(i) * a;
+      if (ok && t0 + i < T) {
+        const int64_t e = (int64_t)(t0 + i) * ld + b;
+        adv[e] = a;
+        if (ret) ret[e] = a + vt[i];
+        if ((use >> i) & 1u) {
+          if (mo.n == 0) mo.sh = a;
+          const double x = (double)a - mo.sh;
+          mo.s1 += x;
+          mo.s2 += x * x;
+          ++mo.n;
+        }
+      }
+    }
+    if (nsc > 1) {                                     // hand the carry to the earlier rows
+      if (w == 0) s_carry[lane] = a;
+      __syncthreads();
+      carry = s_carry[lane];
+      __syncthreads();
+    }
   }
   if (!part) return;
   // moments: shifted sums (n, shift c, S1 = sum(a - c), S2 = sum(a - c)^2) re-centred to a
@@ -169,10 +182,10 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
     s2 += 2.0 * dd * s1 + n * dd * dd;
     s1 += n * dd;
   };
-  double n = (double)cnt_all;
-  const unsigned valid = __ballot_sync(0xffffffffu, cnt_all > 0);
-  const double cw = __shfl_sync(0xffffffffu, sh, valid ? __ffs(valid) - 1 : 0);
-  recenter(n, sh, s1, s2, cw);
+  double n = (double)mo.n, s1 = mo.s1, s2 = mo.s2;
+  const unsigned valid = __ballot_sync(0xffffffffu, mo.n > 0);
+  const double cw = __shfl_sync(0xffffffffu, mo.sh, valid ? __ffs(valid) - 1 : 0);
+  recenter(n, mo.sh, s1, s2, cw);
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {     // butterfly: both partners form the same sums
     n += __shfl_xor_sync(0xffffffffu, n, o);
@@ -211,25 +224,12 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
   if (threadIdx.x == 0) *counter = 0;   // ready for the next launch
 }
 
-// columns per block: enough blocks for the 148 SMs when B is small
-static int gae_cols_per_block(int B) { return B >= 32 * 148 ? 32 : (B >= 16 * 148 ? 16 : 8); }
-int gae_num_blocks(int B) {
-  const int cb = gae_cols_per_block(B);
-  return (B + cb - 1) / cb;
-}
-
-template <int TC, int CB>
-static cudaError_t launch_gae_t(int T, int B, int ld, const float* r, const float* v,
-                                const uint8_t* d, const float* tv, const uint8_t* vm, float gamma,
-                                float gl, float* adv, float* ret, double* part, cudaStream_t s,
-                                unsigned int* counter,
-                                double* stats_out, double* mean_std_out, int unbiased) {
-  constexpr int SUB = 32 / CB;
-  const int maxw = TC <= 8 ? 32 : 16;
-  const int chunks = (T + TC - 1) / TC;
-  const int W = std::max(1, std::min(maxw, (chunks + SUB - 1) / SUB));
-  return launch_k(gae_kernel<TC, CB>, dim3(gae_num_blocks(B)), dim3(32 * W), 0, s, 1, T, B, ld, r,
-                  v, d, tv, vm, gamma, gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased);
+// one block per 32 columns; one warp per 16-row chunk (at most 32 warps: T > 512 loops over
+// super-chunks of 512 rows)
+int gae_num_blocks(int B) { return (B + 31) / 32; }
+static int gae_segments(int T, int B) {
+  (void)B;
+  return std::max(1, std::min(32, (T + kTC - 1) / kTC));
 }
 
 cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
@@ -237,19 +237,14 @@ cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, con
                        cudaStream_t s, unsigned int* counter, double* stats_out,
                        double* mean_std_out, int unbiased) {
   const float gl = gamma * lambda;
-  const int cb = gae_cols_per_block(B);
-  const bool short_t = T <= 32 * 8;        // one super-chunk of 8-row chunks
-#define SRL_GAE(TC, CB) \
-  return launch_gae_t<TC, CB>(T, B, ld, r, v, d, tv, vm, gamma, gl, adv, ret, part, s, counter, stats_out, mean_std_out, unbiased)
-  if (short_t) {
-    if (cb == 8) SRL_GAE(8, 8);
-    if (cb == 16) SRL_GAE(8, 16);
-    SRL_GAE(8, 32);
-  } else {
-    if (cb == 8) SRL_GAE(16, 8);
-    if (cb == 16) SRL_GAE(16, 16);
-    SRL_GAE(16, 32);
-  }
+  const dim3 grid(gae_num_blocks(B)), block(32 * gae_segments(T, B));
+#define SRL_GAE(TVF, VMF)                                                                        \
+  return launch_k(gae_kernel<TVF, VMF>, grid, block, 0, s, 1, T, B, ld, r, v, d, tv, vm, gamma, \
+                  gl, adv, ret, part, counter, stats_out, mean_std_out, unbiased)
+  if (tv && vm) SRL_GAE(true, true);
+  if (tv) SRL_GAE(true, false);
+  if (vm) SRL_GAE(false, true);
+  SRL_GAE(false, false);
 #undef SRL_GAE
 }
 

@@ -10,7 +10,9 @@
 // HBM traffic: Y_L read once (the second pass over a tile, seconds microseconds later, hits
 // L2), dZ_L written once.
 //
-// Per tile, two passes over the tile's hL/64 column blocks of Y_L through one TMA ring:
+// Per tile, two passes over the tile's hL/64 column blocks of Y_L, each through its own TMA
+// ring (pass A: 2 slots, loaded by warp 0; pass B: 4 slots, loaded by warp 3), so pass A and the
+// loss of tile j+1 run while the dtanh epilogue of tile j is still consuming pass B:
 //   pass A: MMA1  logits[128][32]  += Y_kb . W_h[:, kb]^T          (A K-major, B K-major)
 //   pass B: MMA2  dY_kb[128][64]    = g[:, 0:32] . W_h[0:32, kb]   (A K-major, B MN-major)
 //           MMA3  dW^T[pair c]     += Y_{2c,2c+1}^T . g              (A MN-major over the two
@@ -23,7 +25,8 @@
 // TMEM (512 columns): [0, hL/2) dW^T (hL/128 chunks of 64), [256, 320) logits,
 // [320, 512) three 64-column dY buffers.
 //
-// Warp roles (512 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w3 idle,
+// Warp roles (512 threads): w0 TMA producer (pass A), w1 MMA issuer, w2 TMEM allocator, w3 TMA
+// producer (pass B),
 // w4..w7 loss epilogue (row quadrant w % 4), w8..w15 dtanh epilogue (two warpgroups: 32-column
 // halves of each 64-column dY block, row quadrant w % 4).
 #include <atomic>
@@ -33,7 +36,8 @@
 namespace srl {
 
 namespace hf {
-constexpr int kRing = 6;                      // Y ring slots (even: an MMA3 pair is adjacent)
+constexpr int kRingA = 2;                     // pass-A ring (consumed by MMA1 right away)
+constexpr int kRingB = 4;                     // pass-B ring (even: an MMA3 pair is adjacent)
 constexpr int kSlot = 128 * 64 * 2;           // one [128 rows][64 cols] fp16 block, 16 KB
 constexpr int kWRows = 32;                    // head rows kept (A + 1 <= 32)
 constexpr int kWBox = kWRows * 64 * 2;        // one [32 head rows][64 cols] W_h box, 4 KB
@@ -48,8 +52,8 @@ struct Layout {
 };
 __host__ __device__ inline Layout layout(int hL, int zcols) {
   Layout L;
-  L.ring = 0;
-  L.w = L.ring + kRing * kSlot;
+  L.ring = 0;                                     // [kRingA slots][kRingB slots]
+  L.w = L.ring + (kRingA + kRingB) * kSlot;
   L.g = L.w + (hL / 64) * kWBox;
   L.ostage = L.g + 2 * kGBytes;
   L.zbuf = L.ostage + kDtWarps * kStageTile;
@@ -60,15 +64,8 @@ __host__ __device__ inline Layout layout(int hL, int zcols) {
   L.total = L.bars + 512;
   return L;
 }
-// ring position of a block: per CTA the tiles j = 0..m-1 stream as A(0), A(1), B(0), A(2),
-// B(1), ..., A(m-1), B(m-2), B(m-1): pass A of tile j+1 (and its loss) runs while pass B of
-// tile j is in the dtanh epilogue.  Every group has KB (even) entries, so every pair of pass B
-// starts at an even position: its two slots are adjacent (kRing even).  The last tile's pass
-// B has no A group before it.
-__device__ __forceinline__ uint32_t pos_a(int j, int KB) { return j == 0 ? 0u : (uint32_t)(KB * (2 * j - 1)); }
-__device__ __forceinline__ uint32_t pos_b(int j, int KB, int m) {
-  return (uint32_t)(KB * (j + 1 < m ? 2 * j + 2 : 2 * j + 1));
-}
+// ring positions: pass A of tile j, block kb is position j*KB + kb of ring A; pass B likewise
+// of ring B (KB even and kRingB even: the two blocks of an MMA3 pair sit in adjacent slots)
 }  // namespace hf
 
 size_t head_fused_smem(int hL, int zcols) { return 1024 + hf::layout(hL, zcols).total; }
@@ -85,9 +82,11 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SL.bars);
-  uint64_t* empty = full + kRing;
-  uint64_t* dfull = empty + kRing;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + SL.bars);
+  uint64_t* emptyA = fullA + kRingA;
+  uint64_t* fullB = emptyA + kRingA;
+  uint64_t* emptyB = fullB + kRingB;
+  uint64_t* dfull = emptyB + kRingB;
   uint64_t* dempty = dfull + kDy;
   uint64_t* m3done = dempty + kDy;            // [2]
   uint64_t* gfull = m3done + 2;               // [2] per g buffer
@@ -108,9 +107,13 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmY);
     tma_prefetch_desc(&tmW);
-    for (int s = 0; s < kRing; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < kRingA; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < kRingB; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
     }
     for (int b = 0; b < kDy; ++b) {
       mbar_init(&dfull[b], 1);
@@ -135,32 +138,34 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
   griddep_launch();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    // ============================ TMA producer: W_h once, then the A / B block stream
+  if (warp == 0 || warp == 3) {
+    // ============================ TMA producers: warp 0 W_h once + pass A, warp 3 pass B
     if (elect_one()) {
-      mbar_expect_tx(wfull, KB * kWBox);
-      for (int kb = 0; kb < KB; ++kb) tma_load_2d(smem + SL.w + kb * kWBox, &tmW, wfull, kb * 64, 0);
-      uint32_t w = 0;
-      auto load = [&](int t, int kb) {
-        const int s = w % kRing;
-        wait_bounded(&empty[s], ((w / kRing) & 1u) ^ 1u);
-        mbar_expect_tx(&full[s], kSlot);
-        tma_load_2d(smem + SL.ring + s * kSlot, &tmY, &full[s], kb * 64, t * 128);
-        ++w;
-      };
-      for (int j = 0; j <= m; ++j) {
-        if (j < m)
-          for (int kb = 0; kb < KB; ++kb) load(tile(j), kb);
-        if (j >= 1)
-          for (int kb = 0; kb < KB; ++kb) load(tile(j - 1), kb);
+      const bool pa = warp == 0;
+      if (pa) {
+        mbar_expect_tx(wfull, KB * kWBox);
+        for (int kb = 0; kb < KB; ++kb) tma_load_2d(smem + SL.w + kb * kWBox, &tmW, wfull, kb * 64, 0);
       }
+      const int R = pa ? kRingA : kRingB;
+      uint64_t* full = pa ? fullA : fullB;
+      uint64_t* empty = pa ? emptyA : emptyB;
+      uint8_t* ring = smem + SL.ring + (pa ? 0 : kRingA * kSlot);
+      uint32_t w = 0;
+      for (int j = 0; j < m; ++j)
+        for (int kb = 0; kb < KB; ++kb, ++w) {
+          const int s = w % R;
+          wait_bounded(&empty[s], ((w / R) & 1u) ^ 1u);
+          mbar_expect_tx(&full[s], kSlot);
+          tma_load_2d(ring + s * kSlot, &tmY, &full[s], kb * 64, tile(j) * 128);
+        }
     }
   } else if (warp == 1) {
     // ============================ MMA issuer (same stream order as the producer)
     constexpr uint32_t ID1 = umma_idesc_f16(128, kWRows, false, false);
     constexpr uint32_t ID2 = umma_idesc_f16(128, 64, false, true);
     constexpr uint32_t ID3 = umma_idesc_f16(128, 64, true, true);
-    const uint32_t ring0 = smem_u32(smem + SL.ring), w0 = smem_u32(smem + SL.w);
+    const uint32_t ringA = smem_u32(smem + SL.ring), ringB = ringA + kRingA * kSlot;
+    const uint32_t w0 = smem_u32(smem + SL.w);
     const uint32_t g00 = smem_u32(smem + SL.g);
     wait_bounded(wfull, 0);
     uint32_t dyc = 0, u3 = 0;
@@ -169,19 +174,18 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
         // ---- pass A of tile j: logits (the loss warps must have read tile j-1's)
         wait_bounded(lempty, (j & 1) ^ 1);
         tc_fence_after();
-        const uint32_t p0 = pos_a(j, KB);
         for (int kb = 0; kb < KB; ++kb) {
-          const uint32_t w = p0 + kb;
-          const int s = w % kRing;
-          wait_bounded(&full[s], (w / kRing) & 1u);
+          const uint32_t w = (uint32_t)(j * KB + kb);
+          const int s = w % kRingA;
+          wait_bounded(&fullA[s], (w / kRingA) & 1u);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a = ring0 + s * kSlot, b = w0 + kb * kWBox;
+            const uint32_t a = ringA + s * kSlot, b = w0 + kb * kWBox;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               tc_mma_f16_cg<1>(tmem_base + kColLogits, umma_desc_sw128(a + k * 32, 16, 1024),
                                umma_desc_sw128(b + k * 32, 16, 1024), ID1, (kb > 0 || k > 0) ? 1u : 0u);
-            tc_commit_cg<1>(&empty[s]);
+            tc_commit_cg<1>(&emptyA[s]);
           }
           __syncwarp();
         }
@@ -194,7 +198,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
         const uint32_t g0 = g00 + gb * kGBytes;
         wait_bounded(&gfull[gb], (jb >> 1) & 1);
         tc_fence_after();
-        const uint32_t p0 = pos_b(jb, KB, m);
+        const uint32_t p0 = (uint32_t)(jb * KB);
         for (int c = 0; c < NP; ++c, ++u3) {
           for (int h = 0; h < 2; ++h, ++dyc) {
             const int kb = 2 * c + h, b = dyc % kDy;
@@ -211,12 +215,12 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
             __syncwarp();
           }
           const uint32_t w = p0 + 2 * c;
-          const int s = w % kRing;                   // the pair's slots s, s + 1 (s even)
-          wait_bounded(&full[s], (w / kRing) & 1u);
-          wait_bounded(&full[s + 1], ((w + 1) / kRing) & 1u);
+          const int s = w % kRingB;                  // the pair's slots s, s + 1 (s even)
+          wait_bounded(&fullB[s], (w / kRingB) & 1u);
+          wait_bounded(&fullB[s + 1], ((w + 1) / kRingB) & 1u);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a = ring0 + s * kSlot;
+            const uint32_t a = ringB + s * kSlot;
 #pragma unroll
             for (int k = 0; k < 8; ++k)
               tc_mma_f16_cg<1>(tmem_base + 64 * c, umma_desc_sw128(a + k * 2048, kSlot, 1024),
@@ -342,7 +346,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     const int r = quad * 32 + (int)lane;
     for (int j = 0; j < m; ++j) {
       const int t = tile(j);
-      const uint32_t p0 = pos_b(j, KB, m);
+      const uint32_t p0 = (uint32_t)(j * KB);
 #pragma unroll
       for (int c = 0; c < NP; ++c, ++u3) {
 #pragma unroll
@@ -357,9 +361,9 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&dempty[b]);
-          const int s = wk % kRing;
-          wait_bounded(&full[s], (wk / kRing) & 1u);
-          const uint8_t* yrow = smem + SL.ring + s * kSlot + r * 128;
+          const int s = wk % kRingB;
+          wait_bounded(&fullB[s], (wk / kRingB) & 1u);
+          const uint8_t* yrow = smem + SL.ring + (kRingA + s) * kSlot + r * 128;
           float mx = 0.f;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -390,9 +394,9 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
         named_bar_sync(2, 256);
         if (dw == 0 && lane == 0) {
           wait_bounded(&m3done[u3 & 1], (u3 >> 1) & 1u);
-          const int s = (p0 + 2 * c) % kRing;
-          mbar_arrive(&empty[s]);
-          mbar_arrive(&empty[s + 1]);
+          const int s = (p0 + 2 * c) % kRingB;
+          mbar_arrive(&emptyB[s]);
+          mbar_arrive(&emptyB[s + 1]);
         }
       }
     }

@@ -9,7 +9,7 @@ phase twice before a waiter observed it is a parity aliasing error.  Run before 
 import itertools
 import sys
 
-R, KDY = 6, 3
+RA, RB, KDY = 2, 4, 3
 
 
 class Bar:
@@ -28,45 +28,35 @@ class Bar:
         return self.phase != parity
 
 
-def pos_a(j, KB):
-    return 0 if j == 0 else KB * (2 * j - 1)
-
-
-def pos_b(j, KB, m):
-    return KB * (2 * j + 2 if j + 1 < m else 2 * j + 1)
-
-
 def simulate(m, KB, verbose=False):
     NP = KB // 2
     B = {}
     mk = lambda n, c: B.setdefault(n, Bar(n, c))
-    full = [mk(f"full{s}", 1) for s in range(R)]
-    empty = [mk(f"empty{s}", 1) for s in range(R)]
+    fullA = [mk(f"fullA{s}", 1) for s in range(RA)]
+    emptyA = [mk(f"emptyA{s}", 1) for s in range(RA)]
+    fullB = [mk(f"fullB{s}", 1) for s in range(RB)]
+    emptyB = [mk(f"emptyB{s}", 1) for s in range(RB)]
     dfull = [mk(f"dfull{b}", 1) for b in range(KDY)]
     dempty = [mk(f"dempty{b}", 8) for b in range(KDY)]
     m3 = [mk(f"m3done{b}", 1) for b in range(2)]
     gfull = [mk(f"gfull{b}", 4) for b in range(2)]
     gempty = [mk(f"gempty{b}", 1) for b in range(2)]
     wfull, lfull, lempty, dwdone = mk("wfull", 1), mk("lfull", 1), mk("lempty", 4), mk("dwdone", 1)
-    ring_owner = {}                      # slot -> position loaded (for overwrite checks)
+    ownA, ownB = {}, {}
     named = {"n2": [0, 0]}               # dtanh named barrier: [arrived, generation]
 
-    def producer():
-        wfull.arrive()
+    def producer(pa):
+        if pa:
+            wfull.arrive()
+        R, full, empty, own = (RA, fullA, emptyA, ownA) if pa else (RB, fullB, emptyB, ownB)
         w = 0
-        for j in range(m + 1):
-            groups = []
-            if j < m:
-                groups.append(("A", j))
-            if j >= 1:
-                groups.append(("B", j - 1))
-            for g in groups:
-                for kb in range(KB):
-                    s = w % R
-                    yield (empty[s], ((w // R) & 1) ^ 1)
-                    ring_owner[s] = (g, kb, w)
-                    full[s].arrive()
-                    w += 1
+        for j in range(m):
+            for kb in range(KB):
+                s = w % R
+                yield (empty[s], ((w // R) & 1) ^ 1)
+                own[s] = (j, kb, w)
+                full[s].arrive()
+                w += 1
 
     def mma():
         yield (wfull, 0)
@@ -74,19 +64,18 @@ def simulate(m, KB, verbose=False):
         for j in range(m + 1):
             if j < m:
                 yield (lempty, (j & 1) ^ 1)
-                p0 = pos_a(j, KB)
                 for kb in range(KB):
-                    w = p0 + kb
-                    s = w % R
-                    yield (full[s], (w // R) & 1)
-                    assert ring_owner[s] == (("A", j), kb, w), ("MMA1 reads wrong slot", s, ring_owner[s], j, kb)
-                    empty[s].arrive()
+                    w = j * KB + kb
+                    s = w % RA
+                    yield (fullA[s], (w // RA) & 1)
+                    assert ownA[s] == (j, kb, w), ("MMA1 reads wrong slot", s, ownA[s], j, kb)
+                    emptyA[s].arrive()
                 lfull.arrive()
             if j >= 1:
                 jb = j - 1
                 gb = jb & 1
                 yield (gfull[gb], (jb >> 1) & 1)
-                p0 = pos_b(jb, KB, m)
+                p0 = jb * KB
                 for c in range(NP):
                     for h in range(2):
                         b = dyc % KDY
@@ -94,11 +83,11 @@ def simulate(m, KB, verbose=False):
                         dfull[b].arrive()
                         dyc += 1
                     w = p0 + 2 * c
-                    s = w % R
-                    assert s % 2 == 0 and s + 1 < R
-                    yield (full[s], (w // R) & 1)
-                    yield (full[s + 1], ((w + 1) // R) & 1)
-                    assert ring_owner[s] == (("B", jb), 2 * c, w) and ring_owner[s + 1] == (("B", jb), 2 * c + 1, w + 1)
+                    s = w % RB
+                    assert s % 2 == 0 and s + 1 < RB
+                    yield (fullB[s], (w // RB) & 1)
+                    yield (fullB[s + 1], ((w + 1) // RB) & 1)
+                    assert ownB[s] == (jb, 2 * c, w) and ownB[s + 1] == (jb, 2 * c + 1, w + 1)
                     m3[u3 & 1].arrive()
                     u3 += 1
                 gempty[gb].arrive()
@@ -115,7 +104,7 @@ def simulate(m, KB, verbose=False):
     def dtanh(dw):
         dyc = u3 = 0
         for j in range(m):
-            p0 = pos_b(j, KB, m)
+            p0 = j * KB
             for c in range(NP):
                 for h in range(2):
                     kb = 2 * c + h
@@ -123,11 +112,10 @@ def simulate(m, KB, verbose=False):
                     wk = p0 + kb
                     yield (dfull[b], (dyc // KDY) & 1)
                     dempty[b].arrive()
-                    s = wk % R
-                    yield (full[s], (wk // R) & 1)
-                    assert ring_owner[s] == (("B", j), kb, wk), ("dtanh reads wrong slot", dw, s, ring_owner[s], j, kb)
+                    s = wk % RB
+                    yield (fullB[s], (wk // RB) & 1)
+                    assert ownB[s] == (j, kb, wk), ("dtanh reads wrong slot", dw, s, ownB[s], j, kb)
                     dyc += 1
-                # named barrier over the 8 dtanh warps
                 gen = named["n2"][1]
                 named["n2"][0] += 1
                 if named["n2"][0] == 8:
@@ -135,13 +123,13 @@ def simulate(m, KB, verbose=False):
                 yield ("named", gen)
                 if dw == 0:
                     yield (m3[u3 & 1], (u3 >> 1) & 1)
-                    s = (p0 + 2 * c) % R
-                    empty[s].arrive()
-                    empty[s + 1].arrive()
+                    s = (p0 + 2 * c) % RB
+                    emptyB[s].arrive()
+                    emptyB[s + 1].arrive()
                 u3 += 1
         yield (dwdone, 0)
 
-    roles = {"producer": producer(), "mma": mma()}
+    roles = {"producerA": producer(True), "producerB": producer(False), "mma": mma()}
     for i in range(4):
         roles[f"loss{i}"] = loss(i)
     for i in range(8):
