@@ -509,7 +509,8 @@ def main_ours(args, world, rank, local):
     per_step = ours / Kp
     L = len(cfg.hidden)
     updates = max(1, args.epochs) * max(1, args.minibatches)
-    cpu = None if args.no_cpu_baseline else cpu_baselines(cfg, args.cpu_seconds)
+    # the oracle baseline on the host cores: rank 0 at N = 1 only (the contract)
+    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baselines(cfg, args.cpu_seconds)
     clocks = sampler.summary(wall0, wall1) if sampler else None
     out = {
         "metric": METRIC, "value": N * K / (ms_total * 1e-3), "unit": UNIT, "n_gpus": world,
