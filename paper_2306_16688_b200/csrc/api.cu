@@ -184,6 +184,9 @@ struct srl_ctx {
   // rest of the backward computes
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_early = nullptr, ev_late = nullptr, ev_comm = nullptr;
+  // a2's peer exchange on comm_stream during a3 (srl_ppo_train_step): the loss waits on ev_ms
+  cudaEvent_t ev_gae = nullptr, ev_ms = nullptr;
+  bool ms_pending = false;
   double *gae_part = nullptr, *gae_stats = nullptr, *mean_std = nullptr;
   unsigned int* gae_counter = nullptr;
   int gae_part_cap = 0;
@@ -317,7 +320,7 @@ static void free_ctx(srl_ctx* c) {
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
-  for (cudaEvent_t e : {c->ev_early, c->ev_late, c->ev_comm})
+  for (cudaEvent_t e : {c->ev_early, c->ev_late, c->ev_comm, c->ev_gae, c->ev_ms})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -541,7 +544,9 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
     if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_early, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_late, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_gae, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_ms, cudaEventDisableTiming) != cudaSuccess) {
       set_error("srl_ppo_create: stream/event creation failed");
       free_ctx(c);
       return SRL_ECUDA;
@@ -849,6 +854,10 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     g.v_old = vclip ? v_old : nullptr; g.value_clip = c->cfg.value_clip;
     g.valid = valid;
   };
+  if (c->ms_pending) {                                  // mean/std from the a2 exchange
+    CK(cudaStreamWaitEvent(s, c->ev_ms, 0));
+    c->ms_pending = false;
+  }
   if (fused) {
     // a4 + the head's a5 in one kernel: loss, dZ_L, db_L / db_h column sums, dW_h^T partials
     CUtensorMap ty, tw, to;
@@ -1006,8 +1015,10 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   for (int i = 0; i <= HI; ++i)
     part_bytes += 4.0 * splits[i] * c->lay[i].out * c->lay[i].in + 4.0 * colsum_parts[i] * c->lay[i].colsum_ld;
   // the fused finalise -> [grad norm] -> Adam launch (update_kernel)
-  auto update = [&](bool finalize, bool adam, float* bucket) -> srl_status {
+  auto update = [&](bool finalize, bool adam, float* bucket, bool stats) -> srl_status {
     UpdateArgs u{};
+    u.stats = stats; u.apply = apply; u.mean_std = adv_mean_std; u.n_global = n_global;
+    u.cv = c->cfg.value_coef; u.ce = c->cfg.entropy_coef; u.out = stats_out;
     u.t = segs; u.P = c->P; u.inv_n = inv_n; u.bucket = bucket; u.counters = c->counters;
     u.stats_part = c->stats_part; u.nstats = grid_loss;
     u.finalize = finalize; u.adam = adam;
@@ -1025,8 +1036,9 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   if (!overlap) {
     // world 1: ONE launch from the partials to the updated parameters; world > 1: finalise
     // into the bucket the exchange reads, exchange, then the norm + Adam launch
+    // the last launch also writes the step's statistics (its last block)
     const bool one = apply && c->world == 1;
-    if (srl_status st = update(true, one, bk)) return st;
+    if (srl_status st = update(true, one, bk, !apply || c->world == 1)) return st;
     if (apply && c->world > 1) {
       if (p2p) {
         ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8) * 2.0 * (c->world - 1) / c->world);
@@ -1037,7 +1049,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
         ProfScope ps(c, s, "allreduce", 0.0, 4.0 * (c->P + 8));
         CKN(ncclAllReduce(c->grads, c->grads, (size_t)(c->P + 8), ncclFloat, ncclSum, c->comm, s));
       }
-      if (srl_status st = update(false, true, c->grads)) return st;
+      if (srl_status st = update(false, true, c->grads, true)) return st;
     }
   } else {
     // opt-in NCCL overlap path (SRL_AR_OVERLAP=1): layers 1..L were finalised and their
@@ -1064,11 +1076,11 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     CK(launch_adam(segs, c->P, c->params, c->m, c->v, c->grads, c->t_dev, c->cfg.lr,
                    c->cfg.beta1, c->cfg.beta2, c->cfg.adam_eps, s, gclip ? c->gn_coef() : nullptr,
                    c->cc.err_dev));
+    ProfScope ps_stats(c, s, "stats", 0.0, 0.0);
+    CK(launch_stats(c->grads, c->P, adv_mean_std, n_global, c->cfg.value_coef, c->cfg.entropy_coef,
+                    c->t_dev, apply, stats_out, s, c->counters,
+                    gclip ? c->gn_norm() : nullptr, c->world > 1 ? c->cc.err_dev : nullptr));
   }
-  ProfScope ps_stats(c, s, "stats", 0.0, 0.0);
-  CK(launch_stats(c->grads, c->P, adv_mean_std, n_global, c->cfg.value_coef, c->cfg.entropy_coef,
-                  c->t_dev, apply, stats_out, s, c->counters,
-                  gclip ? c->gn_norm() : nullptr, c->world > 1 ? c->cc.err_dev : nullptr));
   return SRL_OK;
 }
 
@@ -1100,11 +1112,21 @@ extern "C" srl_status srl_ppo_train_step(srl_ctx* c, int T, int B, int64_t n_glo
   }
   if (c->world > 1) {
     // a2 (global): all-gather the ranks' {n, mean, M2} and merge them in rank order
-    ProfScope ps(c, s, "adv_norm", 0.0, 24.0 * c->world);
     if (c->p2p && !ar_overlap()) {
-      CK(launch_p2p_moments(c->peers, c->world, c->rank, ++c->mepoch, c->gae_stats, c->mean_std,
-                            c->cfg.adv_unbiased, c->cc, 3, s));
+      // on comm_stream, beside the forward GEMMs (which do not read mean/std): the exchange's
+      // wait for the slowest rank overlaps a3; srl_ppo_step's loss launch waits for ev_ms.
+      // One 256-thread block that co-resides with a GEMM CTA; it spins only on OTHER ranks.
+      CK(cudaEventRecord(c->ev_gae, s));
+      CK(cudaStreamWaitEvent(c->comm_stream, c->ev_gae, 0));
+      {
+        ProfScope ps(c, c->comm_stream, "adv_norm", 0.0, 24.0 * c->world);
+        CK(launch_p2p_moments(c->peers, c->world, c->rank, ++c->mepoch, c->gae_stats, c->mean_std,
+                              c->cfg.adv_unbiased, c->cc, 3, c->comm_stream));
+      }
+      CK(cudaEventRecord(c->ev_ms, c->comm_stream));
+      c->ms_pending = true;
     } else {
+      ProfScope ps(c, s, "adv_norm", 0.0, 24.0 * c->world);
       double* gathered = c->norm_scratch;
       CKN(ncclAllGather(c->gae_stats, gathered, 3, ncclDouble, c->comm, s));
       CK(launch_merge_moments(gathered, c->world, nullptr, c->mean_std, c->cfg.adv_unbiased, s));

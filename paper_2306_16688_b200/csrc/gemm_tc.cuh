@@ -289,6 +289,73 @@ __device__ __forceinline__ void ppo_rows_smem(const GemmArgs& a, float* zb, cons
   st[4] += lp_old - logpi;
 }
 
+// a4 for ONE categorical head (A actions, value at column A; A + 1 <= 32) with the row in
+// registers: z[j] = logit j (bias added) of this lane's row on entry, dloss_i/dz_j on return
+// (0 past A).  The same formulas and per-row operations as ppo_rows_smem (
+// SPEC.md S:L603-611), in the same order (bit-identical g).  act = the row's action (any
+// value if !rvalid).
+__device__ __forceinline__ void ppo_row_regs(const GemmArgs& a, float (&z)[32], int act,
+                                             float Ahat, float lp_old, float R, float vo,
+                                             bool rvalid, double (&st)[5], uint32_t& nonfinite) {
+  const int A = a.A;
+  float V = 0.f, mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (j < A) mx = fmaxf(mx, z[j]);
+    if (j == A) V = z[j];                        // the value column (not a logit)
+  }
+  float se = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < A) se += __expf(z[j] - mx);
+  const float lse = mx + __logf(se);
+  float ent = 0.f, logpi = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float l = z[j] - lse;                  // log-softmax
+    if (j < A) ent -= __expf(l) * l;             // entropy
+    z[j] = l;
+    if (j == act) logpi = l;
+  }
+  const float rho = expf(logpi - lp_old);
+  const float lo = 1.f - a.clip_eps, hi = 1.f + a.clip_eps;
+  const float rc = fminf(fmaxf(rho, lo), hi);
+  const float lpg = -fminf(rho * Ahat, rc * Ahat);
+  const float dv = V - R;
+  float lv = dv * dv;
+  float gv = 2.f * dv;
+  if (a.v_old) {                                 // NEXT-3 value clipping (reading R-V)
+    const float d = V - vo;
+    const float dc = vo + fminf(fmaxf(d, -a.value_clip), a.value_clip) - R;
+    if (dc * dc > lv) {
+      lv = dc * dc;
+      gv = fabsf(d) <= a.value_clip ? 2.f * dc : 0.f;
+    }
+  }
+  const float mask = (Ahat >= 0.f) ? (rho <= hi ? 1.f : 0.f) : (rho >= lo ? 1.f : 0.f);
+  const float pol = -mask * Ahat * rho;
+  const float li = lpg + a.value_coef * lv - a.entropy_coef * ent;
+  const bool ok = rvalid && isfinite(li);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float l = z[j];
+    const float p = __expf(l);
+    const float g = pol * ((j == act ? 1.f : 0.f) - p) + a.entropy_coef * p * (l + ent);
+    z[j] = (ok && j < A) ? g : 0.f;
+    if (j == A) z[j] = ok ? a.value_coef * gv : 0.f;
+  }
+  if (!rvalid) return;
+  if (!ok) {
+    ++nonfinite;
+    return;
+  }
+  st[0] += lpg;
+  st[1] += lv;
+  st[2] += ent;
+  st[3] += fabsf(rho - 1.f) > a.clip_eps ? 1.0 : 0.0;
+  st[4] += lp_old - logpi;
+}
+
 // NEXT-2 (DESIGN.md §3.6 reading R-S): SplitMix64 finaliser of x + golden gamma; the uniform
 // of (seed, key, head) is the top 24 bits of sm64(sm64(seed ^ key) + head), exact in fp32.
 __device__ __forceinline__ unsigned long long sm64(unsigned long long x) {

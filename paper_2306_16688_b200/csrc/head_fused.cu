@@ -11,7 +11,7 @@
 // L2), dZ_L written once.
 //
 // Per tile, two passes over the tile's hL/64 column blocks of Y_L, each through its own TMA
-// ring (pass A: 2 slots, loaded by warp 0; pass B: 4 slots, loaded by warp 3), so pass A and the
+// ring (pass A: 3 slots, loaded by warp 0; pass B: 4 slots, loaded by warp 3), so pass A and the
 // loss of tile j+1 run while the dtanh epilogue of tile j is still consuming pass B:
 //   pass A: MMA1  logits[128][32]  += Y_kb . W_h[:, kb]^T          (A K-major, B K-major)
 //   pass B: MMA2  dY_kb[128][64]    = g[:, 0:32] . W_h[0:32, kb]   (A K-major, B MN-major)
@@ -35,8 +35,21 @@
 
 namespace srl {
 
+#ifdef SRL_HF_TRACE
+// tools/hf_trace.py: per-CTA cycle counters of the waits of each role (variant builds only)
+__device__ unsigned long long g_hf_trace[256 * 16];
+#define HF_WAIT(bar, par, k)                                   \
+  do {                                                         \
+    const long long _t0 = clock64();                           \
+    wait_bounded(bar, par);                                    \
+    trc[k] += (unsigned long long)(clock64() - _t0);           \
+  } while (0)
+#else
+#define HF_WAIT(bar, par, k) wait_bounded(bar, par)
+#endif
+
 namespace hf {
-constexpr int kRingA = 2;                     // pass-A ring (consumed by MMA1 right away)
+constexpr int kRingA = 3;                     // pass-A ring (consumed by MMA1 as it lands)
 constexpr int kRingB = 4;                     // pass-B ring (even: an MMA3 pair is adjacent)
 constexpr int kSlot = 128 * 64 * 2;           // one [128 rows][64 cols] fp16 block, 16 KB
 constexpr int kWRows = 32;                    // head rows kept (A + 1 <= 32)
@@ -137,6 +150,10 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
   griddep_wait();                    // Y_L and the parameters come from earlier kernels
   griddep_launch();
   const uint32_t tmem_base = *tmem_slot;
+#ifdef SRL_HF_TRACE
+  unsigned long long trc[16] = {};
+  const long long t_start = clock64();
+#endif
 
   if (warp == 0 || warp == 3) {
     // ============================ TMA producers: warp 0 W_h once + pass A, warp 3 pass B
@@ -154,7 +171,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
       for (int j = 0; j < m; ++j)
         for (int kb = 0; kb < KB; ++kb, ++w) {
           const int s = w % R;
-          wait_bounded(&empty[s], ((w / R) & 1u) ^ 1u);
+          HF_WAIT(&empty[s], ((w / R) & 1u) ^ 1u, pa ? 1 : 2);
           mbar_expect_tx(&full[s], kSlot);
           tma_load_2d(ring + s * kSlot, &tmY, &full[s], kb * 64, tile(j) * 128);
         }
@@ -168,59 +185,52 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     const uint32_t w0 = smem_u32(smem + SL.w);
     const uint32_t g00 = smem_u32(smem + SL.g);
     wait_bounded(wfull, 0);
+    // Two cursors, each issued as soon as its barriers allow, pass B first (the dtanh warps
+    // are the long pole): a pass-A block whose TMA load is still in flight never holds back
+    // the dY blocks / dW^T pairs of the previous tile.  Pass B of tile jb needs its g, so it
+    // runs behind pass A (jb < ja).  Barrier tests are non-blocking (lane 0, broadcast).
+    auto ready = [&](uint64_t* bar, uint32_t par) -> bool {
+      const uint32_t r = lane == 0 ? (uint32_t)mbar_test(bar, par) : 0u;
+      return __shfl_sync(0xffffffffu, r, 0) != 0u;
+    };
+    int ja = 0, ka = 0;                    // pass A: tile, block
+    int jb = 0, qb = 0;                    // pass B: tile, sub-step (per pair: dY h=0, h=1, dW^T)
+    bool l_ok = false, g_ok = false;       // lempty seen for tile ja / gfull seen for tile jb
     uint32_t dyc = 0, u3 = 0;
-    for (int j = 0; j <= m; ++j) {
-      if (j < m) {
-        // ---- pass A of tile j: logits (the loss warps must have read tile j-1's)
-        wait_bounded(lempty, (j & 1) ^ 1);
-        tc_fence_after();
-        for (int kb = 0; kb < KB; ++kb) {
-          const uint32_t w = (uint32_t)(j * KB + kb);
-          const int s = w % kRingA;
-          wait_bounded(&fullA[s], (w / kRingA) & 1u);
+    long long idle0 = clock64();
+    while (ja < m || jb < m) {
+      bool did = false;
+      // ---- pass B of tile jb: dY blocks and the dW^T pairs
+      while (jb < ja) {
+        const int gb = jb & 1;
+        if (!g_ok) {
+          if (!ready(&gfull[gb], (jb >> 1) & 1)) break;
+          g_ok = true;
+        }
+        const uint32_t g0 = g00 + gb * kGBytes;
+        const int c = qb / 3, h = qb % 3;
+        if (h < 2) {
+          const int kb = 2 * c + h, bf = dyc % kDy;
+          if (!ready(&dempty[bf], ((dyc / kDy) & 1u) ^ 1u)) break;
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a = ringA + s * kSlot, b = w0 + kb * kWBox;
+            const uint32_t wb = w0 + kb * kWBox;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc_mma_f16_cg<1>(tmem_base + kColLogits, umma_desc_sw128(a + k * 32, 16, 1024),
-                               umma_desc_sw128(b + k * 32, 16, 1024), ID1, (kb > 0 || k > 0) ? 1u : 0u);
-            tc_commit_cg<1>(&emptyA[s]);
+            for (int k = 0; k < kWRows / 16; ++k)      // K = the 32 real head columns of g
+              tc_mma_f16_cg<1>(tmem_base + kColDy + 64 * bf, umma_desc_sw128(g0 + k * 32, 16, 1024),
+                               umma_desc_sw128(wb + k * 2048, 8192, 1024), ID2, k > 0 ? 1u : 0u);
+            tc_commit_cg<1>(&dfull[bf]);
           }
           __syncwarp();
-        }
-        if (lane == 0) tc_commit_cg<1>(lfull);
-        __syncwarp();
-      }
-      if (j >= 1) {
-        // ---- pass B of tile jb = j-1: dY blocks and the dW^T pairs (needs its g)
-        const int jb = j - 1, gb = jb & 1;
-        const uint32_t g0 = g00 + gb * kGBytes;
-        wait_bounded(&gfull[gb], (jb >> 1) & 1);
-        tc_fence_after();
-        const uint32_t p0 = (uint32_t)(jb * KB);
-        for (int c = 0; c < NP; ++c, ++u3) {
-          for (int h = 0; h < 2; ++h, ++dyc) {
-            const int kb = 2 * c + h, b = dyc % kDy;
-            wait_bounded(&dempty[b], ((dyc / kDy) & 1u) ^ 1u);
-            tc_fence_after();
-            if (lane == 0) {
-              const uint32_t wb = w0 + kb * kWBox;
-#pragma unroll
-              for (int k = 0; k < kWRows / 16; ++k)      // K = the 32 real head columns of g
-                tc_mma_f16_cg<1>(tmem_base + kColDy + 64 * b, umma_desc_sw128(g0 + k * 32, 16, 1024),
-                                 umma_desc_sw128(wb + k * 2048, 8192, 1024), ID2, k > 0 ? 1u : 0u);
-              tc_commit_cg<1>(&dfull[b]);
-            }
-            __syncwarp();
-          }
-          const uint32_t w = p0 + 2 * c;
-          const int s = w % kRingB;                  // the pair's slots s, s + 1 (s even)
-          wait_bounded(&fullB[s], (w / kRingB) & 1u);
-          wait_bounded(&fullB[s + 1], ((w + 1) / kRingB) & 1u);
+          ++dyc;
+        } else {
+          const uint32_t w = (uint32_t)(jb * KB + 2 * c);
+          const int sb = w % kRingB;                 // the pair's slots sb, sb + 1 (sb even)
+          if (!ready(&fullB[sb], (w / kRingB) & 1u) || !ready(&fullB[sb + 1], ((w + 1) / kRingB) & 1u))
+            break;
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a = ringB + s * kSlot;
+            const uint32_t a = ringB + sb * kSlot;
 #pragma unroll
             for (int k = 0; k < 8; ++k)
               tc_mma_f16_cg<1>(tmem_base + 64 * c, umma_desc_sw128(a + k * 2048, kSlot, 1024),
@@ -229,9 +239,50 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
             tc_commit_cg<1>(&m3done[u3 & 1]);
           }
           __syncwarp();
+          ++u3;
         }
-        if (lane == 0) tc_commit_cg<1>(&gempty[gb]);   // g buffer gb free once these complete
-        __syncwarp();
+        did = true;
+        if (++qb == 3 * NP) {
+          if (lane == 0) tc_commit_cg<1>(&gempty[gb]);   // g buffer gb free once these complete
+          __syncwarp();
+          ++jb;
+          qb = 0;
+          g_ok = false;
+        }
+      }
+      // ---- pass A of tile ja: one logits block (the loss warps must have read tile ja-1's)
+      if (ja < m) {
+        if (!l_ok && ka == 0 && ready(lempty, (ja & 1) ^ 1)) l_ok = true;
+        const uint32_t w = (uint32_t)(ja * KB + ka);
+        const int sa = w % kRingA;
+        if (l_ok && ready(&fullA[sa], (w / kRingA) & 1u)) {
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a = ringA + sa * kSlot, b = w0 + ka * kWBox;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16_cg<1>(tmem_base + kColLogits, umma_desc_sw128(a + k * 32, 16, 1024),
+                               umma_desc_sw128(b + k * 32, 16, 1024), ID1, (ka > 0 || k > 0) ? 1u : 0u);
+            tc_commit_cg<1>(&emptyA[sa]);
+            if (ka == KB - 1) tc_commit_cg<1>(lfull);
+          }
+          __syncwarp();
+          did = true;
+          if (++ka == KB) {
+            ++ja;
+            ka = 0;
+            l_ok = false;
+          }
+        }
+      }
+      if (did) {
+        idle0 = clock64();
+      } else {
+        __nanosleep(32);
+        if (clock64() - idle0 > (1ll << 35)) __trap();   // a lost arrival (kernel bug)
+#ifdef SRL_HF_TRACE
+        trc[4] += 1;
+#endif
       }
     }
     if (lane == 0) tc_commit_cg<1>(dwdone);
@@ -246,6 +297,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     named_bar_sync(3, 128);
     uint32_t nsat = 0, nonfinite = 0;
     double st[5] = {0, 0, 0, 0, 0};
+    const bool single = args.n_heads == 1;          // the register path (ppo_row_regs)
     for (int j = 0; j < m; ++j) {
       const int t = tile(j);
       const int r = quad * 32 + (int)lane;          // row in the tile
@@ -261,24 +313,50 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
         R = __ldg(args.ret + row);
         if (args.v_old) vo = __ldg(args.v_old + row);
       }
-      wait_bounded(lfull, j & 1);
+      const int act0 = (lvalid && single) ? __ldg(arow) : 0;
+      HF_WAIT(lfull, j & 1, j == 0 ? 3 : 8);
       tc_fence_after();
-      {
-        float z[32];                                 // the A + 1 <= 32 head outputs
-        const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + kColLogits;
-        tmem_ld32(ta, z);
-        tc_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(lempty);         // MMA1 of the next tile may overwrite
+      float z[32];                                   // the A + 1 <= 32 head outputs
+      tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + kColLogits, z);
+      tc_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(lempty);           // MMA1 of the next tile may overwrite
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj)
-          if (jj <= args.A) zb[jj * kZPitch + lane] = z[jj] + bias_s[jj];
-      }
+      for (int jj = 0; jj < 32; ++jj) z[jj] += bias_s[jj];   // 0 past A
       if (args.mean_std) {
         const double mu = args.mean_std[0], sd = args.mean_std[1];
         Ahat = (float)(((double)Ahat - mu) / (sd + (double)args.adv_eps));
       }
+      const int gb = j & 1;
+      uint8_t* gtile = smem + SL.g + gb * kGBytes;
+      if (single) {
+        // one categorical head: the row stays in registers
+        ppo_row_regs(args, z, act0, Ahat, lp, R, vo, lvalid, st, nonfinite);
+        HF_WAIT(&gempty[gb], ((j >> 1) & 1) ^ 1, 9);   // tile j-2's MMA2 / MMA3 are done
+#pragma unroll
+        for (int j8 = 0; j8 < 8; ++j8) {
+          uint4 u = make_uint4(0u, 0u, 0u, 0u);
+          if (j8 < 4) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = sat_f16(z[8 * j8 + e], nsat);
+            u.x = pack_half2(v[0], v[1]);
+            u.y = pack_half2(v[2], v[3]);
+            u.z = pack_half2(v[4], v[5]);
+            u.w = pack_half2(v[6], v[7]);
+          }
+          *reinterpret_cast<uint4*>(gtile + r * 128 + ((j8 ^ (r & 7)) << 4)) = u;
+        }
+        fence_proxy_async_smem();                    // generic writes -> tcgen05 (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&gfull[gb]);
+        my_cs[lane] += transpose_reduce32(z);        // db_h partials: column lane, 32 rows
+        continue;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj)
+        if (jj <= args.A) zb[jj * kZPitch + lane] = z[jj];
       ppo_rows_smem(args, zb, arow, Ahat, lp, R, vo, lvalid, st, nonfinite);
       __syncwarp();
       for (int jj = lane; jj <= args.A; jj += 32) {  // db_h partials: column jj over 32 rows
@@ -288,9 +366,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
         my_cs[jj] += cs;
       }
       // g row -> fp16 g buffer j % 2 (128-byte rows, 16-byte chunks swizzled by row % 8)
-      const int gb = j & 1;
-      uint8_t* gtile = smem + SL.g + gb * kGBytes;
-      wait_bounded(&gempty[gb], ((j >> 1) & 1) ^ 1);   // tile j-2's MMA2 / MMA3 are done
+      HF_WAIT(&gempty[gb], ((j >> 1) & 1) ^ 1, 9);   // tile j-2's MMA2 / MMA3 are done
 #pragma unroll
       for (int j8 = 0; j8 < 8; ++j8) {
         float v[8];
@@ -310,6 +386,9 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
       __syncwarp();
       if (lane == 0) mbar_arrive(&gfull[gb]);
     }
+#ifdef SRL_HF_TRACE
+    trc[10] = (unsigned long long)(clock64() - t_start);
+#endif
     if (args.counters) {
       count_warp(args.counters + 1, nsat);
       count_warp(args.counters + 0, nonfinite);
@@ -347,13 +426,14 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     for (int j = 0; j < m; ++j) {
       const int t = tile(j);
       const uint32_t p0 = (uint32_t)(j * KB);
-#pragma unroll
+#pragma unroll 1                     // one copy of the body: the unrolled loop (8 copies
+                                     // at hL = 512) missed in the instruction cache
       for (int c = 0; c < NP; ++c, ++u3) {
-#pragma unroll
+#pragma unroll 1
         for (int h = 0; h < 2; ++h, ++dyc) {
           const int kb = 2 * c + h, b = dyc % kDy;
           const uint32_t wk = p0 + kb;
-          wait_bounded(&dfull[b], (dyc / kDy) & 1u);
+          HF_WAIT(&dfull[b], (dyc / kDy) & 1u, dyc == 0 ? 5 : 11);
           tc_fence_after();
           float v[32];
           tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + kColDy + 64 * b + 32 * grp, v);
@@ -362,7 +442,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
           __syncwarp();
           if (lane == 0) mbar_arrive(&dempty[b]);
           const int s = wk % kRingB;
-          wait_bounded(&fullB[s], (wk / kRingB) & 1u);
+          HF_WAIT(&fullB[s], (wk / kRingB) & 1u, 12);
           const uint8_t* yrow = smem + SL.ring + (kRingA + s) * kSlot + r * 128;
           float mx = 0.f;
 #pragma unroll
@@ -384,14 +464,26 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) v[jj] = sat_f16(v[jj], nsat);
           }
+#ifdef SRL_HF_TRACE
+          const long long ta0 = clock64();
+#endif
           uint8_t* tl = ost.acquire();
+#ifdef SRL_HF_TRACE
+          trc[14] += (unsigned long long)(clock64() - ta0);
+#endif
           stile_write_row(tl, (int)lane, v);
           ost.release(tl, &tmO, kb * 64 + 32 * grp, t * 128 + quad * 32);
           my_cs[kb * 32 + lane] += transpose_reduce32(v);   // db_L: fp32 column sums
         }
         // both blocks of the pair read by all 8 dtanh warps: once MMA3 of the pair is done too,
         // the two ring slots go back to the producer
+#ifdef SRL_HF_TRACE
+        const long long tb0 = clock64();
+#endif
         named_bar_sync(2, 256);
+#ifdef SRL_HF_TRACE
+        trc[13] += (unsigned long long)(clock64() - tb0);
+#endif
         if (dw == 0 && lane == 0) {
           wait_bounded(&m3done[u3 & 1], (u3 >> 1) & 1u);
           const int s = (p0 + 2 * c) % kRingB;
@@ -400,6 +492,9 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
         }
       }
     }
+#ifdef SRL_HF_TRACE
+    trc[15] = (unsigned long long)(clock64() - t_start);
+#endif
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
     if (args.counters) count_warp(args.counters + 1, nsat);
@@ -430,6 +525,14 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
       }
     }
   }
+#ifdef SRL_HF_TRACE
+  // slot 0: kernel cycles (MMA warp); 10 / 15: loss / dtanh warp cycles to the end of its loop
+  if (warp == 1) trc[0] = (unsigned long long)(clock64() - t_start);
+  if (warp == 0 || warp == 1 || warp == 3 || warp == 4 || warp == 8)
+    for (int k = 0; k < 16; ++k)
+      if (trc[k] && (lane == 0 || warp == 0 || warp == 3))   // producers: the elected lane
+        atomicAdd(&g_hf_trace[blockIdx.x * 16 + k], trc[k]);
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -473,3 +576,12 @@ cudaError_t launch_head_fused(const CUtensorMap& tmY, const CUtensorMap& tmW, co
 }
 
 }  // namespace srl
+
+#ifdef SRL_HF_TRACE
+// tools/hf_trace.py: copy out and clear the per-CTA counters [256][16]
+extern "C" int srl_debug_hf_trace(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, srl::g_hf_trace, sizeof(srl::g_hf_trace)) != cudaSuccess) return 1;
+  static unsigned long long zero[256 * 16];
+  return cudaMemcpyToSymbol(srl::g_hf_trace, zero, sizeof(zero)) != cudaSuccess;
+}
+#endif

@@ -9,6 +9,7 @@
 #include <utility>
 
 #include "gemm_tc.cuh"
+#include "srl.h"
 
 namespace srl {
 
@@ -123,7 +124,8 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
 constexpr int kGradNormBlocks = 296;   // 2 x 148 SMs
 // a5 tail + a7 in one persistent launch (misc.cu update_kernel): finalise (if `finalize`) the
 // partials into `bucket` with the loss statistics, then (if `adam`) the optional global-norm
-// clip and Adam + fp16 shadow reading `g` (== bucket at world 1, the reduced bucket otherwise)
+// clip and Adam + fp16 shadow reading `g` (== bucket at world 1, the reduced bucket otherwise),
+// then (if `stats`) the step's statistics
 struct UpdateArgs {
   SegTable t;
   int64_t P, items, witems, nbias;
@@ -135,13 +137,20 @@ struct UpdateArgs {
   int finalize, adam;
   const float* g;
   float *p, *m, *v;
-  const int64_t* t_dev;
+  int64_t* t_dev;
   float lr, b1, b2, eps, max_norm;
   double* gn_part;          // [>= #SMs]
   double* gn_norm;
   float* gn_coef;
   const int* comm_err;
-  unsigned* bar;            // grid barrier words [2], zero-initialised
+  unsigned* bar;            // grid barrier words [3], zero-initialised ([2]: blocks done)
+  // the step's last launch (`stats`): its last block writes srl_ppo_stats from g[P..P+8),
+  // advances t if Adam ran, re-zeroes the counters (what stats_kernel does standalone)
+  int stats, apply;
+  const double* mean_std;
+  int64_t n_global;
+  float cv, ce;
+  srl_ppo_stats* out;
 };
 cudaError_t launch_update(UpdateArgs u, cudaStream_t s);
 // a6 over NVLink peer memory (world <= 8 on one node): every rank's exposed bucket (double

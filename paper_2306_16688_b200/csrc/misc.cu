@@ -252,18 +252,23 @@ __device__ __forceinline__ float adam_one(float& p, float& m, float& v, float g,
   return p;
 }
 
-// Adam over segment s for quads q = q0, q0 + qstride, ...; step = t + 1 (bias corrections)
+// PyTorch's bias corrections for step = t + 1: {lr / (1 - b1^step), sqrt(1 - b2^step)}, in
+// double like torch.optim.Adam; computed once per block (two pow() calls)
+__device__ __forceinline__ float2 adam_bias_corr(float lr, float b1, float b2, double step) {
+  const float bc1 = (float)(1.0 - pow((double)b1, step));
+  const float bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, step));
+  return make_float2(lr / bc1, bc2_sqrt);
+}
+
+// Adam over segment s for quads q = q0, q0 + qstride, ... with the step's bias corrections
 __device__ __forceinline__ void adam_seg_body(const Segment& s, float* __restrict__ p,
                                               float* __restrict__ m, float* __restrict__ v,
-                                              const float* __restrict__ g, double step, float lr,
-                                              float b1, float b2, float eps, float cf, int64_t q0,
-                                              int64_t qstride) {
+                                              const float* __restrict__ g, float step_size,
+                                              float bc2_sqrt, float b1, float b2, float eps,
+                                              float cf, int64_t q0, int64_t qstride) {
   const int cnt = s.rows * s.cols;
   const int64_t nq = (cnt + 3) >> 2;
   if (q0 >= nq) return;
-  const float bc1 = (float)(1.0 - pow((double)b1, step));
-  const float bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, step));
-  const float step_size = lr / bc1;
   const bool vec_w16 = !s.is_bias && (s.cols & 3) == 0 && (s.w16_ld & 3) == 0;
   // float4 only where the segment starts 16-byte aligned (every segment of the shared layout;
   // the separate-trunk layout (R-AC) puts the critic after b_pi[A], A arbitrary)
@@ -329,7 +334,8 @@ __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
   griddep_launch();
   if (g[P + 5] > 0.f || (comm_err && *comm_err)) return;
   const float cf = coef ? *coef : 1.f;           // NEXT-3 global-norm clip coefficient
-  adam_seg_body(t.s[blockIdx.y], p, m, v, g, (double)(t_dev[0] + 1), lr, b1, b2, eps, cf,
+  const float2 bc = adam_bias_corr(lr, b1, b2, (double)(t_dev[0] + 1));
+  adam_seg_body(t.s[blockIdx.y], p, m, v, g, bc.x, bc.y, b1, b2, eps, cf,
                 blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
@@ -353,6 +359,10 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
 // The block partials of the norm are summed in block order: deterministic.
 // The blocks call griddepcontrol.launch_dependents first, so the next grid (PDL) can only
 // start once every block of this one is resident: the spin barrier cannot starve.
+__device__ void write_stats(const float* ex, const double* mean_std, int64_t n_global, float cv,
+                            float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
+                            unsigned long long* counters, const double* gnorm, int cerr);
+
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -371,36 +381,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
-  griddep_launch();
-  griddep_wait();
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double step = (double)(u.t_dev[0] + 1);   // read before anyone can advance it
-  __shared__ double red[16];
-  if (u.finalize) {
-    uint32_t bad = finalize_w_body(u.t, u.items, u.inv_n, u.bucket, tid, nthr);
-    const int64_t gw = tid >> 5, nw = nthr >> 5;
-    bad += finalize_w_warp_body(u.t, u.witems, u.inv_n, u.bucket, gw, nw) * (lane == 0);
-    for (int64_t e = gw; e < u.nbias; e += nw) bad += finalize_b_one(u.t, (int)e, u.inv_n, u.bucket) && lane == 0;
-    const uint32_t tot = __reduce_add_sync(0xffffffffu, bad);
-    if (lane == 0 && tot) atomicAdd(u.counters, (unsigned long long)tot);
-    if (blockIdx.x == 0 && warp < 5) {             // loss statistics / N
-      double x = 0.0;
-      for (int g = lane; g < u.nstats; g += 32) x += u.stats_part[(int64_t)g * 8 + warp];
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) u.bucket[u.P + warp] = (float)(x * (double)u.inv_n);
-    }
-    grid_barrier(u.bar);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      u.bucket[u.P + 5] = (float)u.counters[0];
-      u.bucket[u.P + 6] = (float)u.counters[1];
-      u.bucket[u.P + 7] = 0.f;
-    }
-  }
-  if (!u.adam) return;
+__device__ __forceinline__ void update_adam(const UpdateArgs& u, float2& bc, double* red,
+                                            int64_t tid, int64_t nthr, int warp, int lane) {
   const float* g = u.g;
   const bool skip = (u.finalize ? (*reinterpret_cast<volatile unsigned long long*>(u.counters) > 0)
                                 : (g[u.P + 5] > 0.f)) || (u.comm_err && *u.comm_err);
@@ -435,9 +417,60 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
       *u.gn_coef = cf;
     }
   }
+  __syncthreads();                                 // bc
   if (skip) return;
+  const float2 b = bc;
   for (int i = 0; i < u.t.n; ++i)
-    adam_seg_body(u.t.s[i], u.p, u.m, u.v, g, step, u.lr, u.b1, u.b2, u.eps, cf, tid, nthr);
+    adam_seg_body(u.t.s[i], u.p, u.m, u.v, g, b.x, b.y, u.b1, u.b2, u.eps, cf, tid, nthr);
+}
+
+__global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
+  griddep_launch();
+  griddep_wait();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double red[16];
+  __shared__ float2 bc;                            // Adam bias corrections of step t + 1
+  if (u.adam && threadIdx.x == 0)                  // t read before the last block advances it
+    bc = adam_bias_corr(u.lr, u.b1, u.b2, (double)(u.t_dev[0] + 1));
+  if (u.finalize) {
+    uint32_t bad = finalize_w_body(u.t, u.items, u.inv_n, u.bucket, tid, nthr);
+    const int64_t gw = tid >> 5, nw = nthr >> 5;
+    bad += finalize_w_warp_body(u.t, u.witems, u.inv_n, u.bucket, gw, nw) * (lane == 0);
+    for (int64_t e = gw; e < u.nbias; e += nw) bad += finalize_b_one(u.t, (int)e, u.inv_n, u.bucket) && lane == 0;
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, bad);
+    if (lane == 0 && tot) atomicAdd(u.counters, (unsigned long long)tot);
+    if (blockIdx.x == 0 && warp < 5) {             // loss statistics / N
+      double x = 0.0;
+      for (int g = lane; g < u.nstats; g += 32) x += u.stats_part[(int64_t)g * 8 + warp];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) u.bucket[u.P + warp] = (float)(x * (double)u.inv_n);
+    }
+    grid_barrier(u.bar);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      u.bucket[u.P + 5] = (float)u.counters[0];
+      u.bucket[u.P + 6] = (float)u.counters[1];
+      u.bucket[u.P + 7] = 0.f;
+    }
+  }
+  if (u.adam) update_adam(u, bc, red, tid, nthr, warp, lane);
+  if (u.stats) {
+    // the step's statistics by the LAST block to get here: every block has read t and the
+    // counters by then, and block 0's extras / norm writes precede its arrival
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(u.bar + 2, 1u) == gridDim.x - 1) {
+        __threadfence();
+        u.bar[2] = 0;
+        write_stats(u.g + u.P, u.mean_std, u.n_global, u.cv, u.ce, u.t_dev, u.apply, u.out,
+                    u.counters, u.max_norm > 0.f ? u.gn_norm : nullptr,
+                    u.comm_err ? *(volatile const int*)u.comm_err : 0);
+      }
+    }
+  }
 }
 
 cudaError_t launch_update(UpdateArgs u, cudaStream_t s) {
@@ -627,6 +660,32 @@ cudaError_t launch_shadow(const SegTable& t, const float* p, cudaStream_t s) {
   return launch_k(shadow_kernel, dim3(2 * num_sms()), dim3(256), 0, s, 1, t, p);
 }
 
+// the step's srl_ppo_stats from the (reduced) bucket extras, the policy version advance
+// (Code 1 inc_version) and the counter reset for the next step; ONE thread
+__device__ void write_stats(const float* ex, const double* mean_std, int64_t n_global, float cv,
+                            float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
+                            unsigned long long* counters, const double* gnorm, int cerr) {
+  const float e5 = __ldcg(ex + 5);
+  if (counters) { counters[0] = 0; counters[1] = 0; }   // ready for the next step
+  if (apply && e5 == 0.f && !cerr) t_dev[0] += 1;       // policy version (Code 1 inc_version)
+  if (!out) return;
+  const float e0 = __ldcg(ex), e1 = __ldcg(ex + 1), e2 = __ldcg(ex + 2);
+  out->policy_loss = e0;
+  out->value_loss = e1;
+  out->entropy = e2;
+  out->clip_fraction = __ldcg(ex + 3);
+  out->approx_kl = __ldcg(ex + 4);
+  out->loss = (double)e0 + (double)cv * e1 - (double)ce * e2;
+  out->adv_mean = mean_std ? __ldcg(mean_std) : 0.0;
+  out->adv_std = mean_std ? __ldcg(mean_std + 1) : 1.0;
+  out->n_global = n_global;
+  out->nonfinite = (int64_t)e5;
+  out->fp16_saturated = (int64_t)__ldcg(ex + 6);
+  out->step = t_dev[0];
+  out->grad_norm = gnorm ? __ldcg(gnorm) : 0.0;
+  out->comm_error = cerr;
+}
+
 __global__ void stats_kernel(const float* __restrict__ bucket, int64_t P,
                              const double* __restrict__ mean_std, int64_t n_global, float cv,
                              float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
@@ -634,25 +693,8 @@ __global__ void stats_kernel(const float* __restrict__ bucket, int64_t P,
                              const int* comm_err) {
   griddep_wait();
   griddep_launch();
-  const float* ex = bucket + P;
-  const int cerr = comm_err ? *comm_err : 0;
-  if (counters) { counters[0] = 0; counters[1] = 0; }   // ready for the next step
-  if (apply && ex[5] == 0.f && !cerr) t_dev[0] += 1;   // policy version (Code 1 inc_version)
-  if (!out) return;
-  out->policy_loss = ex[0];
-  out->value_loss = ex[1];
-  out->entropy = ex[2];
-  out->clip_fraction = ex[3];
-  out->approx_kl = ex[4];
-  out->loss = (double)ex[0] + (double)cv * ex[1] - (double)ce * ex[2];
-  out->adv_mean = mean_std ? mean_std[0] : 0.0;
-  out->adv_std = mean_std ? mean_std[1] : 1.0;
-  out->n_global = n_global;
-  out->nonfinite = (int64_t)ex[5];
-  out->fp16_saturated = (int64_t)ex[6];
-  out->step = t_dev[0];
-  out->grad_norm = gnorm ? *gnorm : 0.0;
-  out->comm_error = cerr;
+  write_stats(bucket + P, mean_std, n_global, cv, ce, t_dev, apply, out, counters, gnorm,
+              comm_err ? *comm_err : 0);
 }
 
 cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,

@@ -9,7 +9,7 @@ phase twice before a waiter observed it is a parity aliasing error.  Run before 
 import itertools
 import sys
 
-RA, RB, KDY = 2, 4, 3
+RA, RB, KDY = 3, 4, 3
 
 
 class Bar:
@@ -59,38 +59,61 @@ def simulate(m, KB, verbose=False):
                 w += 1
 
     def mma():
+        # the kernel's polling issuer: pass B steps first while ready, then one pass-A block;
+        # yields ("poll", progressed) so a round where nothing is ready counts as no progress
         yield (wfull, 0)
+        ja = ka = jb = qb = 0
+        l_ok = g_ok = False
         dyc = u3 = 0
-        for j in range(m + 1):
-            if j < m:
-                yield (lempty, (j & 1) ^ 1)
-                for kb in range(KB):
-                    w = j * KB + kb
-                    s = w % RA
-                    yield (fullA[s], (w // RA) & 1)
-                    assert ownA[s] == (j, kb, w), ("MMA1 reads wrong slot", s, ownA[s], j, kb)
-                    emptyA[s].arrive()
-                lfull.arrive()
-            if j >= 1:
-                jb = j - 1
+        NPq = 3 * NP
+        while ja < m or jb < m:
+            did = False
+            while jb < ja:
                 gb = jb & 1
-                yield (gfull[gb], (jb >> 1) & 1)
-                p0 = jb * KB
-                for c in range(NP):
-                    for h in range(2):
-                        b = dyc % KDY
-                        yield (dempty[b], ((dyc // KDY) & 1) ^ 1)
-                        dfull[b].arrive()
-                        dyc += 1
-                    w = p0 + 2 * c
+                if not g_ok:
+                    if not gfull[gb].ready((jb >> 1) & 1):
+                        break
+                    g_ok = True
+                c, h = qb // 3, qb % 3
+                if h < 2:
+                    b = dyc % KDY
+                    if not dempty[b].ready(((dyc // KDY) & 1) ^ 1):
+                        break
+                    dfull[b].arrive()
+                    dyc += 1
+                else:
+                    w = jb * KB + 2 * c
                     s = w % RB
                     assert s % 2 == 0 and s + 1 < RB
-                    yield (fullB[s], (w // RB) & 1)
-                    yield (fullB[s + 1], ((w + 1) // RB) & 1)
+                    if not (fullB[s].ready((w // RB) & 1) and fullB[s + 1].ready(((w + 1) // RB) & 1)):
+                        break
                     assert ownB[s] == (jb, 2 * c, w) and ownB[s + 1] == (jb, 2 * c + 1, w + 1)
                     m3[u3 & 1].arrive()
                     u3 += 1
-                gempty[gb].arrive()
+                did = True
+                qb += 1
+                if qb == NPq:
+                    gempty[gb].arrive()
+                    jb += 1
+                    qb = 0
+                    g_ok = False
+            if ja < m:
+                if not l_ok and ka == 0 and lempty.ready((ja & 1) ^ 1):
+                    l_ok = True
+                w = ja * KB + ka
+                s = w % RA
+                if l_ok and fullA[s].ready((w // RA) & 1):
+                    assert ownA[s] == (ja, ka, w), ("MMA1 reads wrong slot", s, ownA[s], ja, ka)
+                    emptyA[s].arrive()
+                    if ka == KB - 1:
+                        lfull.arrive()
+                    did = True
+                    ka += 1
+                    if ka == KB:
+                        ja += 1
+                        ka = 0
+                        l_ok = False
+            yield ("poll", did)
         dwdone.arrive()
 
     def loss(lw):
@@ -144,6 +167,21 @@ def simulate(m, KB, verbose=False):
                 continue
             while True:
                 w = waiting[name]
+                if w is not None and w[0] == "poll":
+                    waiting[name] = None
+                    try:
+                        nxt = next(g)
+                    except StopIteration:
+                        done.add(name)
+                        progress = True
+                        break
+                    if nxt[0] == "poll" and not nxt[1]:
+                        waiting[name] = nxt
+                        break                     # polled, nothing ready: yield the round
+                    waiting[name] = nxt
+                    progress = True
+                    steps += 1
+                    continue
                 if w is not None:
                     if w[0] == "named":
                         if named["n2"][1] <= w[1]:
@@ -159,7 +197,8 @@ def simulate(m, KB, verbose=False):
                     progress = True
                     break
         if not progress:
-            blocked = {k: (v[0].name if v and v[0] != "named" else "named", v[1] if v else None)
+            blocked = {k: (v[0].name if v and not isinstance(v[0], str) else (v[0] if v else None),
+                           v[1] if v else None)
                        for k, v in waiting.items() if k not in done}
             raise RuntimeError(f"deadlock m={m} KB={KB}: {blocked}")
     return steps
