@@ -838,7 +838,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   const float* hbias = T == 1 ? c->params + hd.b_off : c->hbias;
   const int zcols = c->A + 1 + (int)c->heads.size();
   const bool fused = head_fused_enabled() && hL % 128 == 0 && hL <= 512 && c->A + 1 <= 32 &&
-                     head_fused_smem(hL, zcols) + 512 <= kSmemLimit;
+                     head_fused_smem(hL, zcols, (int)c->heads.size()) + 512 <= kSmemLimit;
   std::vector<int> splits(HI + 1, 1), colsum_parts(HI + 1, 0);
   int cur = 0;
   auto loss_args = [&](GemmArgs& g) {

@@ -22,11 +22,12 @@
 // MMA1 and the MN-major B of MMA2; the g tile serves as the K-major A of MMA2 and the
 // MN-major B of MMA3; a Y ring slot serves as the K-major A of MMA1 and the MN-major A of MMA3.
 //
-// TMEM (512 columns): [0, hL/2) dW^T (hL/128 chunks of 64), [256, 320) logits,
-// [320, 512) three 64-column dY buffers.
+// TMEM (512 columns): [0, hL/2) dW^T (hL/128 chunks of 64), [256, 320) two 32-column logits
+// buffers (MMA1 of tile j+1 runs while the loss warps still read tile j's), [320, 512) three
+// 64-column dY buffers.
 //
-// Warp roles (512 threads): w0 TMA producer (pass A), w1 MMA issuer, w2 TMEM allocator, w3 TMA
-// producer (pass B),
+// Warp roles (512 threads): w0 TMA producer (pass A), w1 MMA issuer of pass A, w2 TMEM
+// allocator + MMA issuer of pass B, w3 TMA producer (pass B),
 // w4..w7 loss epilogue (row quadrant w % 4), w8..w15 dtanh epilogue (two warpgroups: 32-column
 // halves of each 64-column dY block, row quadrant w % 4).
 #include <atomic>
@@ -48,8 +49,17 @@ __device__ unsigned long long g_hf_trace[256 * 16];
 #define HF_WAIT(bar, par, k) wait_bounded(bar, par)
 #endif
 
+#if defined(SRL_HF_EXP_NOB) || defined(SRL_HF_EXP_NOA)
+// timing experiment: complete the expected transaction bytes of a ring slot without a load
+__device__ __forceinline__ void mbar_arrive_expect_noop(uint64_t* bar) {
+  asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(16384) : "memory");
+}
+#endif
+
 namespace hf {
-constexpr int kRingA = 3;                     // pass-A ring (consumed by MMA1 as it lands)
+// pass-A ring depth RA (template, 3..5): the deepest that fits next to everything else.
+// Pass A streams Y_L from HBM and its TMA loads see ~3 us latency under the kernel's own
+// load, so the bytes in flight per SM (RA x 16 KB) bound the tile rate (Little's law).
 constexpr int kRingB = 4;                     // pass-B ring (even: an MMA3 pair is adjacent)
 constexpr int kSlot = 128 * 64 * 2;           // one [128 rows][64 cols] fp16 block, 16 KB
 constexpr int kWRows = 32;                    // head rows kept (A + 1 <= 32)
@@ -63,10 +73,11 @@ constexpr uint32_t kColLogits = 256, kColDy = 320;
 struct Layout {
   uint32_t ring, w, g, ostage, zbuf, cs_y, cs_h, bias, bars, total;
 };
-__host__ __device__ inline Layout layout(int hL, int zcols) {
+// zcols = 0: one categorical head, the loss runs in registers (no row buffer)
+__host__ __device__ inline Layout layout(int hL, int zcols, int ra) {
   Layout L;
-  L.ring = 0;                                     // [kRingA slots][kRingB slots]
-  L.w = L.ring + (kRingA + kRingB) * kSlot;
+  L.ring = 0;                                     // [ra slots][kRingB slots]
+  L.w = L.ring + (ra + kRingB) * kSlot;
   L.g = L.w + (hL / 64) * kWBox;
   L.ostage = L.g + 2 * kGBytes;
   L.zbuf = L.ostage + kDtWarps * kStageTile;
@@ -81,9 +92,12 @@ __host__ __device__ inline Layout layout(int hL, int zcols) {
 // of ring B (KB even and kRingB even: the two blocks of an MMA3 pair sit in adjacent slots)
 }  // namespace hf
 
-size_t head_fused_smem(int hL, int zcols) { return 1024 + hf::layout(hL, zcols).total; }
+static size_t smem_of(int hL, int zcols, int n_heads, int ra) {
+  return 1024 + hf::layout(hL, n_heads == 1 ? 0 : zcols, ra).total;
+}
+size_t head_fused_smem(int hL, int zcols, int n_heads) { return smem_of(hL, zcols, n_heads, 3); }
 
-template <int KB>
+template <int KB, int kRingA>
 __global__ void __launch_bounds__(hf::kThreads, 1)
 head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmW,
                   const __grid_constant__ CUtensorMap tmO, const GemmArgs args,
@@ -91,7 +105,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
   using namespace hf;
   constexpr int hL = KB * 64, NP = KB / 2;
   const int zcols = args.A + 1 + args.n_heads;
-  const Layout SL = layout(hL, zcols);
+  const Layout SL = layout(hL, args.n_heads == 1 ? 0 : zcols, kRingA);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -105,9 +119,9 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
   uint64_t* gfull = m3done + 2;               // [2] per g buffer
   uint64_t* gempty = gfull + 2;               // [2]
   uint64_t* wfull = gempty + 2;
-  uint64_t* lfull = wfull + 1;
-  uint64_t* lempty = lfull + 1;
-  uint64_t* dwdone = lempty + 1;
+  uint64_t* lfull = wfull + 1;                // [2] per logits buffer
+  uint64_t* lempty = lfull + 2;               // [2]
+  uint64_t* dwdone = lempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dwdone + 1);
   float* bias_s = reinterpret_cast<float*>(smem + SL.bias);
 
@@ -138,8 +152,10 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
       mbar_init(&gempty[b], 1);
     }
     mbar_init(wfull, 1);
-    mbar_init(lfull, 1);
-    mbar_init(lempty, kLossWarps);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&lfull[b], 1);
+      mbar_init(&lempty[b], kLossWarps);
+    }
     mbar_init(dwdone, 1);
     fence_mbar_init();
   }
@@ -173,11 +189,21 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
           const int s = w % R;
           HF_WAIT(&empty[s], ((w / R) & 1u) ^ 1u, pa ? 1 : 2);
           mbar_expect_tx(&full[s], kSlot);
+#ifdef SRL_HF_EXP_NOB
+          if (!pa) { mbar_arrive_expect_noop(&full[s]); continue; }   // timing experiment only
+#endif
+#ifdef SRL_HF_EXP_NOA
+          if (pa) { mbar_arrive_expect_noop(&full[s]); continue; }    // timing experiment only
+#endif
           tma_load_2d(ring + s * kSlot, &tmY, &full[s], kb * 64, tile(j) * 128);
         }
     }
-  } else if (warp == 1) {
-    // ============================ MMA issuer (same stream order as the producer)
+  } else if (warp == 1 || warp == 2) {
+    // ============================ MMA issuers: warp 1 pass A (MMA1), warp 2 pass B (MMA2 +
+    // MMA3).  A tcgen05.mma costs its issuing warp ~100 cycles (operand moves to uniform
+    // registers, elect), far more than the tensor core needs for these N = 32 / 64 shapes, so
+    // one issuer for both passes was the kernel's critical path; each warp commits (and so
+    // tracks) only its own MMAs, and the two touch disjoint TMEM columns.
     constexpr uint32_t ID1 = umma_idesc_f16(128, kWRows, false, false);
     constexpr uint32_t ID2 = umma_idesc_f16(128, 64, false, true);
     constexpr uint32_t ID3 = umma_idesc_f16(128, 64, true, true);
@@ -185,49 +211,53 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     const uint32_t w0 = smem_u32(smem + SL.w);
     const uint32_t g00 = smem_u32(smem + SL.g);
     wait_bounded(wfull, 0);
-    // Two cursors, each issued as soon as its barriers allow, pass B first (the dtanh warps
-    // are the long pole): a pass-A block whose TMA load is still in flight never holds back
-    // the dY blocks / dW^T pairs of the previous tile.  Pass B of tile jb needs its g, so it
-    // runs behind pass A (jb < ja).  Barrier tests are non-blocking (lane 0, broadcast).
-    auto ready = [&](uint64_t* bar, uint32_t par) -> bool {
-      const uint32_t r = lane == 0 ? (uint32_t)mbar_test(bar, par) : 0u;
-      return __shfl_sync(0xffffffffu, r, 0) != 0u;
-    };
-    int ja = 0, ka = 0;                    // pass A: tile, block
-    int jb = 0, qb = 0;                    // pass B: tile, sub-step (per pair: dY h=0, h=1, dW^T)
-    bool l_ok = false, g_ok = false;       // lempty seen for tile ja / gfull seen for tile jb
-    uint32_t dyc = 0, u3 = 0;
-    long long idle0 = clock64();
-    while (ja < m || jb < m) {
-      bool did = false;
-      // ---- pass B of tile jb: dY blocks and the dW^T pairs
-      while (jb < ja) {
-        const int gb = jb & 1;
-        if (!g_ok) {
-          if (!ready(&gfull[gb], (jb >> 1) & 1)) break;
-          g_ok = true;
-        }
-        const uint32_t g0 = g00 + gb * kGBytes;
-        const int c = qb / 3, h = qb % 3;
-        if (h < 2) {
-          const int kb = 2 * c + h, bf = dyc % kDy;
-          if (!ready(&dempty[bf], ((dyc / kDy) & 1u) ^ 1u)) break;
+    if (warp == 1) {
+      // ---- pass A of tile j: logits into buffer j % 2 (free once tile j-2's were read)
+      for (int j = 0; j < m; ++j) {
+        HF_WAIT(&lempty[j & 1], ((j >> 1) & 1) ^ 1, 4);
+        for (int kb = 0; kb < KB; ++kb) {
+          const uint32_t w = (uint32_t)(j * KB + kb);
+          const int sa = w % kRingA;
+          HF_WAIT(&fullA[sa], (w / kRingA) & 1u, 6);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t wb = w0 + kb * kWBox;
+            const uint32_t a = ringA + sa * kSlot, b = w0 + kb * kWBox;
 #pragma unroll
-            for (int k = 0; k < kWRows / 16; ++k)      // K = the 32 real head columns of g
-              tc_mma_f16_cg<1>(tmem_base + kColDy + 64 * bf, umma_desc_sw128(g0 + k * 32, 16, 1024),
-                               umma_desc_sw128(wb + k * 2048, 8192, 1024), ID2, k > 0 ? 1u : 0u);
-            tc_commit_cg<1>(&dfull[bf]);
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16_cg<1>(tmem_base + kColLogits + 32 * (j & 1), umma_desc_sw128(a + k * 32, 16, 1024),
+                               umma_desc_sw128(b + k * 32, 16, 1024), ID1, (kb > 0 || k > 0) ? 1u : 0u);
+            tc_commit_cg<1>(&emptyA[sa]);
+            if (kb == KB - 1) tc_commit_cg<1>(&lfull[j & 1]);
           }
           __syncwarp();
-          ++dyc;
-        } else {
-          const uint32_t w = (uint32_t)(jb * KB + 2 * c);
+        }
+      }
+    } else {
+      // ---- pass B of tile j: dY blocks and the dW^T pairs (needs its g)
+      uint32_t dyc = 0, u3 = 0;
+      for (int j = 0; j < m; ++j) {
+        const int gb = j & 1;
+        const uint32_t g0 = g00 + gb * kGBytes;
+        HF_WAIT(&gfull[gb], (j >> 1) & 1, 5);
+        for (int c = 0; c < NP; ++c, ++u3) {
+          for (int h = 0; h < 2; ++h, ++dyc) {
+            const int kb = 2 * c + h, bf = dyc % kDy;
+            HF_WAIT(&dempty[bf], ((dyc / kDy) & 1u) ^ 1u, 7);
+            tc_fence_after();
+            if (lane == 0) {
+              const uint32_t wb = w0 + kb * kWBox;
+#pragma unroll
+              for (int k = 0; k < kWRows / 16; ++k)      // K = the 32 real head columns of g
+                tc_mma_f16_cg<1>(tmem_base + kColDy + 64 * bf, umma_desc_sw128(g0 + k * 32, 16, 1024),
+                                 umma_desc_sw128(wb + k * 2048, 8192, 1024), ID2, k > 0 ? 1u : 0u);
+              tc_commit_cg<1>(&dfull[bf]);
+            }
+            __syncwarp();
+          }
+          const uint32_t w = (uint32_t)(j * KB + 2 * c);
           const int sb = w % kRingB;                 // the pair's slots sb, sb + 1 (sb even)
-          if (!ready(&fullB[sb], (w / kRingB) & 1u) || !ready(&fullB[sb + 1], ((w + 1) / kRingB) & 1u))
-            break;
+          HF_WAIT(&fullB[sb], (w / kRingB) & 1u, 7);
+          HF_WAIT(&fullB[sb + 1], ((w + 1) / kRingB) & 1u, 7);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a = ringB + sb * kSlot;
@@ -235,58 +265,17 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
             for (int k = 0; k < 8; ++k)
               tc_mma_f16_cg<1>(tmem_base + 64 * c, umma_desc_sw128(a + k * 2048, kSlot, 1024),
                                umma_desc_sw128(g0 + k * 2048, 8192, 1024), ID3,
-                               (jb > 0 || k > 0) ? 1u : 0u);
+                               (j > 0 || k > 0) ? 1u : 0u);
             tc_commit_cg<1>(&m3done[u3 & 1]);
           }
           __syncwarp();
-          ++u3;
         }
-        did = true;
-        if (++qb == 3 * NP) {
-          if (lane == 0) tc_commit_cg<1>(&gempty[gb]);   // g buffer gb free once these complete
-          __syncwarp();
-          ++jb;
-          qb = 0;
-          g_ok = false;
-        }
+        if (lane == 0) tc_commit_cg<1>(&gempty[gb]);   // g buffer gb free once these complete
+        __syncwarp();
       }
-      // ---- pass A of tile ja: one logits block (the loss warps must have read tile ja-1's)
-      if (ja < m) {
-        if (!l_ok && ka == 0 && ready(lempty, (ja & 1) ^ 1)) l_ok = true;
-        const uint32_t w = (uint32_t)(ja * KB + ka);
-        const int sa = w % kRingA;
-        if (l_ok && ready(&fullA[sa], (w / kRingA) & 1u)) {
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a = ringA + sa * kSlot, b = w0 + ka * kWBox;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc_mma_f16_cg<1>(tmem_base + kColLogits, umma_desc_sw128(a + k * 32, 16, 1024),
-                               umma_desc_sw128(b + k * 32, 16, 1024), ID1, (ka > 0 || k > 0) ? 1u : 0u);
-            tc_commit_cg<1>(&emptyA[sa]);
-            if (ka == KB - 1) tc_commit_cg<1>(lfull);
-          }
-          __syncwarp();
-          did = true;
-          if (++ka == KB) {
-            ++ja;
-            ka = 0;
-            l_ok = false;
-          }
-        }
-      }
-      if (did) {
-        idle0 = clock64();
-      } else {
-        __nanosleep(32);
-        if (clock64() - idle0 > (1ll << 35)) __trap();   // a lost arrival (kernel bug)
-#ifdef SRL_HF_TRACE
-        trc[4] += 1;
-#endif
-      }
+      if (lane == 0) tc_commit_cg<1>(dwdone);
+      __syncwarp();
     }
-    if (lane == 0) tc_commit_cg<1>(dwdone);
-    __syncwarp();
   } else if (warp >= 4 && warp < 8) {
     // ============================ loss epilogue: one row per lane, quadrant warp % 4
     const int lw = warp - 4, quad = warp & 3;
@@ -314,14 +303,14 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
         if (args.v_old) vo = __ldg(args.v_old + row);
       }
       const int act0 = (lvalid && single) ? __ldg(arow) : 0;
-      HF_WAIT(lfull, j & 1, j == 0 ? 3 : 8);
+      HF_WAIT(&lfull[j & 1], (j >> 1) & 1, j == 0 ? 3 : 8);
       tc_fence_after();
       float z[32];                                   // the A + 1 <= 32 head outputs
-      tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + kColLogits, z);
+      tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + kColLogits + 32 * (j & 1), z);
       tc_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(lempty);           // MMA1 of the next tile may overwrite
+      if (lane == 0) mbar_arrive(&lempty[j & 1]);   // MMA1 of tile j + 2 may overwrite
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) z[jj] += bias_s[jj];   // 0 past A
       if (args.mean_std) {
@@ -422,7 +411,20 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     OutStage1 ost{smem + SL.ostage + dw * kStageTile, 0};
     uint32_t nsat = 0;
     uint32_t dyc = 0, u3 = 0;
-    const int r = quad * 32 + (int)lane;
+    // per-thread constant offsets of the 16x256b fragment: Y row (quad*32 + 16hf + 8h +
+    // lane/4) % 8 == lane/4, so the 128B-swizzled chunk (4 grp + k) ^ (lane/4) is fixed per k;
+    // the 64B-swizzled staging tile row 16hf + 8h + lane/4
+    const uint32_t ring_b0 = smem_u32(smem + SL.ring) + kRingA * kSlot + (uint32_t)(quad * 32 + (lane >> 2)) * 128;
+    // (stile_off(row, k) with row = 16hf + 8h + lane/4: its swizzle (row >> 1) & 3 = (lane >> 3)
+    // & 3 for every hf, h, so row (16hf + 8h) only adds an immediate)
+    uint32_t y_off[4], s_off[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      y_off[k] = (uint32_t)((((4 * grp + k) ^ (int)(lane >> 2)) << 4) + 4 * (lane & 3));
+      s_off[k] = stile_off((int)(lane >> 2), k) + 4 * (lane & 3);
+    }
+    // the column this lane ends the butterfly with: value index 4 b4 + 2 b3 + b2 = 2k + e
+    const int cs_col = 8 * (2 * (int)((lane >> 4) & 1) + (int)((lane >> 3) & 1)) + 2 * (int)(lane & 3) + (int)((lane >> 2) & 1);
     for (int j = 0; j < m; ++j) {
       const int t = tile(j);
       const uint32_t p0 = (uint32_t)(j * KB);
@@ -433,33 +435,40 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
         for (int h = 0; h < 2; ++h, ++dyc) {
           const int kb = 2 * c + h, b = dyc % kDy;
           const uint32_t wk = p0 + kb;
-          HF_WAIT(&dfull[b], (dyc / kDy) & 1u, dyc == 0 ? 5 : 11);
+          HF_WAIT(&dfull[b], (dyc / kDy) & 1u, 11);
           tc_fence_after();
+          // dY block [32 rows of the quadrant][32 columns of the half] as 16x256b fragments:
+          // v[16 hf + 4k + 2h + e] = (row 16hf + 8h + lane/4, col 8k + 2(lane%4) + e), so the
+          // column sums need 4 in-thread rows + a 3-level butterfly instead of a 32x32 transpose
           float v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + kColDy + 64 * b + 32 * grp, v);
+          const uint32_t tq = tmem_base + ((uint32_t)(quad * 32) << 16) + kColDy + 64 * b + 32 * grp;
+          tmem_ld16x256_x4(tq, v);
+          tmem_ld16x256_x4(tq + (16u << 16), v + 16);
           tc_wait_ld();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&dempty[b]);
           const int s = wk % kRingB;
           HF_WAIT(&fullB[s], (wk / kRingB) & 1u, 12);
-          const uint8_t* yrow = smem + SL.ring + (kRingA + s) * kSlot + r * 128;
+          // v := dY .* (Y^2 - 1) = -dZ (negated: the packed fma needs no operand negation; the
+          // stores negate the fp16 pairs, the column sums are negated once at the end)
+          const uint32_t ybase = ring_b0 + s * kSlot;
           float mx = 0.f;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int chunk = 4 * grp + q;           // 16-byte chunk of the 128-byte row
-            const uint4 u = *reinterpret_cast<const uint4*>(yrow + ((chunk ^ (r & 7)) << 4));
-            const __half2* hh = reinterpret_cast<const __half2*>(&u);
+          for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 y = __half22float2(hh[e]);
-              float& a0 = v[8 * q + 2 * e];
-              float& a1 = v[8 * q + 2 * e + 1];
-              a0 *= fmaf(-y.x, y.x, 1.f);
-              a1 *= fmaf(-y.y, y.y, 1.f);
-              mx = fmaxf(mx, fmaxf(fabsf(a0), fabsf(a1)));
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t yr = ybase + (uint32_t)(16 * hf + 8 * h) * 128;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t u = lds32(yr + y_off[k]);
+                const float2 y = __half22float2(*reinterpret_cast<const __half2*>(&u));
+                float& a0 = v[16 * hf + 4 * k + 2 * h];
+                float& a1 = v[16 * hf + 4 * k + 2 * h + 1];
+                mul_sqm1_x2(a0, a1, y.x, y.y);
+                mx = fmaxf(mx, fmaxf(fabsf(a0), fabsf(a1)));
+              }
             }
-          }
           if (mx > 65504.f) {
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) v[jj] = sat_f16(v[jj], nsat);
@@ -471,9 +480,44 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
 #ifdef SRL_HF_TRACE
           trc[14] += (unsigned long long)(clock64() - ta0);
 #endif
-          stile_write_row(tl, (int)lane, v);
+          const uint32_t tls = smem_u32(tl);
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int i = 16 * hf + 4 * k + 2 * h;
+                sts32(tls + s_off[k] + (uint32_t)(16 * hf + 8 * h) * 64,
+                      pack_half2(v[i], v[i + 1]) ^ 0x80008000u);
+              }
+#ifdef SRL_HF_EXP_NOSTORE
+          ++ost.k;                                   // timing experiment only: no dZ store
+#else
           ost.release(tl, &tmO, kb * 64 + 32 * grp, t * 128 + quad * 32);
-          my_cs[kb * 32 + lane] += transpose_reduce32(v);   // db_L: fp32 column sums
+#endif
+          // column sums of -dZ: 4 rows in-thread, then lanes differing in bits 4, 3, 2
+          float c8[8];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float x0 = v[4 * k], x1 = v[4 * k + 1], z0 = v[16 + 4 * k], z1 = v[16 + 4 * k + 1];
+            add_x2(x0, x1, v[4 * k + 2], v[4 * k + 3]);
+            add_x2(z0, z1, v[16 + 4 * k + 2], v[16 + 4 * k + 3]);
+            add_x2(x0, x1, z0, z1);
+            c8[2 * k] = x0;
+            c8[2 * k + 1] = x1;
+          }
+#pragma unroll
+          for (int w = 4; w >= 1; w >>= 1) {
+            const bool up = (lane & (4u * w)) != 0;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+              const float send = up ? c8[i] : c8[i + w];
+              const float keep = up ? c8[i + w] : c8[i];
+              c8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4 * w);
+            }
+          }
+          my_cs[kb * 32 + cs_col] += c8[0];
         }
         // both blocks of the pair read by all 8 dtanh warps: once MMA3 of the pair is done too,
         // the two ring slots go back to the producer
@@ -505,7 +549,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
       const int kb = i / 64, g2 = (i % 64) / 32, c = i % 32;
       float x = 0.f;
       for (int q = 0; q < 4; ++q) x += cs0[(g2 * 4 + q) * (hL / 2) + kb * 32 + c];
-      colsum_y[(int64_t)blockIdx.x * hL + i] = x;
+      colsum_y[(int64_t)blockIdx.x * hL + i] = -x;      // the sums were of -dZ
     }
     // dW_h^T of this CTA -> partial [blockIdx][hL][64] (the transposed split-K layout of the
     // head segment; the finalise sums the CTAs in index order)
@@ -528,7 +572,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
 #ifdef SRL_HF_TRACE
   // slot 0: kernel cycles (MMA warp); 10 / 15: loss / dtanh warp cycles to the end of its loop
   if (warp == 1) trc[0] = (unsigned long long)(clock64() - t_start);
-  if (warp == 0 || warp == 1 || warp == 3 || warp == 4 || warp == 8)
+  if (warp <= 4 || warp == 8)
     for (int k = 0; k < 16; ++k)
       if (trc[k] && (lane == 0 || warp == 0 || warp == 3))   // producers: the elected lane
         atomicAdd(&g_hf_trace[blockIdx.x * 16 + k], trc[k]);
@@ -541,11 +585,11 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
   }
 }
 
-template <int KB>
+template <int KB, int RA>
 static cudaError_t launch_kb(const CUtensorMap& tmY, const CUtensorMap& tmW, const CUtensorMap& tmO,
                              const GemmArgs& args, float* colsum_y, int grid, size_t smem,
                              cudaStream_t s) {
-  auto kern = head_fused_kernel<KB>;
+  auto kern = head_fused_kernel<KB, RA>;
   static std::atomic<size_t> configured[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
@@ -560,17 +604,29 @@ static cudaError_t launch_kb(const CUtensorMap& tmY, const CUtensorMap& tmW, con
   return cudaGetLastError();
 }
 
+template <int KB>
+static cudaError_t launch_ra(const CUtensorMap& tmY, const CUtensorMap& tmW, const CUtensorMap& tmO,
+                             const GemmArgs& args, float* colsum_y, int grid, int zcols, cudaStream_t s) {
+  constexpr int hL = KB * 64;
+  for (int ra = 5; ra >= 3; --ra) {
+    const size_t smem = smem_of(hL, zcols, args.n_heads, ra);
+    if (smem + 512 > kSmemLimit) continue;
+    if (ra == 5) return launch_kb<KB, 5>(tmY, tmW, tmO, args, colsum_y, grid, smem, s);
+    if (ra == 4) return launch_kb<KB, 4>(tmY, tmW, tmO, args, colsum_y, grid, smem, s);
+    return launch_kb<KB, 3>(tmY, tmW, tmO, args, colsum_y, grid, smem, s);
+  }
+  return cudaErrorInvalidConfiguration;
+}
+
 cudaError_t launch_head_fused(const CUtensorMap& tmY, const CUtensorMap& tmW, const CUtensorMap& tmO,
                               const GemmArgs& args, int hL, float* colsum_y, int grid,
                               cudaStream_t s) {
   if (args.A + 1 > hf::kWRows) return cudaErrorInvalidValue;
   const int zcols = args.A + 1 + args.n_heads;
-  const size_t smem = head_fused_smem(hL, zcols);
-  if (smem + 512 > kSmemLimit) return cudaErrorInvalidConfiguration;
   switch (hL) {
-    case 128: return launch_kb<2>(tmY, tmW, tmO, args, colsum_y, grid, smem, s);
-    case 256: return launch_kb<4>(tmY, tmW, tmO, args, colsum_y, grid, smem, s);
-    case 512: return launch_kb<8>(tmY, tmW, tmO, args, colsum_y, grid, smem, s);
+    case 128: return launch_ra<2>(tmY, tmW, tmO, args, colsum_y, grid, zcols, s);
+    case 256: return launch_ra<4>(tmY, tmW, tmO, args, colsum_y, grid, zcols, s);
+    case 512: return launch_ra<8>(tmY, tmW, tmO, args, colsum_y, grid, zcols, s);
     default: return cudaErrorInvalidValue;
   }
 }

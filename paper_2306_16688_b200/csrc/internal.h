@@ -84,7 +84,7 @@ cudaError_t launch_gemm(int bn, bool a_mn, bool b_mn, int epi, int cg, const CUt
 
 // ---- a4 + head part of a5 in one kernel (head_fused.cu): loss, dZ_L (+ db_L column sums into
 // colsum_y [grid][hL]) and dW_h^T partials [grid][hL][64] (args.part); hL % 128 == 0, <= 512
-size_t head_fused_smem(int hL, int zcols);
+size_t head_fused_smem(int hL, int zcols, int n_heads);
 cudaError_t launch_head_fused(const CUtensorMap& tmY, const CUtensorMap& tmW, const CUtensorMap& tmO,
                               const GemmArgs& args, int hL, float* colsum_y, int grid,
                               cudaStream_t s);

@@ -223,6 +223,50 @@ __device__ __forceinline__ void tc_wait_ld() {
 }
 
 // 32 lanes x 32 consecutive fp32 columns: thread t gets row (lane base + t), cols c..c+31
+// 16 lanes x 256 bits, 4 repeats (32 fp32 columns): thread t gets rows t/4 and t/4 + 8 of the
+// 16 lanes at taddr, columns 8k + 2(t % 4) + {0, 1}: v[4k + 2h + e] = (row t/4 + 8h, col
+// 8k + 2(t%4) + e) (CuTe SM100_TMEM_LOAD_16dp256b4x)
+__device__ __forceinline__ void tmem_ld16x256_x4(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// shared-window loads / stores by 32-bit address (no generic-address round trip)
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// packed fp32x2 (FFMA2 / FMUL2 / FADD2 on sm_100)
+__device__ __forceinline__ void mul_sqm1_x2(float& a0, float& a1, float y0, float y1) {
+  // (a0, a1) *= (y0 * y0 - 1, y1 * y1 - 1), each factor rounded once (fma)
+  asm("{\n\t.reg .b64 A, Y, T, M;\n\t"
+      "mov.b64 A, {%0, %1};\n\t"
+      "mov.b64 Y, {%2, %3};\n\t"
+      "mov.b64 M, {%4, %4};\n\t"
+      "fma.rn.f32x2 T, Y, Y, M;\n\t"
+      "mul.rn.f32x2 A, A, T;\n\t"
+      "mov.b64 {%0, %1}, A;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(y0), "f"(y1), "f"(-1.f));
+}
+__device__ __forceinline__ void add_x2(float& a0, float& a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 A, B;\n\t"
+      "mov.b64 A, {%0, %1};\n\t"
+      "mov.b64 B, {%2, %3};\n\t"
+      "add.rn.f32x2 A, A, B;\n\t"
+      "mov.b64 {%0, %1}, A;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1));
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(

@@ -9,7 +9,7 @@ phase twice before a waiter observed it is a parity aliasing error.  Run before 
 import itertools
 import sys
 
-RA, RB, KDY = 3, 4, 3
+RB, KDY = 4, 3
 
 
 class Bar:
@@ -28,7 +28,7 @@ class Bar:
         return self.phase != parity
 
 
-def simulate(m, KB, verbose=False):
+def simulate(m, KB, RA=3, verbose=False):
     NP = KB // 2
     B = {}
     mk = lambda n, c: B.setdefault(n, Bar(n, c))
@@ -41,7 +41,9 @@ def simulate(m, KB, verbose=False):
     m3 = [mk(f"m3done{b}", 1) for b in range(2)]
     gfull = [mk(f"gfull{b}", 4) for b in range(2)]
     gempty = [mk(f"gempty{b}", 1) for b in range(2)]
-    wfull, lfull, lempty, dwdone = mk("wfull", 1), mk("lfull", 1), mk("lempty", 4), mk("dwdone", 1)
+    wfull, dwdone = mk("wfull", 1), mk("dwdone", 1)
+    lfull = [mk(f"lfull{b}", 1) for b in range(2)]      # two logits buffers
+    lempty = [mk(f"lempty{b}", 4) for b in range(2)]
     ownA, ownB = {}, {}
     named = {"n2": [0, 0]}               # dtanh named barrier: [arrived, generation]
 
@@ -58,68 +60,46 @@ def simulate(m, KB, verbose=False):
                 full[s].arrive()
                 w += 1
 
-    def mma():
-        # the kernel's polling issuer: pass B steps first while ready, then one pass-A block;
-        # yields ("poll", progressed) so a round where nothing is ready counts as no progress
+    def mma_a():                          # warp 1: pass A (MMA1)
         yield (wfull, 0)
-        ja = ka = jb = qb = 0
-        l_ok = g_ok = False
+        for j in range(m):
+            yield (lempty[j & 1], ((j >> 1) & 1) ^ 1)
+            for kb in range(KB):
+                w = j * KB + kb
+                s = w % RA
+                yield (fullA[s], (w // RA) & 1)
+                assert ownA[s] == (j, kb, w), ("MMA1 reads wrong slot", s, ownA[s], j, kb)
+                emptyA[s].arrive()
+                if kb == KB - 1:
+                    lfull[j & 1].arrive()
+
+    def mma_b():                          # warp 2: pass B (MMA2 + MMA3)
+        yield (wfull, 0)
         dyc = u3 = 0
-        NPq = 3 * NP
-        while ja < m or jb < m:
-            did = False
-            while jb < ja:
-                gb = jb & 1
-                if not g_ok:
-                    if not gfull[gb].ready((jb >> 1) & 1):
-                        break
-                    g_ok = True
-                c, h = qb // 3, qb % 3
-                if h < 2:
+        for j in range(m):
+            gb = j & 1
+            yield (gfull[gb], (j >> 1) & 1)
+            for c in range(NP):
+                for h in range(2):
                     b = dyc % KDY
-                    if not dempty[b].ready(((dyc // KDY) & 1) ^ 1):
-                        break
+                    yield (dempty[b], ((dyc // KDY) & 1) ^ 1)
                     dfull[b].arrive()
                     dyc += 1
-                else:
-                    w = jb * KB + 2 * c
-                    s = w % RB
-                    assert s % 2 == 0 and s + 1 < RB
-                    if not (fullB[s].ready((w // RB) & 1) and fullB[s + 1].ready(((w + 1) // RB) & 1)):
-                        break
-                    assert ownB[s] == (jb, 2 * c, w) and ownB[s + 1] == (jb, 2 * c + 1, w + 1)
-                    m3[u3 & 1].arrive()
-                    u3 += 1
-                did = True
-                qb += 1
-                if qb == NPq:
-                    gempty[gb].arrive()
-                    jb += 1
-                    qb = 0
-                    g_ok = False
-            if ja < m:
-                if not l_ok and ka == 0 and lempty.ready((ja & 1) ^ 1):
-                    l_ok = True
-                w = ja * KB + ka
-                s = w % RA
-                if l_ok and fullA[s].ready((w // RA) & 1):
-                    assert ownA[s] == (ja, ka, w), ("MMA1 reads wrong slot", s, ownA[s], ja, ka)
-                    emptyA[s].arrive()
-                    if ka == KB - 1:
-                        lfull.arrive()
-                    did = True
-                    ka += 1
-                    if ka == KB:
-                        ja += 1
-                        ka = 0
-                        l_ok = False
-            yield ("poll", did)
+                w = j * KB + 2 * c
+                s = w % RB
+                assert s % 2 == 0 and s + 1 < RB
+                yield (fullB[s], (w // RB) & 1)
+                yield (fullB[s + 1], ((w + 1) // RB) & 1)
+                assert ownB[s] == (j, 2 * c, w) and ownB[s + 1] == (j, 2 * c + 1, w + 1)
+                m3[u3 & 1].arrive()
+                u3 += 1
+            gempty[gb].arrive()
         dwdone.arrive()
 
     def loss(lw):
         for j in range(m):
-            yield (lfull, j & 1)
-            lempty.arrive()
+            yield (lfull[j & 1], (j >> 1) & 1)
+            lempty[j & 1].arrive()
             gb = j & 1
             yield (gempty[gb], ((j >> 1) & 1) ^ 1)
             gfull[gb].arrive()
@@ -152,7 +132,7 @@ def simulate(m, KB, verbose=False):
                 u3 += 1
         yield (dwdone, 0)
 
-    roles = {"producerA": producer(True), "producerB": producer(False), "mma": mma()}
+    roles = {"producerA": producer(True), "producerB": producer(False), "mmaA": mma_a(), "mmaB": mma_b()}
     for i in range(4):
         roles[f"loss{i}"] = loss(i)
     for i in range(8):
@@ -205,7 +185,7 @@ def simulate(m, KB, verbose=False):
 
 
 if __name__ == "__main__":
-    for KB, m in itertools.product((2, 4, 8), (1, 2, 3, 4, 7, 8)):
-        simulate(m, KB)
-    print("protocol ok for KB in {2,4,8}, m in {1,2,3,4,7,8}")
+    for KB, m, RA in itertools.product((2, 4, 8), (1, 2, 3, 4, 7, 8), (3, 4, 5)):
+        simulate(m, KB, RA)
+    print("protocol ok for KB in {2,4,8}, m in {1,2,3,4,7,8}, pass-A ring RA in {3,4,5}")
     sys.exit(0)

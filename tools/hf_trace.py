@@ -17,10 +17,10 @@ import paper_2306_16688_b200 as P  # noqa: E402
 from paper_2306_16688_b200 import srl  # noqa: E402
 import synth  # noqa: E402
 
-NAMES = {0: "kernel (MMA warp)", 1: "prodA wait emptyA", 2: "prodB wait emptyB",
-         3: "loss wait lfull (tile 0)", 4: "mma idle polls", 5: "dtanh wait dfull (first)", 6: "-",
-         7: "-", 8: "loss wait lfull (rest)", 9: "loss wait gempty", 10: "loss loop end",
-         11: "dtanh wait dfull (rest)", 12: "dtanh wait fullB", 13: "dtanh pair barrier",
+NAMES = {0: "pass-A issuer loop", 1: "prodA wait emptyA", 2: "prodB wait emptyB",
+         3: "loss wait lfull (tile 0)", 4: "mmaA wait lempty", 5: "mmaB wait gfull", 6: "mmaA wait fullA",
+         7: "mmaB wait dempty/fullB", 8: "loss wait lfull (rest)", 9: "loss wait gempty", 10: "loss loop end",
+         11: "dtanh wait dfull", 12: "dtanh wait fullB", 13: "dtanh pair barrier",
          14: "dtanh staging acquire", 15: "dtanh loop end"}
 name = sys.argv[1] if len(sys.argv) > 1 else "atari"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5

@@ -1,6 +1,6 @@
 # fused-head iteration (gpurun, 1 GPU): head tests, per-role trace, bench at N=1
 python -m paper_2306_16688_b200.build > gpurun_out/build.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_head_fused.py tests/test_gpu_ppo.py tests/test_gpu_ac.py tests/test_gpu_next3.py -q -x -p no:cacheprovider > gpurun_out/hf_tests.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_head_fused.py -q -x -p no:cacheprovider > gpurun_out/hf_tests.txt 2>&1
 tail -2 gpurun_out/hf_tests.txt
 for c in atari gfootball; do SRL_LIB=variants/hftrace/libsrl.so timeout 120 python tools/hf_trace.py $c 5; done > gpurun_out/hf_trace.txt 2>&1
 cat gpurun_out/hf_trace.txt
