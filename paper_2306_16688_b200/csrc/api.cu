@@ -278,6 +278,20 @@ static bool head_fused_enabled() {
   return !(e && e[0] == '0');
 }
 
+// opt-in (SRL_DW_FIXUP=1): the split-K sum inside each dW launch (gemm_tc.cuh part_fixup).
+// Measured slower on the Atari step (0.480 vs 0.473 ms): the grid barrier holds every CTA
+// until the slowest split is done, so the next launch no longer overlaps the dW tail (PDL),
+// which costs more than the ~8 us the update launch saves.
+static bool dw_fixup_enabled() {
+  const char* e = getenv("SRL_DW_FIXUP");
+  return e && e[0] == '1';
+}
+
+static bool dw_discard_enabled() {
+  const char* e = getenv("SRL_DW_DISCARD");
+  return !(e && e[0] == '0');
+}
+
 static bool dw512_enabled() {   // opt-in: measured ~5% slower dW + finalize on the Atari shape
   const char* e = getenv("SRL_DW512");
   return e && e[0] == '1';
@@ -341,7 +355,8 @@ extern "C" srl_status srl_nccl_unique_id(uint8_t out[128]) {
 // the flat parameter vector as segments with their gradient sources (split-K / per-CTA
 // partials and column sums, indexed like c->lay) and fp16 shadows
 static SegTable make_segs(srl_ctx* c, const std::vector<int>& splits,
-                          const std::vector<int>& colsum_parts, int dz_parts) {
+                          const std::vector<int>& colsum_parts, int dz_parts,
+                          const std::vector<int>& reduced = {}) {
   SegTable t{};
   t.n = 0;
   const int L = c->L, T = c->T;
@@ -359,6 +374,7 @@ static SegTable make_segs(srl_ctx* c, const std::vector<int>& splits,
       w.part = y.part; w.splits = nsp(i); w.ld_part = y.ld_part;
       w.split_stride = y.part_rows * y.ld_part; w.transposed = 0;
       w.w16 = y.w16; w.w16_ld = y.w16_ld;
+      w.done = reduced.empty() ? 0 : reduced[i];
       t.s[t.n++] = w;
       Segment b{};
       b.off = y.b_off; b.rows = 1; b.cols = y.out; b.is_bias = 1;
@@ -562,7 +578,7 @@ extern "C" srl_status srl_ppo_create(const srl_ppo_config* cfg, int rank, int wo
   if ((st = dalloc(c, &c->gn, sizeof(double) * (kGradNormBlocks + 2)))) return bail(st);
   if ((st = dalloc(c, &c->gn_counter, sizeof(unsigned int) * 4))) return bail(st);
   if ((st = dalloc(c, &c->cc.err_dev, sizeof(int) * 4))) return bail(st);
-  if ((st = dalloc(c, &c->gbar, sizeof(unsigned) * 4))) return bail(st);
+  if ((st = dalloc(c, &c->gbar, sizeof(unsigned) * 8))) return bail(st);   // [0..3] update, [4..5] dW
   if (cudaHostAlloc(reinterpret_cast<void**>(&c->err_pinned), sizeof(int) * 4, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->cc.err_host), c->err_pinned, 0) != cudaSuccess) {
     c->err_pinned = nullptr;
@@ -839,7 +855,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
   const int zcols = c->A + 1 + (int)c->heads.size();
   const bool fused = head_fused_enabled() && hL % 128 == 0 && hL <= 512 && c->A + 1 <= 32 &&
                      head_fused_smem(hL, zcols, (int)c->heads.size()) + 512 <= kSmemLimit;
-  std::vector<int> splits(HI + 1, 1), colsum_parts(HI + 1, 0);
+  std::vector<int> splits(HI + 1, 1), colsum_parts(HI + 1, 0), reduced(HI + 1, 0);
   int cur = 0;
   auto loss_args = [&](GemmArgs& g) {
     g.bias = hbias;
@@ -895,6 +911,13 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     if (srl_status st = gemm(64, false, false, EPI_LOSS, 1, ta, tb, to, to, g, sms, s, &grid_loss)) return st;
     colsum_parts[HI] = grid_loss;
   }
+  // a6 through NVLink peer memory: finalise and extras write this rank's bucket into its
+  // exposed buffer (parity of the step's epoch) and the allreduce kernel sums all ranks' into
+  // c->grads.  Otherwise they write c->grads directly (NCCL allreduce in place, or world 1).
+  const bool p2p = apply && c->world > 1 && c->p2p && !ar_overlap();
+  const unsigned long long epoch = p2p ? c->epoch + 1 : 0;
+  const int64_t xoff = (int64_t)(epoch & 1ull) * c->xstride();
+  float* bk = p2p ? c->xbuf + xoff : c->grads;
   // ---------------- a5: backward.  dW via split-K partials, dX with fused dtanh + db sums
   // dW of layer index i (c->lay): D[dM][dN] = A^T B over the n samples (MN-major operands)
   auto dW = [&](int i, const __half* Amat, int lda, const __half* Bmat, int ldb) -> srl_status {
@@ -915,6 +938,13 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     g.k_splits = S;
     g.part = y.part; g.ld_part = y.ld_part; g.part_split_stride = y.part_rows * y.ld_part;
     splits[i] = S;
+    if (!is_head && dw_fixup_enabled() && dN % 4 == 0) {
+      // the split-K sum inside the launch, straight into the bucket the exchange / Adam read
+      g.red_out = bk + y.w_off; g.red_scale = inv_n; g.red_bar = c->gbar + 4;
+      g.red_discard = dw_discard_enabled();
+      g.counters = c->counters;
+      reduced[i] = 1;
+    }
     const int realN = is_head ? y.out : dN;
     ProfScope ps(c, s, is_head ? "dW_head" : (y.l == 0 ? "dW_l1" : "dW_hidden"),
                  2.0 * n * dM * realN, 2.0 * n * (dM + dN) + 4.0 * S * dM * y.ld_part);
@@ -947,16 +977,9 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     else colsum_parts[c->hidx(y.t, y.l - 1)] = grid;
     return st;
   };
-  // a6 through NVLink peer memory: finalise and extras write this rank's bucket into its
-  // exposed buffer (parity of the step's epoch) and the allreduce kernel sums all ranks' into
-  // c->grads.  Otherwise they write c->grads directly (NCCL allreduce in place, or world 1).
-  const bool p2p = apply && c->world > 1 && c->p2p && !ar_overlap();
-  const unsigned long long epoch = p2p ? c->epoch + 1 : 0;
-  const int64_t xoff = (int64_t)(epoch & 1ull) * c->xstride();
-  float* bk = p2p ? c->xbuf + xoff : c->grads;
   // finalise (1/N-scaled split/column-sum reduction into the bucket) layers [lo, hi] (T = 1)
   auto finalize_layers = [&](int lo, int hi) -> srl_status {
-    SegTable all = make_segs(c, splits, colsum_parts, dz_parts), t{};
+    SegTable all = make_segs(c, splits, colsum_parts, dz_parts, reduced), t{};
     double rd = 0;
     for (int l = lo; l <= hi; ++l) {
       t.s[t.n++] = all.s[2 * l];
@@ -1009,7 +1032,7 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
       cur ^= 1;
     }
   }
-  SegTable segs = make_segs(c, splits, colsum_parts, dz_parts);
+  SegTable segs = make_segs(c, splits, colsum_parts, dz_parts, reduced);
   const bool gclip = apply && c->cfg.max_grad_norm > 0.f;
   double part_bytes = 4.0 * dz_parts * hd.in;
   for (int i = 0; i <= HI; ++i)

@@ -42,6 +42,9 @@ struct GemmArgs {
   int stages;                     // operand ring slots (<= 8), from gemm_stages()
   // outputs / epilogue inputs (TANH/DTANH/LOSS write through the output tensor map)
   float* part; int64_t ld_part; int64_t part_split_stride;   // PART
+  // PART with red_out: after a grid barrier the kernel itself sums the k_splits partials (in
+  // split order, L2-hot) into red_out[M][N] scaled by red_scale (the 1/N-scaled gradient)
+  float* red_out; float red_scale; unsigned* red_bar; int red_discard;
   const float* bias;                              // TANH, LOSS
   float* colsum; int colsum_ld;                   // DTANH, LOSS: [grid][colsum_ld]
   unsigned long long* counters;                   // [0] nonfinite, [1] fp16 saturations
@@ -444,6 +447,80 @@ struct OutStage1 {
     ++k;
   }
 };
+
+// ---------------------------------------------------------------------------------------
+// Grid-wide barrier of a persistent launch (grid <= #SMs, one CTA per SM, all co-resident):
+// arrival count + generation word.  bar[0..1], zero-initialised, reusable across launches.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// a5 split-K reduction inside the dW launch (EPI_PART with red_out): every CTA has written its
+// partial, so after the barrier the [M][N] gradient is summed over the k_splits partials in
+// split order -- deterministic -- while they are still in L2, scaled by 1/N and stored into
+// the bucket; the partial lines are then discarded from L2 (never written back to HBM).
+// Warp-strided over float4 quads (N % 4 == 0), 8 split loads in flight per lane.
+static __device__ __noinline__ void part_fixup(const GemmArgs& a) {
+  grid_barrier(a.red_bar);
+  const uint32_t lane = lane_id();
+  const int S = a.k_splits;
+  const int qpr = a.N >> 2;
+  const int64_t nq = (int64_t)a.M * qpr;
+  const int64_t st4 = a.part_split_stride >> 2;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec_out = (reinterpret_cast<uintptr_t>(a.red_out) & 15) == 0;
+  const bool discard = a.red_discard && (qpr & 7) == 0 && (a.ld_part & 31) == 0;
+  uint32_t bad = 0;
+  for (int64_t qb = gw * 32; qb < nq; qb += nw * 32) {
+    const int64_t q = qb + lane;
+    const bool valid = q < nq;
+    const int r = valid ? (int)(q / qpr) : 0, c = valid ? 4 * (int)(q % qpr) : 0;
+    const float4* src = reinterpret_cast<const float4*>(a.part + (int64_t)r * a.ld_part + c);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+      for (int k0 = 0; k0 < S; k0 += 8) {
+        float4 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (k0 + j < S) x[j] = __ldcg(src + (int64_t)(k0 + j) * st4);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (k0 + j < S) { acc.x += x[j].x; acc.y += x[j].y; acc.z += x[j].z; acc.w += x[j].w; }
+      }
+      acc.x *= a.red_scale; acc.y *= a.red_scale; acc.z *= a.red_scale; acc.w *= a.red_scale;
+      bad += !isfinite(acc.x) + !isfinite(acc.y) + !isfinite(acc.z) + !isfinite(acc.w);
+      float* dst = a.red_out + (int64_t)r * a.N + c;
+      if (vec_out) {
+        *reinterpret_cast<float4*>(dst) = acc;
+      } else {
+        dst[0] = acc.x; dst[1] = acc.y; dst[2] = acc.z; dst[3] = acc.w;
+      }
+    }
+    __syncwarp();
+    // the 8 lanes of a 128-byte partial line have read it: drop it from L2 unwritten (only when
+    // rows hold whole lines, so a line's 8 quads are lanes 8j..8j+7 of this iteration)
+    if (discard && valid && (c & 31) == 0)
+      for (int k = 0; k < S; ++k)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(src + (int64_t)k * st4) : "memory");
+  }
+  const uint32_t tot = __reduce_add_sync(0xffffffffu, bad);
+  if (lane == 0 && tot && a.counters) atomicAdd(a.counters, (unsigned long long)tot);
+}
 
 // ---------------------------------------------------------------------------------------
 template <int BN, bool A_MN, bool B_MN, int EPI_KIND, int CG>
@@ -859,6 +936,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_cg<CG>(tmem_base, Cfg::TMEM_COLS);
+  }
+  if constexpr (EPI == EPI_PART) {
+    if (args.red_out) part_fixup(args);   // a5: the split-K sum, in this launch
   }
 }
 

@@ -105,6 +105,7 @@ struct Segment {
   __half* w16;
   int w16_ld;
   float* b32;           // bias only, nullable: fp32 mirror the GEMM epilogue reads (R-AC head)
+  int done;             // weight already reduced into the bucket by its dW launch (part_fixup)
   int64_t item0;        // finalize: first work item (4 partial-buffer entries) of this segment
   int warp;             // finalize: 1 = many splits, one WARP per item (lanes stride the splits)
 };

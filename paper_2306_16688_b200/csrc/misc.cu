@@ -31,7 +31,7 @@ __device__ __forceinline__ uint32_t finalize_w_body(const SegTable& t, int64_t i
   for (int64_t q = q0; q < items; q += qstride) {
     int k = 0;
     for (int i = 0; i < t.n; ++i)
-      if (!t.s[i].is_bias && !t.s[i].warp && q >= t.s[i].item0) k = i;
+      if (!t.s[i].is_bias && !t.s[i].done && !t.s[i].warp && q >= t.s[i].item0) k = i;
     const Segment& s = t.s[k];
     // contiguous extent of a partial row; a transposed (head) partial holds dW^T [in][64] of
     // which this segment's `rows` columns are used
@@ -86,7 +86,7 @@ __device__ __forceinline__ uint32_t finalize_w_warp_body(const SegTable& t, int6
   for (int64_t q = w0; q < witems; q += wstride) {
     int k = -1;
     for (int i = 0; i < t.n; ++i)
-      if (!t.s[i].is_bias && t.s[i].warp && q >= t.s[i].item0) k = i;
+      if (!t.s[i].is_bias && !t.s[i].done && t.s[i].warp && q >= t.s[i].item0) k = i;
     if (k < 0) continue;
     const Segment& s = t.s[k];
     const int prow_len = s.transposed ? min((int)s.ld_part, s.rows) : s.cols;
@@ -189,6 +189,7 @@ static int64_t finalize_items(SegTable& t, int* nbias, int64_t* witems = nullptr
   for (int i = 0; i < t.n; ++i) {
     Segment& g = t.s[i];
     if (g.is_bias) { nb += g.cols; continue; }
+    if (g.done) continue;
     const int64_t prow = g.transposed ? std::min<int64_t>(g.ld_part, g.rows) : g.cols;
     const int64_t nrow = g.transposed ? g.cols : g.rows;      // head partial: [in][64]
     const int64_t cnt = nrow * ((prow + 3) / 4);
@@ -363,23 +364,6 @@ __device__ void write_stats(const float* ex, const double* mean_std, int64_t n_g
                             float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
                             unsigned long long* counters, const double* gnorm, int cerr);
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
 
 __device__ __forceinline__ void update_adam(const UpdateArgs& u, float2& bc, double* red,
                                             int64_t tid, int64_t nthr, int warp, int lane) {
