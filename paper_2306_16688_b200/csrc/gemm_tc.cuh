@@ -770,6 +770,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
         }
       } else if constexpr (EPI == EPI_DTANH) {
+        // dY chunks as 16x256b TMEM fragments (v[16 hf + 4k + 2h + e] = row 16hf + 8h + lane/4,
+        // col 8k + 2(lane%4) + e of the warp's 32x32 block): packed fp32x2 math, and the db
+        // column sums need 4 in-thread rows + a 3-level butterfly instead of a 32x32 transpose
+        // (the head_fused.cu dtanh epilogue).  v := dY .* (Y^2 - 1) = -dZ; the
+        // stores negate the fp16 pairs and the per-CTA sums are negated when written.
+        uint32_t s_off[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s_off[k] = stile_off((int)(lane >> 2), k) + 4 * (lane & 3);
+        const int cs_col = 8 * (2 * (int)((lane >> 4) & 1) + (int)((lane >> 3) & 1)) +
+                           2 * (int)(lane & 3) + (int)((lane >> 2) & 1);
         auto body = [&](int c, float (&v)[32]) {
           const int yb = (ybase + c) % kYSlots;
           if (c + kYSlots - 1 < NCH && lane == 0) {   // keep kYSlots-1 chunks in flight
@@ -781,37 +791,77 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const int col0 = n0 + c * 32;
           wait_bounded(&my_ybar[yb], (yph >> yb) & 1u);
           yph ^= 1u << yb;
-          float y[32];
-          stile_read_row(ystage + yb * kStageTile, (int)lane, y);
-          __syncwarp();
+          const uint32_t ys = smem_u32(ystage + yb * kStageTile);
           float mx = 0.f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            v[j] *= fmaf(-y[j], y[j], 1.f);      // rows >= M: acc = 0, y = 0 -> 0
-            mx = fmaxf(mx, fabsf(v[j]));
-          }
+          for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {       // rows >= M: acc = 0, y = 0 -> 0
+                const uint32_t u = lds32(ys + s_off[k] + (uint32_t)(16 * hf + 8 * h) * 64);
+                const float2 y = __half22float2(*reinterpret_cast<const __half2*>(&u));
+                float& a0 = v[16 * hf + 4 * k + 2 * h];
+                float& a1 = v[16 * hf + 4 * k + 2 * h + 1];
+                mul_sqm1_x2(a0, a1, y.x, y.y);
+                mx = fmaxf(mx, fmaxf(fabsf(a0), fabsf(a1)));
+              }
+          __syncwarp();                            // the y slot may be refilled
           if (mx > 65504.f) {                    // rare: clamp to the fp16 range and count
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = sat_f16(v[j], nsat);
           }
           uint8_t* t = ost.acquire();
-          stile_write_row(t, (int)lane, v);
+          const uint32_t ts = smem_u32(t);
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int i = 16 * hf + 4 * k + 2 * h;
+                sts32(ts + s_off[k] + (uint32_t)(16 * hf + 8 * h) * 64,
+                      pack_half2(v[i], v[i + 1]) ^ 0x80008000u);
+              }
           ost.release(t, &tmO, col0, row0);
           // db column sums of the fp32 values (summing the fp16-rounded tile on the tensor
           // core was measured too imprecise for some bias tensors, and slower)
-          const float s = transpose_reduce32(v);
-          my_colsum[col0 + lane] += s;
+          float c8[8];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float x0 = v[4 * k], x1 = v[4 * k + 1], z0 = v[16 + 4 * k], z1 = v[16 + 4 * k + 1];
+            add_x2(x0, x1, v[4 * k + 2], v[4 * k + 3]);
+            add_x2(z0, z1, v[16 + 4 * k + 2], v[16 + 4 * k + 3]);
+            add_x2(x0, x1, z0, z1);
+            c8[2 * k] = x0;
+            c8[2 * k + 1] = x1;
+          }
+#pragma unroll
+          for (int w = 4; w >= 1; w >>= 1) {
+            const bool up = (lane & (4u * w)) != 0;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+              const float send = up ? c8[i] : c8[i + w];
+              const float keep = up ? c8[i + w] : c8[i];
+              c8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4 * w);
+            }
+          }
+          my_colsum[col0 + cs_col] += c8[0];
+        };
+        auto ld16 = [&](uint32_t ta, float* v) {
+          tmem_ld16x256_x4(ta, v);
+          tmem_ld16x256_x4(ta + (16u << 16), v + 16);
         };
         float b0[32], b1[32];
-        tmem_ld32(taddr, b0);
+        ld16(taddr, b0);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           tc_wait_ld();
           if (c & 1) {
-            if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, b0);
+            if (c + 1 < NCH) ld16(taddr + (c + 1) * 32, b0);
             body(c, b1);
           } else {
-            if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, b1);
+            if (c + 1 < NCH) ld16(taddr + (c + 1) * 32, b1);
             body(c, b0);
           }
         }
@@ -926,7 +976,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int i = ew * 32 + lane; i < args.colsum_ld; i += 256) {
         float x = 0.f;
         for (int w = 0; w < 8; ++w) x += colsum_s[w * args.colsum_ld + i];
-        dst[i] = x;
+        dst[i] = EPI == EPI_DTANH ? -x : x;    // DTANH summed -dZ
       }
     }
   }

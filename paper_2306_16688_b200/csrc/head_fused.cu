@@ -184,6 +184,7 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
       uint64_t* empty = pa ? emptyA : emptyB;
       uint8_t* ring = smem + SL.ring + (pa ? 0 : kRingA * kSlot);
       uint32_t w = 0;
+      const uint64_t pol = pa ? l2_policy_evict_last() : l2_policy_evict_first();
       for (int j = 0; j < m; ++j)
         for (int kb = 0; kb < KB; ++kb, ++w) {
           const int s = w % R;
@@ -195,7 +196,9 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
 #ifdef SRL_HF_EXP_NOA
           if (pa) { mbar_arrive_expect_noop(&full[s]); continue; }    // timing experiment only
 #endif
-          tma_load_2d(ring + s * kSlot, &tmY, &full[s], kb * 64, tile(j) * 128);
+          // pass A marks the tile evict-last so pass B (one tile period later) hits L2; pass
+          // B's read is the last use: evict-first
+          tma_load_2d_hint(ring + s * kSlot, &tmY, &full[s], kb * 64, tile(j) * 128, pol);
         }
     }
   } else if (warp == 1 || warp == 2) {
