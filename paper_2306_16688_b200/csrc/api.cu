@@ -372,7 +372,7 @@ static SegTable make_segs(srl_ctx* c, const std::vector<int>& splits,
       Segment w{};
       w.off = y.w_off; w.rows = y.out; w.cols = y.in; w.is_bias = 0;
       w.part = y.part; w.splits = nsp(i); w.ld_part = y.ld_part;
-      w.split_stride = y.part_rows * y.ld_part; w.transposed = 0;
+      w.split_stride = y.part_rows * y.ld_part; w.transposed = 0; w.prow_cap = (int)y.ld_part;
       w.w16 = y.w16; w.w16_ld = y.w16_ld;
       w.done = reduced.empty() ? 0 : reduced[i];
       t.s[t.n++] = w;
@@ -391,6 +391,7 @@ static SegTable make_segs(srl_ctx* c, const std::vector<int>& splits,
     w.off = off; w.rows = rows; w.cols = hL; w.is_bias = 0;
     w.part = hd.part + (int64_t)row0 * hd.ld_part + col0; w.splits = nsp(hi);
     w.ld_part = hd.ld_part; w.split_stride = hd.part_rows * hd.ld_part; w.transposed = 1;
+    w.prow_cap = (int)hd.ld_part - col0;
     w.w16 = hd.w16 + (int64_t)col0 * hd.w16_ld + row0; w.w16_ld = hd.w16_ld;
     t.s[t.n++] = w;
   };

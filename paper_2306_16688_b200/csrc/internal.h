@@ -99,6 +99,8 @@ struct Segment {
   int splits;
   int64_t ld_part, split_stride;
   int transposed;       // head: partial holds dW^T ([in][G])
+  int prow_cap;         // floats readable from a partial row's first used entry (<= ld_part):
+                        // a 4-wide load at any used column stays inside the allocation
   const float* colsum;  // bias: [nparts][colsum_ld]
   int nparts, colsum_ld;
   // fp16 shadow (weights only)
@@ -107,6 +109,7 @@ struct Segment {
   float* b32;           // bias only, nullable: fp32 mirror the GEMM epilogue reads (R-AC head)
   int done;             // weight already reduced into the bucket by its dW launch (part_fixup)
   int64_t item0;        // finalize: first work item (4 partial-buffer entries) of this segment
+  int64_t aq0;          // Adam (update_kernel): first quad of this segment in the flat space
   int warp;             // finalize: 1 = many splits, one WARP per item (lanes stride the splits)
 };
 constexpr int kMaxSegs = 20;
@@ -129,7 +132,7 @@ constexpr int kGradNormBlocks = 296;   // 2 x 148 SMs
 // then (if `stats`) the step's statistics
 struct UpdateArgs {
   SegTable t;
-  int64_t P, items, witems, nbias;
+  int64_t P, items, witems, nbias, aquads;
   float inv_n;
   float* bucket;
   unsigned long long* counters;

@@ -41,7 +41,9 @@ __device__ __forceinline__ uint32_t finalize_w_body(const SegTable& t, int64_t i
     const int pr = (int)(qi / per_row), pc = 4 * (int)(qi % per_row);
     const float* src = s.part + (int64_t)pr * s.ld_part + pc;
     float a[4] = {0.f, 0.f, 0.f, 0.f};
-    if ((s.ld_part & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pc + 4 <= prow_len) {
+    // 4-wide loads also for a row's last, partial quad (the entries past prow_len are read
+    // from the allocation and dropped below)
+    if ((s.ld_part & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pc + 4 <= s.prow_cap) {
       const float4* s4 = reinterpret_cast<const float4*>(src);
       const int64_t st4 = s.split_stride / 4;
       for (int k0 = 0; k0 < s.splits; k0 += 20) {   // 20 loads in flight, summed in split order
@@ -96,7 +98,7 @@ __device__ __forceinline__ uint32_t finalize_w_warp_body(const SegTable& t, int6
     const float* src = s.part + (int64_t)pr * s.ld_part + pc;
     const int cnt = min(4, prow_len - pc);
     float a[4] = {0.f, 0.f, 0.f, 0.f};
-    if ((s.ld_part & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && cnt == 4) {
+    if ((s.ld_part & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && pc + 4 <= s.prow_cap) {
       for (int sp0 = lane; sp0 < s.splits; sp0 += 256) {     // 8 loads in flight per lane
         float4 x[8];
 #pragma unroll
@@ -109,8 +111,18 @@ __device__ __forceinline__ uint32_t finalize_w_warp_body(const SegTable& t, int6
         for (int j = 0; j < 8; ++j) { a[0] += x[j].x; a[1] += x[j].y; a[2] += x[j].z; a[3] += x[j].w; }
       }
     } else {
-      for (int sp = lane; sp < s.splits; sp += 32)
-        for (int e = 0; e < cnt; ++e) a[e] += __ldg(src + (int64_t)sp * s.split_stride + e);
+      for (int sp0 = lane; sp0 < s.splits; sp0 += 256) {     // 8 splits in flight per lane
+        float x[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            x[j][e] = (sp0 + 32 * j < s.splits && e < cnt) ? __ldg(src + (int64_t)(sp0 + 32 * j) * s.split_stride + e) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a[e] += x[j][e];
+      }
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e)
@@ -193,7 +205,11 @@ static int64_t finalize_items(SegTable& t, int* nbias, int64_t* witems = nullptr
     const int64_t prow = g.transposed ? std::min<int64_t>(g.ld_part, g.rows) : g.cols;
     const int64_t nrow = g.transposed ? g.cols : g.rows;      // head partial: [in][64]
     const int64_t cnt = nrow * ((prow + 3) / 4);
-    g.warp = (witems && g.splits > 32) ? 1 : 0;
+    // a warp per item (lanes stride the splits) only for FEW items with many splits (the head's
+    // per-CTA partials): with many items one thread per item and 20 splits in flight keeps
+    // every thread busy, while a warp walking 20+ items one after another is latency-bound
+    // (gFootball's 74-split hidden layers: 42 us -> see DESIGN.md §5)
+    g.warp = (witems && g.splits > 32 && cnt <= 8192) ? 1 : 0;
     if (g.warp) { g.item0 = wit; wit += cnt; }
     else { g.item0 = items; items += cnt; }
   }
@@ -262,19 +278,18 @@ __device__ __forceinline__ float2 adam_bias_corr(float lr, float b1, float b2, d
 }
 
 // Adam over segment s for quads q = q0, q0 + qstride, ... with the step's bias corrections
-__device__ __forceinline__ void adam_seg_body(const Segment& s, float* __restrict__ p,
-                                              float* __restrict__ m, float* __restrict__ v,
-                                              const float* __restrict__ g, float step_size,
-                                              float bc2_sqrt, float b1, float b2, float eps,
-                                              float cf, int64_t q0, int64_t qstride) {
+// Adam for quad q (entries 4q .. 4q+3) of segment s
+__device__ __forceinline__ void adam_quad(const Segment& s, int64_t q, float* __restrict__ p,
+                                          float* __restrict__ m, float* __restrict__ v,
+                                          const float* __restrict__ g, float step_size,
+                                          float bc2_sqrt, float b1, float b2, float eps,
+                                          float cf) {
   const int cnt = s.rows * s.cols;
-  const int64_t nq = (cnt + 3) >> 2;
-  if (q0 >= nq) return;
   const bool vec_w16 = !s.is_bias && (s.cols & 3) == 0 && (s.w16_ld & 3) == 0;
   // float4 only where the segment starts 16-byte aligned (every segment of the shared layout;
   // the separate-trunk layout (R-AC) puts the critic after b_pi[A], A arbitrary)
   const bool vec = (s.off & 3) == 0;
-  for (int64_t q = q0; q < nq; q += qstride) {
+  {
     const int e0 = 4 * (int)q;
     const int64_t i0 = s.off + e0;
     if (vec && e0 + 4 <= cnt) {
@@ -321,6 +336,16 @@ __device__ __forceinline__ void adam_seg_body(const Segment& s, float* __restric
       }
     }
   }
+}
+
+__device__ __forceinline__ void adam_seg_body(const Segment& s, float* __restrict__ p,
+                                              float* __restrict__ m, float* __restrict__ v,
+                                              const float* __restrict__ g, float step_size,
+                                              float bc2_sqrt, float b1, float b2, float eps,
+                                              float cf, int64_t q0, int64_t qstride) {
+  const int64_t nq = ((int64_t)s.rows * s.cols + 3) >> 2;
+  for (int64_t q = q0; q < nq; q += qstride)
+    adam_quad(s, q, p, m, v, g, step_size, bc2_sqrt, b1, b2, eps, cf);
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(const SegTable t, int64_t P,
@@ -404,13 +429,29 @@ __device__ __forceinline__ void update_adam(const UpdateArgs& u, float2& bc, dou
   __syncthreads();                                 // bc
   if (skip) return;
   const float2 b = bc;
-  for (int i = 0; i < u.t.n; ++i)
-    adam_seg_body(u.t.s[i], u.p, u.m, u.v, g, b.x, b.y, u.b1, u.b2, u.eps, cf, tid, nthr);
+  // one flat quad space over all segments (Segment::aq0 prefix offsets): each thread takes
+  // its ~P/4/#threads quads whichever segments they fall in, instead of one pass per segment
+  for (int64_t q = tid; q < u.aquads; q += nthr) {
+    int k = 0;
+    for (int i = 1; i < u.t.n; ++i)
+      if (q >= u.t.s[i].aq0) k = i;
+    adam_quad(u.t.s[k], q - u.t.s[k].aq0, u.p, u.m, u.v, g, b.x, b.y, u.b1, u.b2, u.eps, cf);
+  }
 }
+
+#ifdef SRL_UPD_TRACE
+// tools/upd_trace.py: per-block clock64 marks of update_kernel phases (variant builds only)
+__device__ long long g_upd_trace[256 * 8];
+#define UPD_MARK(k) do { __syncthreads(); if (threadIdx.x == 0) g_upd_trace[blockIdx.x * 8 + (k)] = (long long)globaltimer_ns(); } while (0)
+#else
+#define UPD_MARK(k) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
   griddep_launch();
+  UPD_MARK(0);
   griddep_wait();
+  UPD_MARK(1);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -420,9 +461,12 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
     bc = adam_bias_corr(u.lr, u.b1, u.b2, (double)(u.t_dev[0] + 1));
   if (u.finalize) {
     uint32_t bad = finalize_w_body(u.t, u.items, u.inv_n, u.bucket, tid, nthr);
+    UPD_MARK(2);
     const int64_t gw = tid >> 5, nw = nthr >> 5;
     bad += finalize_w_warp_body(u.t, u.witems, u.inv_n, u.bucket, gw, nw) * (lane == 0);
+    UPD_MARK(6);
     for (int64_t e = gw; e < u.nbias; e += nw) bad += finalize_b_one(u.t, (int)e, u.inv_n, u.bucket) && lane == 0;
+    UPD_MARK(7);
     const uint32_t tot = __reduce_add_sync(0xffffffffu, bad);
     if (lane == 0 && tot) atomicAdd(u.counters, (unsigned long long)tot);
     if (blockIdx.x == 0 && warp < 5) {             // loss statistics / N
@@ -432,7 +476,9 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
       for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
       if (lane == 0) u.bucket[u.P + warp] = (float)(x * (double)u.inv_n);
     }
+    UPD_MARK(3);
     grid_barrier(u.bar);
+    UPD_MARK(4);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       u.bucket[u.P + 5] = (float)u.counters[0];
       u.bucket[u.P + 6] = (float)u.counters[1];
@@ -440,6 +486,7 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
     }
   }
   if (u.adam) update_adam(u, bc, red, tid, nthr, warp, lane);
+  UPD_MARK(5);
   if (u.stats) {
     // the step's statistics by the LAST block to get here: every block has read t and the
     // counters by then, and block 0's extras / norm writes precede its arrival
@@ -460,6 +507,12 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
 cudaError_t launch_update(UpdateArgs u, cudaStream_t s) {
   int nb = 0;
   int64_t wit = 0;
+  int64_t aq = 0;
+  for (int i = 0; i < u.t.n; ++i) {
+    u.t.s[i].aq0 = aq;
+    aq += ((int64_t)u.t.s[i].rows * u.t.s[i].cols + 3) / 4;
+  }
+  u.aquads = aq;
   u.items = finalize_items(u.t, &nb, &wit);
   u.witems = wit;
   u.nbias = nb;
@@ -691,3 +744,9 @@ cudaError_t launch_stats(const float* bucket, int64_t P, const double* mean_std,
 }
 
 }  // namespace srl
+
+#ifdef SRL_UPD_TRACE
+extern "C" int srl_debug_upd_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, srl::g_upd_trace, sizeof(srl::g_upd_trace)) != cudaSuccess;
+}
+#endif
