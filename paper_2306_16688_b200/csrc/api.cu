@@ -287,6 +287,12 @@ static bool dw_fixup_enabled() {
   return e && e[0] == '1';
 }
 
+// SRL_XFUSED=0: the peer-path exchange as its own launch between two update launches
+static bool xfused_enabled() {
+  const char* e = getenv("SRL_XFUSED");
+  return !(e && e[0] == '0');
+}
+
 static bool dw_discard_enabled() {
   const char* e = getenv("SRL_DW_DISCARD");
   return !(e && e[0] == '0');
@@ -1057,7 +1063,28 @@ extern "C" srl_status srl_ppo_step(srl_ctx* c, int64_t n_local, int64_t n_global
     CK(launch_update(u, s));
     return SRL_OK;
   };
-  if (!overlap) {
+  if (!overlap && p2p && xfused_enabled()) {
+    // world > 1 over peer memory: ONE launch -- finalise into the exposed bucket, the two-shot
+    // exchange into c->grads, [norm], Adam, statistics (misc.cu update_kernel, `xchg`)
+    UpdateArgs u{};
+    u.t = segs; u.P = c->P; u.inv_n = inv_n; u.bucket = bk; u.counters = c->counters;
+    u.stats_part = c->stats_part; u.nstats = grid_loss;
+    u.finalize = 1; u.adam = 1; u.stats = 1; u.apply = apply;
+    u.g = c->grads; u.p = c->params; u.m = c->m; u.v = c->v; u.t_dev = c->t_dev;
+    u.lr = c->cfg.lr; u.b1 = c->cfg.beta1; u.b2 = c->cfg.beta2; u.eps = c->cfg.adam_eps;
+    u.max_norm = gclip ? c->cfg.max_grad_norm : 0.f;
+    u.gn_part = c->gn; u.gn_norm = c->gn_norm(); u.gn_coef = c->gn_coef();
+    u.comm_err = c->cc.err_dev;
+    u.bar = c->gbar;
+    u.mean_std = adv_mean_std; u.n_global = n_global;
+    u.cv = c->cfg.value_coef; u.ce = c->cfg.entropy_coef; u.out = stats_out;
+    u.xchg = 1; u.world = c->world; u.rank = c->rank; u.pe = c->peers; u.cc = c->cc;
+    u.xoff = xoff; u.epoch = epoch; u.xout = c->grads;
+    c->epoch = epoch;
+    ProfScope ps(c, s, "grad_update_x", 0.0,
+                 part_bytes + 4.0 * (c->P + 8) * 2.0 * (c->world - 1) / c->world + 30.0 * c->P);
+    CK(launch_update(u, s));
+  } else if (!overlap) {
     // world 1: ONE launch from the partials to the updated parameters; world > 1: finalise
     // into the bucket the exchange reads, exchange, then the norm + Adam launch
     // the last launch also writes the step's statistics (its last block)

@@ -126,37 +126,6 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
                         float b2, float eps, cudaStream_t s, const float* coef = nullptr,
                         const int* comm_err = nullptr);
 constexpr int kGradNormBlocks = 296;   // 2 x 148 SMs
-// a5 tail + a7 in one persistent launch (misc.cu update_kernel): finalise (if `finalize`) the
-// partials into `bucket` with the loss statistics, then (if `adam`) the optional global-norm
-// clip and Adam + fp16 shadow reading `g` (== bucket at world 1, the reduced bucket otherwise),
-// then (if `stats`) the step's statistics
-struct UpdateArgs {
-  SegTable t;
-  int64_t P, items, witems, nbias, aquads;
-  float inv_n;
-  float* bucket;
-  unsigned long long* counters;
-  const double* stats_part;
-  int nstats;
-  int finalize, adam;
-  const float* g;
-  float *p, *m, *v;
-  int64_t* t_dev;
-  float lr, b1, b2, eps, max_norm;
-  double* gn_part;          // [>= #SMs]
-  double* gn_norm;
-  float* gn_coef;
-  const int* comm_err;
-  unsigned* bar;            // grid barrier words [3], zero-initialised ([2]: blocks done)
-  // the step's last launch (`stats`): its last block writes srl_ppo_stats from g[P..P+8),
-  // advances t if Adam ran, re-zeroes the counters (what stats_kernel does standalone)
-  int stats, apply;
-  const double* mean_std;
-  int64_t n_global;
-  float cv, ce;
-  srl_ppo_stats* out;
-};
-cudaError_t launch_update(UpdateArgs u, cudaStream_t s);
 // a6 over NVLink peer memory (world <= 8 on one node): every rank's exposed bucket (double
 // buffered by step parity) and flag array, mapped into this process with CUDA IPC
 constexpr int kMaxPeers = 8;
@@ -187,6 +156,46 @@ struct CommCtl {
   int* err_host;                // device alias of pinned host memory, read by the host
   unsigned long long timeout_ns;
 };
+
+// a5 tail + a7 in one persistent launch (misc.cu update_kernel): finalise (if `finalize`) the
+// partials into `bucket` with the loss statistics, then (if `adam`) the optional global-norm
+// clip and Adam + fp16 shadow reading `g` (== bucket at world 1, the reduced bucket otherwise),
+// then (if `stats`) the step's statistics
+struct UpdateArgs {
+  SegTable t;
+  int64_t P, items, witems, nbias, aquads;
+  float inv_n;
+  float* bucket;
+  unsigned long long* counters;
+  const double* stats_part;
+  int nstats;
+  int finalize, adam;
+  const float* g;
+  float *p, *m, *v;
+  int64_t* t_dev;
+  float lr, b1, b2, eps, max_norm;
+  double* gn_part;          // [>= #SMs]
+  double* gn_norm;
+  float* gn_coef;
+  const int* comm_err;
+  unsigned* bar;            // grid barrier words [3], zero-initialised ([2]: blocks done)
+  // the step's last launch (`stats`): its last block writes srl_ppo_stats from g[P..P+8),
+  // advances t if Adam ran, re-zeroes the counters (what stats_kernel does standalone)
+  int stats, apply;
+  const double* mean_std;
+  int64_t n_global;
+  float cv, ce;
+  srl_ppo_stats* out;
+  // xchg: world > 1 over NVLink peer memory -- the a6 exchange between finalise and Adam in
+  // this launch (grid = #SMs on every rank: the same sub-block partition everywhere)
+  int xchg, world, rank;
+  P2PPeers pe;
+  CommCtl cc;
+  int64_t xoff;
+  unsigned long long epoch;
+  float* xout;
+};
+cudaError_t launch_update(UpdateArgs u, cudaStream_t s);
 // phases: bit 0 = publish / reduce my chunk, bit 1 = gather the other chunks (3 = both; the
 // single-GPU virtual-rank test runs bit 0 for every rank, then bit 1 for every rank).
 cudaError_t launch_p2p_moments(const P2PPeers& pe, int world, int rank, unsigned long long epoch,

@@ -388,13 +388,19 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
 __device__ void write_stats(const float* ex, const double* mean_std, int64_t n_global, float cv,
                             float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
                             unsigned long long* counters, const double* gnorm, int cerr);
+__device__ bool p2p_exchange_body(const P2PPeers& pe, int world, int rank, int64_t off,
+                                  int64_t count, unsigned long long epoch, float scale,
+                                  float* __restrict__ out, const CommCtl& cc, int phases,
+                                  bool publish);
 
 
 __device__ __forceinline__ void update_adam(const UpdateArgs& u, float2& bc, double* red,
                                             int64_t tid, int64_t nthr, int warp, int lane) {
   const float* g = u.g;
-  const bool skip = (u.finalize ? (*reinterpret_cast<volatile unsigned long long*>(u.counters) > 0)
-                                : (g[u.P + 5] > 0.f)) || (u.comm_err && *u.comm_err);
+  // the local non-finite count at world 1; the reduced bucket's (every rank's) otherwise
+  const bool skip = ((u.finalize && !u.xchg) ? (*reinterpret_cast<volatile unsigned long long*>(u.counters) > 0)
+                                             : (__ldcg(g + u.P + 5) > 0.f)) ||
+                    (u.comm_err && *reinterpret_cast<volatile const int*>(u.comm_err));
   float cf = 1.f;
   if (u.max_norm > 0.f) {                          // NEXT-3: global norm of the (reduced) bucket
     double acc = 0.0;
@@ -477,6 +483,7 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
       if (lane == 0) u.bucket[u.P + warp] = (float)(x * (double)u.inv_n);
     }
     UPD_MARK(3);
+    if (u.xchg) __threadfence_system();            // this block's bucket entries, for the peers
     grid_barrier(u.bar);
     UPD_MARK(4);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -484,6 +491,18 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
       u.bucket[u.P + 6] = (float)u.counters[1];
       u.bucket[u.P + 7] = 0.f;
     }
+  }
+  if (u.xchg) {
+    // a6 in the same launch (world > 1, NVLink peer memory): block 0 publishes the bucket once
+    // its extras are written (the other blocks wait on that flag like any rank's), then the
+    // two-shot rank-order sum of p2p_allreduce_kernel over this grid; a barrier before Adam
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x < u.world) {
+      __threadfence_system();
+      st_release_sys(u.pe.flag[threadIdx.x] + u.rank, u.epoch);
+    }
+    p2p_exchange_body(u.pe, u.world, u.rank, u.xoff, u.P + 8, u.epoch, 1.f, u.xout, u.cc, 3, false);
+    grid_barrier(u.bar);
   }
   if (u.adam) update_adam(u, bc, red, tid, nthr, warp, lane);
   UPD_MARK(5);
@@ -612,25 +631,25 @@ __device__ __forceinline__ void sum_range(const P2PPeers& pe, int world, int64_t
   }
 }
 
-__global__ void __launch_bounds__(512) p2p_allreduce_kernel(const P2PPeers pe, int world, int rank,
-                                                            int64_t off, int64_t count,
-                                                            unsigned long long epoch, float scale,
-                                                            float* __restrict__ out,
-                                                            const CommCtl cc, int phases) {
-  griddep_wait();
-  griddep_launch();
+// The two phases for block g of G; `publish` = block 0 also publishes this rank's bucket
+// (the standalone kernel; the fused update launch publishes after its extras).  Returns false
+// after a comm timeout (the error words are raised; the caller skips the rest, no early exit).
+__device__ bool p2p_exchange_body(const P2PPeers& pe, int world, int rank, int64_t off,
+                                  int64_t count, unsigned long long epoch, float scale,
+                                  float* __restrict__ out, const CommCtl& cc, int phases,
+                                  bool publish) {
   __shared__ int s_ok;
   const int g = blockIdx.x, G = gridDim.x;
   if (threadIdx.x == 0) s_ok = 1;
   __syncthreads();
   if (phases & 1) {
-    if (g == 0 && threadIdx.x < world) {
+    if (publish && g == 0 && threadIdx.x < world) {
       __threadfence_system();
       st_release_sys(pe.flag[threadIdx.x] + rank, epoch);
     }
     if (threadIdx.x < world && !wait_epoch(pe.flag[rank] + threadIdx.x, epoch, cc)) s_ok = 0;
     __syncthreads();
-    if (!s_ok) return;
+    if (!s_ok) return false;
     const int64_t c0 = split4(count, rank, world), c1 = split4(count, rank + 1, world);
     const int64_t lo = c0 + split4(c1 - c0, g, G), hi = c0 + split4(c1 - c0, g + 1, G);
     sum_range(pe, world, off, lo, hi, scale, out, pe.x[rank] + off);
@@ -646,7 +665,7 @@ __global__ void __launch_bounds__(512) p2p_allreduce_kernel(const P2PPeers pe, i
       if (threadIdx.x == 0 && !wait_epoch(p2p_rflags(pe.flag[rank]) + j * kXBlocks + g, epoch, cc))
         s_ok = 0;
       __syncthreads();
-      if (!s_ok) return;
+      if (!s_ok) return false;
       const int64_t c0 = split4(count, j, world), c1 = split4(count, j + 1, world);
       const int64_t lo = c0 + split4(c1 - c0, g, G), hi = c0 + split4(c1 - c0, g + 1, G);
       const float* src = pe.x[j] + off;
@@ -656,6 +675,17 @@ __global__ void __launch_bounds__(512) p2p_allreduce_kernel(const P2PPeers pe, i
         if (i >= lo) out[i] = __ldcg(src + i);
     }
   }
+  return true;
+}
+
+__global__ void __launch_bounds__(512) p2p_allreduce_kernel(const P2PPeers pe, int world, int rank,
+                                                            int64_t off, int64_t count,
+                                                            unsigned long long epoch, float scale,
+                                                            float* __restrict__ out,
+                                                            const CommCtl cc, int phases) {
+  griddep_wait();
+  griddep_launch();
+  p2p_exchange_body(pe, world, rank, off, count, epoch, scale, out, cc, phases, true);
 }
 
 cudaError_t launch_p2p_allreduce(const P2PPeers& pe, int world, int rank, int64_t off,
