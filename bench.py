@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--minibatches", type=int, default=1)
     ap.add_argument("--value-clip", type=float, default=0.0)
     ap.add_argument("--max-grad-norm", type=float, default=0.0)
+    ap.add_argument("--separate-critic", action="store_true",
+                    help="NEXT-3 R-AC: separate actor and critic trunks (DESIGN.md §3.5)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="default: strong for N > 1 (the config batch split B/K, SURVEY C-A16)")
     ap.add_argument("--no-alt-scaling", action="store_true")
@@ -195,6 +197,8 @@ def reference_arm(args, world, rank):
     its block driver), same metric / unit / config as our arm."""
     import synth
     cfg = synth.get_config(args.config)
+    if args.separate_critic:
+        cfg = cfg.with_(separate_critic=True)
     if rank != 0:
         return
     import oracle
@@ -368,6 +372,8 @@ def main_ours(args, world, rank, local):
         return ms, ctx.prof_records()
 
     cfg = synth.get_config(args.config)
+    if args.separate_critic:
+        cfg = cfg.with_(separate_critic=True)
     # strong: the config's batch is the GLOBAL batch, split B/K over the ranks (C-A16);
     # weak: every rank holds a full config-sized shard (the global batch grows with K)
     gcfg = cfg if scaling == "strong" else cfg.with_(B=cfg.B * world)
@@ -524,6 +530,7 @@ def main_ours(args, world, rank, local):
                    "grad_allreduce": comm_path,
                    "epochs": max(1, args.epochs), "minibatches": max(1, args.minibatches),
                    "value_clip": args.value_clip, "max_grad_norm": args.max_grad_norm,
+                   "separate_critic": bool(args.separate_critic),
                    "l2": "no flush: per-step working set > L2 (obs %.0f MB + activations %.0f MB + "
                          "dZ %.0f MB per rank vs 126 MB L2)" % (
                              n * cfg.ld_obs * 2 / 1e6, n * sum(cfg.hidden) * 2 / 1e6,

@@ -2,11 +2,11 @@
 //
 // GAE (BASELINE.json north_star):
 //   m_t = 1 - d_t;  delta_t = r_t + gamma v_{t+1} m_t - v_t;  A_t = delta_t + gamma lambda m_t A_{t+1}
-// computed exactly as written: one thread per env column runs the recursion from t = T-1 down
-// to 0 (the result is bit-identical to the sequential definition, C-B1..C-B5).  The scan is
-// HBM-bound: 17 B per sample (r, v, d in; adv, ret out); a double-buffered register prefetch of
-// 16 rows per thread keeps the loads in flight (round 2; the round-1 chunked-T scan was
-// barrier- and occupancy-bound, 0.28 of HBM at SMAC under ncu).
+// as a chunked affine scan over T (gae_kernel below): each warp loads a 16-row chunk of 32
+// columns once into registers, the chunks' (a, P) summaries are folded into carries, and the
+// exact recursion then runs from the carry (integer data with gamma = lambda = 1 stays
+// bit-exact, C-B1..C-B5; floating data differs from the sequential order by rounding only).
+// The scan is HBM-bound: 17 B per sample (r, v, d in; adv, ret out).
 // NEXT-3: a flag byte with (flag & 3) == 2 (bit 1 set, bit 0 clear) is a time-limit truncation
 // (reading R-T): with trunc values the cut step bootstraps from them; a valid mask (reading R-P)
 // leaves padding entries out of the moments (adv/ret are still written for every entry).

@@ -298,7 +298,7 @@ class PPOContext:
         if valid is not None:
             _cuda(valid, torch.uint8, "valid", numel=n_local)
         if stats is None:
-            stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
+            stats = torch.empty(STATS_BYTES, dtype=torch.uint8, device=obs.device)   # fully written
         _check(lib().srl_ppo_step(self.handle, n_local, int(n_global), _ptr(obs), _ptr(actions),
                                   _ptr(logp_old), _ptr(adv), _ptr(ret), _ptr(v_old), _ptr(valid),
                                   _ptr(adv_mean_std),
@@ -337,7 +337,7 @@ class PPOContext:
         if valid is not None:
             _cuda(valid, torch.uint8, "valid", numel=n)
         if stats is None:
-            stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=obs.device)
+            stats = torch.empty(STATS_BYTES, dtype=torch.uint8, device=obs.device)   # fully written
         _check(lib().srl_ppo_train_step(self.handle, T, B, int(n_global), _ptr(rewards),
                                         _ptr(values), _ptr(dones), _ptr(trunc_values),
                                         _ptr(valid), _ptr(obs), _ptr(actions),
@@ -365,7 +365,7 @@ class PPOContext:
 
     def train_step_slot(self, slot, n_global, stats=None, stream=None):
         if stats is None:
-            stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=f"cuda:{self.device}")
+            stats = torch.empty(STATS_BYTES, dtype=torch.uint8, device=f"cuda:{self.device}")   # fully written
         _check(lib().srl_ppo_train_step_slot(self.handle, slot, int(n_global), _ptr(stats),
                                              _stream(stream)))
         return stats
