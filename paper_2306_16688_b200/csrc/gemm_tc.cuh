@@ -432,6 +432,7 @@ struct OutStage {
 struct OutStage1 {
   uint8_t* buf;
   int k;
+  uint64_t policy;   // 0: no L2 hint; else a createpolicy value for the stores
   __device__ __forceinline__ uint8_t* acquire() {
     if (k > 0 && lane_id() == 0) bulk_wait_read<0>();
     __syncwarp();
@@ -441,7 +442,8 @@ struct OutStage1 {
     fence_proxy_async_smem();
     __syncwarp();
     if (lane_id() == 0) {
-      tma_store_2d(map, t, col, row);
+      if (policy) tma_store_2d_hint(map, t, col, row, policy);
+      else tma_store_2d(map, t, col, row);
       bulk_commit();
     }
     ++k;
