@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -102,7 +103,22 @@ extern "C" srl_status srl_gae(int T, int B, int ld, const float* rewards, const 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   double* part = nullptr;
   const int nb = gae_num_blocks(B);
-  if (stats_out) CK(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * 3 * nb, s));
+  if (stats_out) {
+    // the per-call moment partials come from the device's stream-ordered pool; keep its memory
+    // (release threshold = max) so steady-state calls neither map nor unmap pages
+    static std::atomic<uint64_t> pool_set{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 &&
+        !(pool_set.load(std::memory_order_relaxed) & (1ull << dev))) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_set.fetch_or(1ull << dev, std::memory_order_relaxed);
+    }
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * 3 * nb, s));
+  }
   CK(launch_gae(T, B, ld, rewards, values, dones, trunc_values, valid, gamma, lambda, adv_out,
                 ret_out, part, s));
   if (stats_out) {
