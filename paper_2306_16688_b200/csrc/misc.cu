@@ -447,8 +447,8 @@ __device__ __forceinline__ void update_adam(const UpdateArgs& u, float2& bc, dou
 
 #ifdef SRL_UPD_TRACE
 // tools/upd_trace.py: per-block clock64 marks of update_kernel phases (variant builds only)
-__device__ long long g_upd_trace[256 * 8];
-#define UPD_MARK(k) do { __syncthreads(); if (threadIdx.x == 0) g_upd_trace[blockIdx.x * 8 + (k)] = (long long)globaltimer_ns(); } while (0)
+__device__ long long g_upd_trace[256 * 12];
+#define UPD_MARK(k) do { __syncthreads(); if (threadIdx.x == 0) g_upd_trace[blockIdx.x * 12 + (k)] = (long long)globaltimer_ns(); } while (0)
 #else
 #define UPD_MARK(k) do { } while (0)
 #endif
@@ -483,7 +483,9 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
       if (lane == 0) u.bucket[u.P + warp] = (float)(x * (double)u.inv_n);
     }
     UPD_MARK(3);
-    if (u.xchg) __threadfence_system();            // this block's bucket entries, for the peers
+    // (no per-block fence.sys: the blocks' bucket writes reach the peers through the barrier's
+    // gpu-scope release/acquire and block 0's fence.sys + release store of the publish flag --
+    // causality composes; a fence.sys in all 148 blocks cost ~5 us at 4 ranks)
     grid_barrier(u.bar);
     UPD_MARK(4);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -502,7 +504,9 @@ __global__ void __launch_bounds__(512) update_kernel(const UpdateArgs u) {
       st_release_sys(u.pe.flag[threadIdx.x] + u.rank, u.epoch);
     }
     p2p_exchange_body(u.pe, u.world, u.rank, u.xoff, u.P + 8, u.epoch, 1.f, u.xout, u.cc, 3, false);
+    UPD_MARK(8);
     grid_barrier(u.bar);
+    UPD_MARK(9);
   }
   if (u.adam) update_adam(u, bc, red, tid, nthr, warp, lane);
   UPD_MARK(5);

@@ -26,12 +26,12 @@ ctx = P.PPOContext(P.NetSpec.from_config(cfg), max_local_n=b["n"])
 ctx.load_params(torch.from_numpy(synth.make_params(cfg, 0)).to(dev))
 fn = srl.lib().srl_debug_upd_trace
 fn.argtypes = [ctypes.c_void_p]
-buf = np.zeros(256 * 8, dtype=np.int64)
+buf = np.zeros(256 * 12, dtype=np.int64)
 for _ in range(4):
     ctx.train_step(b["n"], b["rewards"], b["values"], b["dones"], b["obs"], b["actions"], b["logp_old"])
 torch.cuda.synchronize()
 fn(buf.ctypes.data)
-t = buf.reshape(256, 8)[:148].astype(np.float64)
+t = buf.reshape(256, 12)[:148].astype(np.float64)
 t0 = t[:, 0].min()
 for k, nm in [(0, "start"), (1, "griddep_wait"), (2, "weights"), (6, "weight warp items"),
               (7, "biases"), (3, "stats"), (4, "barrier"), (5, "adam")]:
