@@ -22,6 +22,10 @@ def _port():
 
 def _worker(rank, world, port, q, p2p="1", steps=1):
     import sys
+    # "1u": the peer path with the exchange as its own launch between two update launches
+    # (SRL_XFUSED=0) instead of inside the update launch
+    os.environ["SRL_XFUSED"] = "0" if p2p == "1u" else "1"
+    p2p = "1" if p2p == "1u" else p2p
     os.environ["SRL_P2P_AR"] = p2p
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -114,6 +118,21 @@ def test_p2p_allreduce_equals_nccl_over_steps(world):
     d = np.abs(a[0][2].astype(np.float64) - b[0][2].astype(np.float64))
     assert d.max() <= 2 * 3e-4 * 3 + 1e-6 and np.mean(d > 1e-5) <= 1e-3
     assert a[0][1]["step"] == 1 and b[0][1]["step"] == 1
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_exchange_equals_three_launches(world):
+    """The a6 exchange inside the update launch (default) and as its own launch between the
+    finalise and Adam launches (SRL_XFUSED=0) do the same arithmetic (rank-order sum per entry,
+    whatever the sub-block partition): bit-identical gradients and parameters after 3 steps."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    a = _run(world, "1", steps=3)
+    b = _run(world, "1u", steps=3)
+    assert a[0][4] == "nvlink-p2p" and b[0][4] == "nvlink-p2p"
+    for ra, rb in zip(a, b):
+        assert np.array_equal(ra[3], rb[3]) and np.array_equal(ra[2], rb[2])
+        assert ra[1]["step"] == rb[1]["step"] == 1 and ra[1]["comm_error"] == 0
 
 
 def _api_worker(rank, world, port, q, p2p):
