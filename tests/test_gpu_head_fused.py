@@ -51,6 +51,24 @@ def test_fused_head_vs_oracle_and_unfused(name, B, T):
     assert f["stats"]["nonfinite"] == 0 and f["stats"]["fp16_saturated"] == 0
 
 
+@pytest.mark.parametrize("B,T", [(8, 100), (40, 160)])
+def test_fused_head_multi_head(B, T):
+    """Several categorical heads (the shared-memory loss path of the fused kernel; every
+    BASELINE config that fuses has one head): HnS-style heads [11, 11, 2, 2] (A + 1 = 27 <= 32)
+    on a 256-wide trunk, ragged row counts, one and several tiles per CTA."""
+    cfg = synth.get_config("hns").with_(hidden=(256, 256), heads=(11, 11, 2, 2), B=B, T=T)
+    params, b = make_inputs(cfg, seed=61)
+    f = _run(cfg, params, b, True)
+    u = _run(cfg, params, b, False)
+    o = oracle.ppo_step(cfg, params, [b], apply=False)
+    P = cfg.n_params
+    _cmp(cfg, f["bucket"][:P], o["grad"], TOL)
+    _cmp(cfg, f["bucket"][:P], u["bucket"][:P], 1e-5)
+    for k in ("policy_loss", "value_loss", "entropy", "clip_fraction", "approx_kl"):
+        assert abs(f["stats"][k] - u["stats"][k]) <= 1e-6 * (1 + abs(u["stats"][k])), k
+    assert f["stats"]["nonfinite"] == 0
+
+
 @pytest.mark.parametrize("name,B", [("atari", 512), ("gfootball", 1024)])
 def test_fused_head_many_tiles_per_cta(name, B):
     """n = 65536 / 204800 rows: 512 / 1600 tiles over <= 148 CTAs, so dW_h^T accumulates in
