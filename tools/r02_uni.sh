@@ -1,0 +1,15 @@
+# uniform-register MMA operands: GEMM/head tests, then A/B bench + ncu tensor activity
+python -m paper_2306_16688_b200.build > gpurun_out/build.log 2>&1
+timeout 1500 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_ppo.py tests/test_gpu_head_fused.py tests/test_gpu_ac.py -q -x -p no:cacheprovider 2>&1 | tail -1
+for i in 1 2; do
+for lib in paper_2306_16688_b200/libsrl.so variants/nouni/libsrl.so; do
+  SRL_LIB=$lib timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-all-configs > gpurun_out/ab.json 2> gpurun_out/ab.err
+  python - $lib <<'PY'
+import json, sys
+d = json.loads(open("gpurun_out/ab.json").read().strip().splitlines()[-1])
+print(sys.argv[1].split("/")[-2], "value", round(d["value"] / 1e6, 1), "ms", round(d["ms_per_step"], 4), " ".join(f'{k["name"]}={k["ms_per_step"]*1e3:.1f}' for k in d["kernels"]))
+PY
+done; done
+for lib in paper_2306_16688_b200/libsrl.so variants/nouni/libsrl.so; do
+SRL_LIB=$lib ncu --clock-control none -k regex:"gemm_tc|head_fused" -s 7 -c 6 --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed python tools/kernel_probe.py step atari 2 2>&1 | grep -E "gemm_tc_kernel|head_fused_kernel|gpu__time|tensor" | sed 's/(CUtensorMap.*//'
+done
