@@ -70,7 +70,7 @@ __device__ void warp0_merge_parts(const double* part, int count, double* out, do
 
 // Chunked reverse scan with register-resident chunks.  A block owns 32 consecutive env columns
 // (one per lane) and W warps; warp w owns the 16-row chunk [16 w, 16 w + 16) of every
-// super-chunk of 16 W rows (one super-chunk whenever T <= 512, every BASELINE config).  The
+// super-chunk of 16 W rows (T > 16 W loops over super-chunks, carrying A between them).  The
 // recurrence A_t = delta_t + c_t A_{t+1} (c_t = gamma lambda m_t) is affine, so
 //   load:   every warp loads its 16 rows once (r, v, d and v of the row after) -> delta, c;
 //   pass 1: chunk summary with A = 0 after it: (a, P = prod c), published in shared memory;
@@ -85,8 +85,14 @@ struct GaeMoments {          // shifted sums of this thread's advantages (no div
   int n = 0;
 };
 
+// warps per block (-DSRL_GAE_MAX_WARPS for the A/B): ncu per launch, atari / smac / hns /
+// gfootball, 32 warps 10.2 / 61.0 / 32.4 / 12.2 us (64 registers: spills), 16 warps 6.9 / 53.5
+// / 37.4 / 8.5, 8 warps 6.8 / 42.4 / 32.1 / 9.4 (no spills, two blocks per SM)
+#ifndef SRL_GAE_MAX_WARPS
+#define SRL_GAE_MAX_WARPS 8
+#endif
 template <bool TV, bool VM>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(32 * SRL_GAE_MAX_WARPS)
 gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __restrict__ v,
            const uint8_t* __restrict__ d, const float* __restrict__ tv,
            const uint8_t* __restrict__ vmask, float gamma, float gl, float* __restrict__ adv,
@@ -224,12 +230,14 @@ gae_kernel(int T, int B, int ld, const float* __restrict__ r, const float* __res
   if (threadIdx.x == 0) *counter = 0;   // ready for the next launch
 }
 
-// one block per 32 columns; one warp per 16-row chunk (at most 32 warps: T > 512 loops over
-// super-chunks of 512 rows)
+// one block per 32 columns; one warp per 16-row chunk (at most SRL_GAE_MAX_WARPS warps; longer
+// T loops over super-chunks)
 int gae_num_blocks(int B) { return (B + 31) / 32; }
 static int gae_segments(int T, int B) {
   (void)B;
-  return std::max(1, std::min(32, (T + kTC - 1) / kTC));
+  // at most SRL_GAE_MAX_WARPS warps: the register-resident chunks need ~115 registers per
+  // thread, which a 1024-thread bound (64 registers) spilled; longer T loops over super-chunks
+  return std::max(1, std::min(SRL_GAE_MAX_WARPS, (T + kTC - 1) / kTC));
 }
 
 cudaError_t launch_gae(int T, int B, int ld, const float* r, const float* v, const uint8_t* d,
