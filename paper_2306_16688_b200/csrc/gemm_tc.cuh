@@ -476,7 +476,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 // split order -- deterministic -- while they are still in L2, scaled by 1/N and stored into
 // the bucket; the partial lines are then discarded from L2 (never written back to HBM).
 // Warp-strided over float4 quads (N % 4 == 0), 8 split loads in flight per lane.
-static __device__ __noinline__ void part_fixup(const GemmArgs& a) {
+__device__ __forceinline__ void part_fixup(const GemmArgs& a) {
   grid_barrier(a.red_bar);
   const uint32_t lane = lane_id();
   const int S = a.k_splits;
