@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(256) merge_moments_kernel(const double* __rest
 // merge_parts_block as the NCCL path (identical result on every rank and on both paths).
 // phases bit 0: publish this rank's triple; bit 1: wait for every rank's and merge.  A wait
 // past the timeout raises the CommCtl error words and leaves mean_std as it was.
-__global__ void __launch_bounds__(256) p2p_moments_kernel(const P2PPeers pe, int world, int rank,
+__global__ void __launch_bounds__(256) p2p_moments_kernel(const __grid_constant__ P2PPeers pe, int world, int rank,
                                                           unsigned long long epoch,
                                                           const double* __restrict__ local,
                                                           double* mean_std, int unbiased,

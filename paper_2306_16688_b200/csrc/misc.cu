@@ -388,7 +388,7 @@ cudaError_t launch_adam(const SegTable& t, int64_t P, float* p, float* m, float*
 __device__ void write_stats(const float* ex, const double* mean_std, int64_t n_global, float cv,
                             float ce, int64_t* t_dev, int apply, srl_ppo_stats* out,
                             unsigned long long* counters, const double* gnorm, int cerr);
-__device__ bool p2p_exchange_body(const P2PPeers& pe, int world, int rank, int64_t off,
+__device__ __forceinline__ bool p2p_exchange_body(const P2PPeers& pe, int world, int rank, int64_t off,
                                   int64_t count, unsigned long long epoch, float scale,
                                   float* __restrict__ out, const CommCtl& cc, int phases,
                                   bool publish);
@@ -638,7 +638,7 @@ __device__ __forceinline__ void sum_range(const P2PPeers& pe, int world, int64_t
 // The two phases for block g of G; `publish` = block 0 also publishes this rank's bucket
 // (the standalone kernel; the fused update launch publishes after its extras).  Returns false
 // after a comm timeout (the error words are raised; the caller skips the rest, no early exit).
-__device__ bool p2p_exchange_body(const P2PPeers& pe, int world, int rank, int64_t off,
+__device__ __forceinline__ bool p2p_exchange_body(const P2PPeers& pe, int world, int rank, int64_t off,
                                   int64_t count, unsigned long long epoch, float scale,
                                   float* __restrict__ out, const CommCtl& cc, int phases,
                                   bool publish) {
@@ -682,7 +682,7 @@ __device__ bool p2p_exchange_body(const P2PPeers& pe, int world, int rank, int64
   return true;
 }
 
-__global__ void __launch_bounds__(512) p2p_allreduce_kernel(const P2PPeers pe, int world, int rank,
+__global__ void __launch_bounds__(512) p2p_allreduce_kernel(const __grid_constant__ P2PPeers pe, int world, int rank,
                                                             int64_t off, int64_t count,
                                                             unsigned long long epoch, float scale,
                                                             float* __restrict__ out,
