@@ -248,7 +248,9 @@ srl_status srl_ppo_train_step_slot(srl_ctx* ctx, int slot, int64_t n_global,
 /* How srl_ppo_step reduces the gradient bucket across ranks (a6): 0 = world 1 (none),
  * 1 = NCCL allreduce, 2 = two-shot allreduce over NVLink peer memory (CUDA IPC-mapped buckets:
  * each rank sums its 1/world chunk of all ranks' buckets in rank order, then gathers the other
- * chunks; the default when every rank could map every peer; SRL_P2P_AR=0 selects NCCL).
+ * chunks; the default when every rank could map every peer; SRL_P2P_AR=0 selects NCCL).  On
+ * the peer path the exchange runs inside the step's update launch, between the split-K
+ * finalise and Adam (SRL_XFUSED=0: as its own launch; bit-identical results).
  * -1 on a null ctx. */
 int srl_ppo_comm_path(srl_ctx* ctx);
 
