@@ -566,17 +566,19 @@ head_fused_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant
     // head segment; the finalise sums the CTAs in index order)
     wait_bounded(dwdone, 0);
     tc_fence_after();
-    // only the first 32 of the 64 accumulator columns: g has A + 1 <= 32 real columns, the
-    // finalise reads no others (half the partial bytes of the full 64-column row)
+    // only the quads of the A + 1 <= 32 real columns of g (the finalise reads no others; the
+    // 64-column row is allocated)
     for (int c = grp; c < NP; c += 2) {
       float v[32];
       const int fr = 128 * c + quad * 32 + (int)lane;   // feature row of dW^T
       float* dst = args.part + (int64_t)blockIdx.x * args.part_split_stride + (int64_t)fr * args.ld_part;
       tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + 64 * c, v);
       tc_wait_ld();
+      const int nq = (args.A + 1 + 3) >> 2;          // the quads the finalise reads
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if (q < nq)
+          reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
   }
 #ifdef SRL_HF_TRACE
