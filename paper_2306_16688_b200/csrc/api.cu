@@ -361,7 +361,10 @@ static void free_ctx(srl_ctx* c) {
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->err_pinned) cudaFreeHost(c->err_pinned);
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm) {
+    if (c->failed) ncclCommAbort(c->comm);   // a failed exchange: do not wait on any peer
+    else ncclCommDestroy(c->comm);
+  }
   for (void* p : c->allocs) cudaFree(p);
   delete c;
 }

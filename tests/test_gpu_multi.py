@@ -212,3 +212,72 @@ def test_allreduce_grads_and_adv_norm_api(world, p2p):
     for r in res:
         assert np.array_equal(r[1]["ms"][0], ms)
     assert abs(ms[0] - mu) <= 1e-12 * sd and abs(ms[1] - sd) <= 1e-12 * sd
+
+
+def _timeout_worker(rank, world, port, q):
+    """Rank 1 creates its context but never steps: rank 0's exchange waits time out after
+    SRL_COMM_TIMEOUT_S; the step reports comm_error with Adam skipped, the next call fails."""
+    import sys
+    import time
+    os.environ["SRL_COMM_TIMEOUT_S"] = "2"
+    os.environ["SRL_P2P_AR"] = "1"
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        import synth
+        import paper_2306_16688_b200 as P
+        from paper_2306_16688_b200.dist import broadcast_unique_id
+        from ppo_harness import make_inputs, to_dev
+        cfg = synth.get_config("gfootball").with_(B=16)
+        params, sh = make_inputs(cfg, seed=3, world=world, rank=rank)
+        uid = broadcast_unique_id(device=torch.device("cuda", rank))
+        ctx = P.PPOContext(P.NetSpec.from_config(cfg), max_local_n=sh["n"], rank=rank, world=world,
+                           nccl_id=uid, device=rank)
+        ctx.load_params(torch.from_numpy(params).cuda())
+        torch.cuda.synchronize()
+        out = None
+        if rank == 0:
+            d = to_dev(sh)
+            t0 = time.time()
+            st = P.decode_stats(ctx.train_step(cfg.N, d["rewards"], d["values"], d["dones"],
+                                               d["obs"], d["actions"], d["logp_old"]))
+            waited = time.time() - t0
+            try:
+                ctx.train_step(cfg.N, d["rewards"], d["values"], d["dones"], d["obs"],
+                               d["actions"], d["logp_old"])
+                err = ""
+            except P.SrlError as e:
+                err = str(e)
+            out = (st["comm_error"], st["step"], waited, err, ctx.comm_path)
+        q.put((rank, out))
+        dist.barrier()
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_comm_timeout_reports_enccl():
+    """SPEC.md S:L532 ReduceTimeout as SRL_ENCCL: a missing peer makes the
+    peer-path waits give up after SRL_COMM_TIMEOUT_S instead of hanging or trapping."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _port()
+    procs = [mpc.Process(target=_timeout_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in range(2)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    comm_error, step, waited, err, path = res[0][1]
+    assert path == "nvlink-p2p"
+    assert comm_error == 1 and step == 0                 # Adam skipped
+    assert 1.5 <= waited <= 60.0
+    assert "status 3" in err                             # SRL_ENCCL on the next call
