@@ -301,25 +301,44 @@ __device__ __forceinline__ void ppo_row_regs(const GemmArgs& a, float (&z)[32], 
                                              float Ahat, float lp_old, float R, float vo,
                                              bool rvalid, double (&st)[5], uint32_t& nonfinite) {
   const int A = a.A;
+  // the columns in 8-wide chunks; chunks past the value column are skipped by a warp-uniform
+  // branch (A + 1 = 19 for Atari: 3 of 4 chunks), the same operations in the same order
+  const int nch = (A + 1 + 7) >> 3;
   float V = 0.f, mx = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    if (j < A) mx = fmaxf(mx, z[j]);
-    if (j == A) V = z[j];                        // the value column (not a logit)
-  }
+  for (int c8 = 0; c8 < 4; ++c8)
+    if (c8 < nch) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = 8 * c8 + i;
+        if (j < A) mx = fmaxf(mx, z[j]);
+        if (j == A) V = z[j];                    // the value column (not a logit)
+      }
+    }
   float se = 0.f;
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j < A) se += __expf(z[j] - mx);
+  for (int c8 = 0; c8 < 4; ++c8)
+    if (c8 < nch) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = 8 * c8 + i;
+        if (j < A) se += __expf(z[j] - mx);
+      }
+    }
   const float lse = mx + __logf(se);
   float ent = 0.f, logpi = 0.f;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float l = z[j] - lse;                  // log-softmax
-    if (j < A) ent -= __expf(l) * l;             // entropy
-    z[j] = l;
-    if (j == act) logpi = l;
-  }
+  for (int c8 = 0; c8 < 4; ++c8)
+    if (c8 < nch) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = 8 * c8 + i;
+        const float l = z[j] - lse;              // log-softmax
+        if (j < A) ent -= __expf(l) * l;         // entropy
+        z[j] = l;
+        if (j == act) logpi = l;
+      }
+    }
   const float rho = expf(logpi - lp_old);
   const float lo = 1.f - a.clip_eps, hi = 1.f + a.clip_eps;
   const float rc = fminf(fmaxf(rho, lo), hi);
@@ -340,12 +359,21 @@ __device__ __forceinline__ void ppo_row_regs(const GemmArgs& a, float (&z)[32], 
   const float li = lpg + a.value_coef * lv - a.entropy_coef * ent;
   const bool ok = rvalid && isfinite(li);
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float l = z[j];
-    const float p = __expf(l);
-    const float g = pol * ((j == act ? 1.f : 0.f) - p) + a.entropy_coef * p * (l + ent);
-    z[j] = (ok && j < A) ? g : 0.f;
-    if (j == A) z[j] = ok ? a.value_coef * gv : 0.f;
+  for (int c8 = 0; c8 < 4; ++c8) {
+    if (c8 < nch) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = 8 * c8 + i;
+        const float l = z[j];
+        const float p = __expf(l);
+        const float g = pol * ((j == act ? 1.f : 0.f) - p) + a.entropy_coef * p * (l + ent);
+        z[j] = (ok && j < A) ? g : 0.f;
+        if (j == A) z[j] = ok ? a.value_coef * gv : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) z[8 * c8 + i] = 0.f;
+    }
   }
   if (!rvalid) return;
   if (!ok) {
